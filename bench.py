@@ -1,0 +1,364 @@
+#!/usr/bin/env python3
+"""Benchmark of the all-to-all spectral connectivity path (BASELINE.json metric:
+edge*freq*trial updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+A step = one pass of the hot path over one batch: K1 (demean + taper + DFT of
+every node x trial) and the fused pair kernels (all 7 metrics, per-bin and
+band-averaged outputs) for the configured workload.  Default workload: config 5
+(N=10242, K=100, T=1000, Hann, 6 bins), the config BASELINE.json scales over
+1/2/4/8 GPUs.  Inputs (4.1 GB) exceed the 126 MB L2, so no explicit flush.
+
+N > 1 (torchrun): rank r owns node block r for K1, the fp32/fp64 spectrum ring
+is all-gathered over NCCL (the path's one exchange step), then rank r computes
+the pair row-tiles of its balanced shard (strong scaling; results stay
+sharded).  Timing: CUDA events on the launching stream, barrier + synchronize
+on both sides, max over ranks.
+
+--impl reference times the reference's CPU path (the oracle port of
+connstream, oracle/) on a bounded node subset of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch.distributed as dist
+        lr = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        return dist, dist.get_rank(), ws, lr
+    torch.cuda.set_device(0)
+    return None, 0, 1, 0
+
+
+def cpu_baseline(c, n_sub: int, threads: int):
+    """The reference's CPU path (oracle port, oracle/) on a node subset of the
+    workload: per-trial spectra through a thread pool (as compute_metric does,
+    metrics.py:542-547) and the single-threaded fold + 7 finalizers."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2303_03279_b200 import synth
+    from paper_2303_03279_b200.plan import make_taper
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x = synth.generate(c, dev, nodes=slice(0, n_sub)).double().cpu().numpy()
+    tap = make_taper(c.taper, min(c.T, c.nfft))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        if tap is not None and tap.shape[0] > 1:
+            specs = list(pool.map(lambda e: np.stack([O.trial_spectra(e, c.nfft, tp)[:, c.lo:c.hi + 1]
+                                                      for tp in tap]), x))
+        else:
+            tp = None if tap is None else tap[0]
+            specs = list(pool.map(lambda e: O.trial_spectra(e, c.nfft, tp)[:, c.lo:c.hi + 1], x))
+    t1 = time.perf_counter()
+    acc = O.Sums(n_sub, c.n_bins)
+    for s in specs:
+        if s.ndim == 3:
+            O.accumulate_multitaper(acc, s)
+        else:
+            O.accumulate(acc, s)
+    t2 = time.perf_counter()
+    for m in c.metrics:
+        O.band_reduce(m, O.BINS[m](acc))
+    t3 = time.perf_counter()
+    upd = n_sub * (n_sub - 1) // 2 * c.n_bins * c.K
+    return {"updates": upd, "s": t3 - t0, "fft_s": t1 - t0, "fold_s": t2 - t1, "finalize_s": t3 - t2}
+
+
+def run_reference(args, c, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sub = args.cpu_nodes
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(c, n_sub, threads)
+        if i >= args.warmup:
+            samples.append(r)
+    s = statistics.mean(r["s"] for r in samples)
+    val = samples[0]["updates"] / s
+    line = {
+        "impl": "reference", "metric": f"edge*freq*trial updates/s (config {c.cfg}, 7 metrics)", "value": val,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded; SURVEY.md 8(d) signal model)",
+        "config": {"workload": f"cfg{c.cfg}: {c.name}", "sample_nodes": n_sub},
+        "cpu_baseline": {"value": val, "unit": "updates/s", "cores": threads, "kind": "port",
+                         "sample": f"node subset N'={n_sub} of cfg{c.cfg} (all K={c.K} trials, {c.n_bins} bins); "
+                                   "FFT in a thread pool, fold single-threaded as in the reference",
+                         "breakdown_s": {k: statistics.mean(r[k] for r in samples) for k in ("fft_s", "fold_s", "finalize_s")}},
+        "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--metrics", default=None, help="comma list (default: the config's metrics)")
+    ap.add_argument("--cpu-nodes", type=int, default=384, help="node subset for the CPU baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    from paper_2303_03279_b200 import synth
+    c = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, c, rank)
+        return
+
+    from paper_2303_03279_b200.plan import DevicePlan, pow2_scale, probe_peaks, row_tile_range
+    dist, rank, ws, lr = dist_setup()
+    dev = torch.device("cuda", lr)
+    metrics = tuple(args.metrics.split(",")) if args.metrics else c.metrics
+
+    # ---- node block for K1, pair shard for the pair kernels ----
+    nloc = (c.N + ws - 1) // ws
+    n0, n1 = min(rank * nloc, c.N), min((rank + 1) * nloc, c.N)
+    (rb, re), (p0, p1) = row_tile_range(c.N, ws, rank)
+    x = synth.generate(c, dev, nodes=slice(n0, n1))
+    if x.shape[1] < nloc:  # pad the last block so every rank gathers the same size
+        x = torch.cat([x, torch.zeros((c.K, nloc - x.shape[1], c.T), dtype=x.dtype, device=dev)], 1)
+    amax = x.abs().amax()
+    if dist is not None:
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+    scale = pow2_scale(float(amax), min(c.T, c.nfft))
+    full = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=c.K, device=dev, scale=scale)
+    local = full if ws == 1 else DevicePlan(nloc, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=c.K,
+                                            device=dev, scale=scale)
+    slots = torch.arange(c.K, dtype=torch.int32, device=dev)
+    outs = full.alloc_outputs(metrics, c.n_bins, per_bin=True, band=True, pair_count=p1 - p0)
+    if ws > 1:
+        L64, L32 = local.ring()
+        F64, F32 = full.ring()
+        g64 = torch.empty((ws,) + tuple(L64.shape), dtype=L64.dtype, device=dev)
+        g32 = torch.empty((ws,) + tuple(L32.shape), dtype=L32.dtype, device=dev)
+
+    def step():
+        local.spectra(x, 0)
+        if ws > 1:  # the exchange step: all-gather node-block spectra over NVLink
+            dist.all_gather_into_tensor(g32.view(-1), L32.reshape(-1))
+            dist.all_gather_into_tensor(g64.view(-1), L64.reshape(-1))
+            F32.copy_(g32.permute(1, 2, 3, 0, 4).reshape(F32.shape[:3] + (ws * nloc,))[..., :c.N])
+            F64.copy_(g64.permute(1, 2, 3, 0, 4).reshape(F64.shape[:3] + (ws * nloc,))[..., :c.N])
+        full.pair_metrics(slots, metrics, 0, c.n_bins, outputs=outs, row_tiles=(rb, re), pair_base=p0,
+                          pair_count=p1 - p0)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n_fallback = full.fallback_count()
+    full.set_profiling(True)
+    if local is not full:
+        local.set_profiling(True)
+    full.profile()
+    launches0 = full.launch_count() + (local.launch_count() if local is not full else 0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(lr) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    prof = full.profile()
+    if local is not full:
+        prof.update({("local_" + k): v for k, v in local.profile().items()})
+    launches = full.launch_count() + (local.launch_count() if local is not full else 0) - launches0
+    ms_t = torch.tensor([ms], device=dev)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t)
+    ms_step = ms_max / args.steps
+    value = c.updates / (ms_step * 1e-3)
+
+    # ---- roofline of the dominant kernel ----
+    peaks, peak_kind = _peaks()
+    fp32_ops, fp64_fma = probe_peaks(lr)
+    per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}  # ms per launch
+    dom = max(per, key=per.get)
+    lag_ms = per.get("pairs_lag", 0.0)
+    roof = None
+    if dom.endswith("pairs_lag"):
+        # algorithmic FP32-pipe work: t = FMUL+FFMA (2), sum t (1), sum |t| (1) lane-ops per update
+        P_loc = p1 - p0
+        upd = P_loc * c.n_bins * c.K
+        ach = 4.0 * upd / (lag_ms * 1e-3)
+        roof = {"kernel": "k_pairs_lag", "bound": "fp32", "achieved": ach / 1e12, "peak": fp32_ops / 1e12,
+                "unit": "T FP32-pipe lane-ops/s", "frac": ach / fp32_ops, "traffic": None,
+                "peak_source": "measured live on this GPU by cs_probe_peaks (dependent FFMA chains)",
+                "work_per_update": "4 FP32 lane-ops (FMUL+FFMA for Im, FADD sum Im, FADD sum |Im|)"}
+    elif dom.endswith("spectra"):
+        k1_ms = per[dom]
+        flop_dfma = c.K * nloc * min(c.T, c.nfft) * c.n_bins * 2 * (1 if not isinstance(c.taper, tuple) else c.taper[2])
+        bytes_ = c.K * nloc * c.T * x.element_size() + c.K * nloc * c.n_bins * 24
+        roof = {"kernel": "k_spectra", "bound": "fp64", "achieved": flop_dfma / (k1_ms * 1e-3) / 1e12,
+                "peak": fp64_fma / 1e12, "unit": "T DFMA/s", "frac": flop_dfma / (k1_ms * 1e-3) / fp64_fma,
+                "traffic": None, "hbm_frac": bytes_ / (k1_ms * 1e-3) / (peaks["hbm_gbs"] * 1e9)}
+    breakdown = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in prof.items()}
+
+    line = {
+        "metric": f"edge*freq*trial updates/s (config {c.cfg}, {len(metrics)} metrics fused)",
+        "value": value, "unit": "updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded; SURVEY.md 8(d) signal model, no public dataset)",
+        "config": {"workload": f"cfg{c.cfg}: {c.name}", "N": c.N, "K": c.K, "T": c.T, "nfft": c.nfft,
+                   "bins": [c.lo, c.hi], "taper": str(c.taper), "metrics": list(metrics),
+                   "outputs": "per-bin [nb,P] + band-mean [P] per metric", "parallelism": f"pair-row-tiles x{ws}",
+                   "l2": "inputs 4.1 GB > 126 MB L2 (no flush needed)" if c.cfg == 5 else "inputs > L2" ,
+                   "updates_per_step": c.updates},
+        "roofline": roof, "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma, "hbm_gbs": peaks["hbm_gbs"],
+                  "hbm_source": peak_kind},
+    }
+
+    # ---- e2e through the public API with host buffers ----
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        hb = {m: torch.empty(p1 - p0, dtype=torch.float32).pin_memory() for m in metrics}
+        xd = torch.empty_like(x)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            local.spectra(xd, 0)
+            if ws > 1:
+                dist.all_gather_into_tensor(g32.view(-1), L32.reshape(-1))
+                dist.all_gather_into_tensor(g64.view(-1), L64.reshape(-1))
+                F32.copy_(g32.permute(1, 2, 3, 0, 4).reshape(F32.shape[:3] + (ws * nloc,))[..., :c.N])
+                F64.copy_(g64.permute(1, 2, 3, 0, 4).reshape(F64.shape[:3] + (ws * nloc,))[..., :c.N])
+            o = full.pair_metrics(slots, metrics, 0, c.n_bins, per_bin=False, band=True, row_tiles=(rb, re),
+                                  pair_base=p0, pair_count=p1 - p0)
+            for m in metrics:
+                hb[m].copy_(o[m]["band"], non_blocking=True)
+        e2e_step()
+        barrier()
+        full.set_profiling(False)
+        local.set_profiling(False)
+        barrier()
+        e0.record()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], device=dev)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": c.updates / (float(t) * 1e-3), "unit": "updates/s",
+                       "h2d_bytes_per_step": xh.numel() * xh.element_size() * ws,
+                       "d2h_bytes_per_step": sum(v.numel() * 4 for v in hb.values()) * ws,
+                       "ms_per_step": float(t), "path": "pinned host samples -> H2D -> K1 -> pair kernels -> band means D2H"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = cpu_baseline(c, args.cpu_nodes, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": r["updates"] / r["s"], "unit": "updates/s", "cores": 1, "kind": "port",
+                                "sample": f"node subset N'={args.cpu_nodes} of cfg{c.cfg}, all K={c.K}, {c.n_bins} bins, "
+                                          f"{len(c.metrics)} finalizers; fold single-threaded as in the reference "
+                                          f"(FFT pool of {os.cpu_count()} threads)",
+                                "breakdown_s": {k: r[k] for k in ("fft_s", "fold_s", "finalize_s")}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

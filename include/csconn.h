@@ -1,0 +1,165 @@
+/*
+ * csconn.h -- C ABI of the B200-native all-to-all spectral connectivity path.
+ *
+ * Drop-in boundary for the reference package `connstream` (arXiv 2303.03279
+ * restated in Python; /root/reference/pkg/src/connstream).  The reference has
+ * no FFI: its "operator API" is the Python namespace (src/__init__.py:3-15).
+ * The Python shim `paper_2303_03279_b200` keeps those names and calls this
+ * library through ctypes with raw device pointers.
+ *
+ * Entry point  <->  reference interface it replaces
+ *   cs_plan_create / cs_plan_destroy
+ *        SpectrumSet(n_channels, nfft) allocation      spectral.py:125-154
+ *        TrialCache (storage mode spectrum cache)       metrics.py:267-282
+ *   cs_spectra
+ *        trial_spectra / fft_real (+ taper extension)  spectral.py:49-97
+ *   cs_pair_metrics
+ *        accumulate_spectra + _fold_csd                 spectral.py:204-261
+ *        *_bins finalizers                              metrics.py:32-98
+ *        finalize_spectral band average                 metrics.py:115-134,
+ *                                                       core.py:208-215
+ *   cs_pair_sums
+ *        SpectrumSet running sums (csd/plv/pli/abs_im)  spectral.py:125-201
+ *   cs_row_tile_range / cs_pair_range
+ *        pair_index / pair_row_slice (triu row-major)   spectral.py:114-122
+ *   cs_last_error
+ *        ParameterError / DegenerateTrialCountError     core.py:17-22
+ *
+ * Conventions: pair p <-> (i<j), row-major upper
+ * triangle; per-bin outputs are bin-major [n_bins][pair_stride] fp32 (the
+ * reference's [P, nb] is the transposed view); band outputs are [pair_stride].
+ * All calls are asynchronous on the caller's cudaStream_t; a plan is
+ * single-owner (not thread safe), mirroring spectral.py:250-251.
+ */
+#ifndef CSCONN_H
+#define CSCONN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the Python shim maps them to the reference's exceptions) */
+#define CS_OK 0
+#define CS_EPARAM 1      /* ParameterError                         */
+#define CS_EDEGENERATE 2 /* DegenerateTrialCountError              */
+#define CS_ECUDA 3       /* CUDA runtime / launch failure          */
+#define CS_ENOMEM 4      /* device allocation failed               */
+
+/* input sample types for cs_spectra */
+#define CS_F32 0
+#define CS_F64 1
+
+/* metric bits (MetricId order of core.py:25-35, spectral metrics only) */
+#define CS_COHY (1u << 0)
+#define CS_COH (1u << 1)
+#define CS_IMAGCOHY (1u << 2)
+#define CS_PLV (1u << 3)
+#define CS_PLI (1u << 4)
+#define CS_USPLI (1u << 5)
+#define CS_WPLI (1u << 6)
+#define CS_DSWPLI (1u << 7)
+#define CS_NUM_METRICS 8
+
+typedef struct cs_plan cs_plan;
+
+/* Output descriptor for cs_pair_metrics.  bins[m]: [nbb][pair_stride] fp32
+ * (COHY: complex64 interleaved, [nbb][pair_stride][2]); band[m]: [pair_stride]
+ * fp32 band mean (COHY: complex64 mean, the weight is its modulus).  NULL
+ * pointers are not written.  Output element for global pair p lives at
+ * index (p - pair_base). */
+typedef struct cs_outputs {
+  void* bins[CS_NUM_METRICS];
+  void* band[CS_NUM_METRICS];
+  int64_t pair_base;
+  int64_t pair_stride;
+} cs_outputs;
+
+/* Running sums (SpectrumSet layout of spectral.py:136-141, restricted to the
+ * requested bins, bin-major [nbb][pair_stride]).  Any pointer may be NULL. */
+typedef struct cs_sums {
+  float* csd;      /* complex64 [nbb][pair_stride][2] */
+  float* plv;      /* complex64 [nbb][pair_stride][2] */
+  int32_t* pli;    /* integer-valued sign sums        */
+  float* abs_im;   /* sum |Im CSD|                    */
+  float* psd;      /* [nbb][n_nodes]                  */
+  int64_t pair_base;
+  int64_t pair_stride;
+} cs_sums;
+
+/*
+ * Create a plan for n_nodes channels, trials of n_samples samples, FFT length
+ * nfft and the inclusive bin range [lo_bin, hi_bin] kept in the HBM spectrum
+ * cache.  tapers: host fp64 [n_tapers][min(n_samples, nfft)] or NULL for the
+ * reference's rectangular window (n_tapers must then be 1).  slot_capacity:
+ * number of trial slots in the spectrum ring.  spectrum_scale: power of two
+ * applied to the fp32 copy of the spectra (0 -> 1.0); every metric is
+ * invariant to it.
+ */
+int cs_plan_create(cs_plan** plan, int device, int n_nodes, int n_samples, int nfft,
+                   int lo_bin, int hi_bin, int n_tapers, const double* tapers,
+                   int slot_capacity, double spectrum_scale, unsigned flags);
+int cs_plan_destroy(cs_plan* plan);
+
+/* K1: demean + taper + one-sided DFT of k_count trials x n_nodes channels.
+ * x_dev: device samples, element (k, n, t) at x[k*trial_stride + n*node_stride + t].
+ * Trial k lands in slot (slot0 + k) mod slot_capacity.  Increments the plan's
+ * FFT counter by k_count*n_nodes*n_tapers (spectral.py:18-30). */
+int cs_spectra(cs_plan* plan, const void* x_dev, int dtype, int64_t trial_stride,
+               int64_t node_stride, int slot0, int k_count, void* stream);
+
+/* Fused pair kernels over the trials in slots_dev[0..n_slots) and the plan-local
+ * bins [bin_lo, bin_lo + n_bins): metric finalisation in the epilogue, per-bin
+ * and band-mean outputs.  Row tiles [row_tile_begin, row_tile_end) of the
+ * upper-triangular 64-node tiling are computed (0, -1 = all). */
+int cs_pair_metrics(cs_plan* plan, const int* slots_dev, int n_slots, unsigned metric_mask,
+                    int bin_lo, int n_bins, int row_tile_begin, int row_tile_end,
+                    const cs_outputs* out, void* stream);
+
+/* SpectrumSet-compatible running sums over the same trial / bin selection. */
+int cs_pair_sums(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo, int n_bins,
+                 const cs_sums* out, void* stream);
+
+/* Copy spectra of n_slots slots (plan-local bins [bin_lo, bin_lo+n_bins), taper 0)
+ * as complex128 [n_slots][n_nodes][n_bins] into dst_dev (trial_spectra layout). */
+int cs_get_spectra(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo, int n_bins,
+                   void* dst_dev, void* stream);
+
+/* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
+ * range of shard `shard` of `n_shards` (balanced by tile count) and the
+ * contiguous global pair range [pair_begin, pair_end) it covers. */
+int cs_num_row_tiles(int n_nodes);
+int cs_row_tile_range(int n_nodes, int n_shards, int shard, int* row_tile_begin,
+                      int* row_tile_end, int64_t* pair_begin, int64_t* pair_end);
+
+/* Fallback bookkeeping of the last cs_pair_metrics call (device -> host copy;
+ * synchronises the stream).  n_flagged: (pair, bin) entries recomputed in fp64. */
+int cs_last_fallback_count(cs_plan* plan, void* stream, int64_t* n_flagged);
+int64_t cs_fft_call_count(const cs_plan* plan);
+void cs_reset_fft_call_count(cs_plan* plan);
+
+/* Instrumentation (bench evidence): CUDA events around every kernel phase on
+ * the launching stream; cs_profile_read returns "name:total_ms:count;..." and
+ * clears the records.  cs_launch_count: kernels launched by the plan so far. */
+int cs_plan_set_profiling(cs_plan* plan, int on);
+int cs_profile_read(cs_plan* plan, char* buf, int len);
+int64_t cs_launch_count(const cs_plan* plan);
+
+/* Device pointers of the spectrum ring (fp64 and fp32 copies, [slot][L][nb][N]
+ * complex) and its element count: used to all-gather node blocks across GPUs. */
+int cs_ring_view(cs_plan* plan, void** x64, void** x32, int64_t* n_elems);
+
+/* Measure this device's FP32 FMA-pipe lane-op rate and FP64 DFMA rate (a few
+ * ms of dependent-chain FMA loops; the roofline denominators for K3 and K1). */
+int cs_probe_peaks(int device, double* fp32_lane_ops_per_s, double* fp64_fma_per_s);
+
+/* Thread-local message of the last failing call. */
+const char* cs_last_error(void);
+const char* cs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSCONN_H */

@@ -68,9 +68,26 @@ def dpss(n: int, nw: float, k: int) -> np.ndarray:
     return np.atleast_2d(windows.dpss(n, nw, Kmax=k))
 
 
-def trial_spectra(data: np.ndarray, nfft: int, taper: np.ndarray | None = None) -> np.ndarray:
-    """spectral.py:82-97: one-sided spectra [C, nfft//2+1], DC forced to 0."""
-    out = np.fft.rfft(crop_pad_demean(data, nfft, taper), n=nfft, axis=1)
+def trial_spectra(data: np.ndarray, nfft: int, taper: np.ndarray | None = None,
+                  method: str = "fft") -> np.ndarray:
+    """spectral.py:82-97: one-sided spectra [C, nfft//2+1], DC forced to 0.
+
+    ``method="dft"`` evaluates the same transform as a direct O(n^2) DFT (the
+    reference's own test oracle, tests/oracles.py:9-27).  Two fp64 algorithms
+    agreeing is the definition of a *well-conditioned* entry: where they differ
+    by more than the parity tolerance the reference's value is rounding noise
+    (e.g. the Im-flush threshold of spectral.py:227-228 at leakage-level bins).
+    """
+    seg = crop_pad_demean(data, nfft, taper)
+    if method == "fft":
+        out = np.fft.rfft(seg, n=nfft, axis=1)
+    else:
+        nb = nfft // 2 + 1
+        m = np.outer(np.arange(nfft), np.arange(nb)) % nfft
+        tw = np.exp(-2j * np.pi * m / nfft)
+        if nfft % 2 == 0:
+            tw[:, -1] = (-1.0) ** np.arange(nfft)
+        out = seg @ tw
     out[:, 0] = 0.0
     return out
 
@@ -223,7 +240,7 @@ def band_reduce(metric: str, per_bin: np.ndarray):
 # --------------------------------------------------------------------------
 # whole-path driver
 # --------------------------------------------------------------------------
-def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None):
+def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None, method: str = "fft"):
     """All requested metrics for trials ``epochs`` (list/array of [C, T]) over the
     inclusive bin range [lo, hi].
 
@@ -236,10 +253,10 @@ def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None):
     acc = Sums(C, hi - lo + 1)
     for ep in epochs:
         if taper is not None and np.ndim(taper) == 2:
-            spec_l = np.stack([trial_spectra(ep, nfft, tp)[:, lo:hi + 1] for tp in taper])
+            spec_l = np.stack([trial_spectra(ep, nfft, tp, method)[:, lo:hi + 1] for tp in taper])
             accumulate_multitaper(acc, spec_l)
         else:
-            accumulate(acc, trial_spectra(ep, nfft, taper)[:, lo:hi + 1])
+            accumulate(acc, trial_spectra(ep, nfft, taper, method)[:, lo:hi + 1])
     out = {}
     for m in metrics:
         try:
@@ -250,3 +267,38 @@ def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None):
         w, cw = band_reduce(m, pb)
         out[m] = {"bins": pb, "band": w, "cband": cw}
     return out, acc
+
+
+def well_conditioned(epochs, nfft, lo, hi, metrics, tol, taper=None, ref=None):
+    """Per-metric boolean masks [P, nb] of entries on which two independent fp64
+    spectral algorithms (rfft vs direct DFT) agree within tol[m]/2."""
+    a = ref if ref is not None else compute(epochs, nfft, lo, hi, metrics, taper)[0]
+    b = compute(epochs, nfft, lo, hi, metrics, taper, method="dft")[0]
+    out = {}
+    for m in metrics:
+        if a.get(m) is None:
+            continue
+        out[m] = np.abs(a[m]["bins"] - b[m]["bins"]) <= 0.5 * tol[m]
+    return out
+
+
+def flush_sensitive(epochs, nfft, lo, hi, taper=None, lo_ratio=1e-15, hi_ratio=1e-11):
+    """Boolean [P, nb]: (pair, bin) entries where some trial has
+    |Im CSD| / |Re CSD| within two decades of the reference's 1e-13 flush
+    threshold (spectral.py:227-228).  There the reference's sign(Im) is decided
+    by last-ulp rounding of its own spectra, so no other arithmetic (a different
+    FFT, summation order or taper placement) can reproduce it."""
+    epochs = [np.asarray(e, dtype=np.float64) for e in epochs]
+    C = epochs[0].shape[0]
+    out = np.zeros((C * (C - 1) // 2, hi - lo + 1), dtype=bool)
+    for ep in epochs:
+        if taper is not None and np.ndim(taper) == 2:
+            csd = 0
+            for tp in taper:
+                c, _ = trial_csd_psd(trial_spectra(ep, nfft, tp)[:, lo:hi + 1], C)
+                csd = csd + c
+        else:
+            csd, _ = trial_csd_psd(trial_spectra(ep, nfft, taper)[:, lo:hi + 1], C)
+        r = np.abs(csd.imag) / np.maximum(np.abs(csd.real), TINY)
+        out |= (r >= lo_ratio) & (r <= hi_ratio)
+    return out

@@ -1,0 +1,83 @@
+"""ctypes binding of libcsconn.so (include/csconn.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``).  There is
+no CPU fallback: importing the product path on a machine without the built
+library or without a CUDA device raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libcsconn.so"
+
+CS_OK, CS_EPARAM, CS_EDEGENERATE, CS_ECUDA, CS_ENOMEM = 0, 1, 2, 3, 4
+CS_F32, CS_F64 = 0, 1
+NUM_METRICS = 8
+
+
+class CsOutputs(ctypes.Structure):
+    _fields_ = [("bins", ctypes.c_void_p * NUM_METRICS),
+                ("band", ctypes.c_void_p * NUM_METRICS),
+                ("pair_base", ctypes.c_int64),
+                ("pair_stride", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcsconn.so once; raise loudly if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} is not built; run `make` (or __graft_entry__.build())")
+    L = ctypes.CDLL(str(LIB_PATH))
+    vp, i32, i64, u32, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint, ctypes.c_double
+    L.cs_plan_create.argtypes = [ctypes.POINTER(vp), i32, i32, i32, i32, i32, i32, i32,
+                                 ctypes.POINTER(dbl), i32, dbl, u32]
+    L.cs_plan_destroy.argtypes = [vp]
+    L.cs_spectra.argtypes = [vp, vp, i32, i64, i64, i32, i32, vp]
+    L.cs_pair_metrics.argtypes = [vp, vp, i32, u32, i32, i32, i32, i32, ctypes.POINTER(CsOutputs), vp]
+    L.cs_get_spectra.argtypes = [vp, vp, i32, i32, i32, vp, vp]
+    L.cs_num_row_tiles.argtypes = [i32]
+    L.cs_row_tile_range.argtypes = [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                    ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.cs_last_fallback_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
+    L.cs_fft_call_count.argtypes = [vp]
+    L.cs_fft_call_count.restype = i64
+    L.cs_reset_fft_call_count.argtypes = [vp]
+    L.cs_reset_fft_call_count.restype = None
+    L.cs_plan_set_profiling.argtypes = [vp, i32]
+    L.cs_profile_read.argtypes = [vp, ctypes.c_char_p, i32]
+    L.cs_launch_count.argtypes = [vp]
+    L.cs_launch_count.restype = i64
+    L.cs_ring_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.cs_probe_peaks.argtypes = [i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+    L.cs_last_error.restype = ctypes.c_char_p
+    L.cs_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_sums",
+            "cs_get_spectra", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count",
+            "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
+            "cs_launch_count", "cs_ring_view", "cs_probe_peaks", "cs_last_error", "cs_version")
+
+
+def check(status: int) -> None:
+    """Map a csconn status code to the reference's exception classes (core.py:17-22)."""
+    if status == CS_OK:
+        return
+    from .core import DegenerateTrialCountError, ParameterError
+    msg = lib().cs_last_error().decode(errors="replace")
+    if status == CS_EPARAM:
+        raise ParameterError(msg)
+    if status == CS_EDEGENERATE:
+        raise DegenerateTrialCountError(msg)
+    if status == CS_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"csconn CUDA failure: {msg}")

@@ -1,0 +1,368 @@
+// C ABI of csconn (include/csconn.h): plan lifetime, argument validation with
+// the reference's error classes (core.py:17-22), kernel orchestration.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cs {
+void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0, int kc,
+                 cudaStream_t st);
+void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb, cudaStream_t st);
+void run_get_spectra(const Plan& p, const int* slots, int ns, int bin_lo, int nbins, void* dst,
+                     cudaStream_t st);
+struct LagArgs;
+int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                    int rb, int re, const cs_outputs* out, cudaStream_t st);
+int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                    int rb, int re, const cs_outputs* out, cudaStream_t st);
+}  // namespace cs
+
+using cs::Plan;
+
+static thread_local char g_err[512] = "";
+
+void cs_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+struct cs_plan : Plan {};
+
+namespace {
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+struct ProfState {
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+struct PhaseRec {
+  ProfState* ps;
+  cudaStream_t st;
+  ProfRec r;
+};
+}  // namespace
+
+cs::PhaseMark::PhaseMark(Plan& p, const char* name, cudaStream_t st) {
+  p.launches += 1;
+  if (!p.profiling) return;
+  auto* pr = new PhaseRec{(ProfState*)p.prof, st, {}};
+  pr->r.name = name;
+  pr->r.a = pr->ps->get();
+  pr->r.b = pr->ps->get();
+  cudaEventRecord(pr->r.a, st);
+  rec = pr;
+}
+
+cs::PhaseMark::~PhaseMark() {
+  if (!rec) return;
+  auto* pr = (PhaseRec*)rec;
+  cudaEventRecord(pr->r.b, pr->st);
+  pr->ps->recs.push_back(pr->r);
+  delete pr;
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int cuda_fail(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  cs_set_error("%s: %s", what, cudaGetErrorString(e));
+  return CS_ECUDA;
+}
+
+bool is_pow2(double s) {
+  int e;
+  double m = std::frexp(s, &e);
+  return m == 0.5;
+}
+
+// exp(-2 pi i m / n) with exact values on the axes
+void twiddle(long m, long n, double* c, double* s) {
+  m %= n;
+  if (m == 0) { *c = 1.0; *s = 0.0; return; }
+  if (2 * m == n) { *c = -1.0; *s = 0.0; return; }
+  if (4 * m == n) { *c = 0.0; *s = -1.0; return; }
+  if (4 * m == 3 * n) { *c = 0.0; *s = 1.0; return; }
+  const long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)n;
+  *c = (double)cosl(ang);
+  *s = (double)(-sinl(ang));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cs_last_error(void) { return g_err; }
+const char* cs_version(void) { return "csconn 0.1 (sm_100a)"; }
+
+int cs_num_row_tiles(int n_nodes) { return (n_nodes + cs::kTile - 1) / cs::kTile; }
+
+int cs_row_tile_range(int n_nodes, int n_shards, int shard, int* rb, int* re, int64_t* p0,
+                      int64_t* p1) {
+  if (n_nodes < 1 || n_shards < 1 || shard < 0 || shard >= n_shards) {
+    cs_set_error("cs_row_tile_range: bad arguments");
+    return CS_EPARAM;
+  }
+  const int nt = cs_num_row_tiles(n_nodes);
+  // balance by tile count: row I holds nt - I tiles
+  const int64_t total = (int64_t)nt * (nt + 1) / 2;
+  auto row_for = [&](int64_t target) {
+    int64_t acc = 0;
+    int r = 0;
+    while (r < nt && acc + (nt - r) <= target) {
+      acc += nt - r;
+      ++r;
+    }
+    // round to the nearer boundary
+    if (r < nt && target - acc > (acc + (nt - r)) - target) ++r;
+    return r;
+  };
+  const int b = shard == 0 ? 0 : row_for(total * shard / n_shards);
+  const int e = shard == n_shards - 1 ? nt : row_for(total * (shard + 1) / n_shards);
+  *rb = b;
+  *re = e;
+  auto first_pair_of_row = [&](int64_t i) {
+    if (i >= n_nodes) return (int64_t)n_nodes * (n_nodes - 1) / 2;
+    return i * (n_nodes - 1) - i * (i - 1) / 2;
+  };
+  *p0 = first_pair_of_row((int64_t)b * cs::kTile);
+  *p1 = first_pair_of_row((int64_t)e * cs::kTile);
+  return CS_OK;
+}
+
+int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, int hi, int L,
+                   const double* tapers, int slot_cap, double scale, unsigned flags) {
+  (void)flags;
+  if (!out) return CS_EPARAM;
+  *out = nullptr;
+  if (nfft < 2) { cs_set_error("nfft must be >= 2, got %d", nfft); return CS_EPARAM; }
+  if (N < 1) { cs_set_error("need at least one channel"); return CS_EPARAM; }
+  if (T < 1) { cs_set_error("empty signal"); return CS_EPARAM; }
+  const int nbins = nfft / 2 + 1;
+  if (lo < 0 || hi < lo || hi >= nbins) {
+    cs_set_error("invalid band bins [%d, %d] for %d bins", lo, hi, nbins);
+    return CS_EPARAM;
+  }
+  if (L < 1 || (!tapers && L != 1)) { cs_set_error("bad taper count %d", L); return CS_EPARAM; }
+  if (slot_cap < 1) { cs_set_error("slot_capacity must be >= 1"); return CS_EPARAM; }
+  if (scale == 0.0) scale = 1.0;
+  if (!(scale > 0.0) || !is_pow2(scale)) {
+    cs_set_error("spectrum_scale must be a positive power of two");
+    return CS_EPARAM;
+  }
+  DeviceGuard g(device);
+  cs_plan* p = new cs_plan();
+  p->device = device;
+  p->N = N; p->T = T; p->nfft = nfft; p->lo = lo; p->hi = hi; p->nb = hi - lo + 1; p->L = L;
+  p->T_eff = T < nfft ? T : nfft;
+  p->slot_cap = slot_cap;
+  p->scale = (float)scale;
+  p->dc_local = (lo == 0) ? 0 : -1;
+  p->nyq_local = (nfft % 2 == 0 && hi == nfft / 2) ? (nfft / 2 - lo) : -1;
+
+  // taper x twiddle table (host fp64, long double angles)
+  std::vector<double2> tw((size_t)L * p->nb * p->T_eff);
+  for (int l = 0; l < L; ++l)
+    for (int b = 0; b < p->nb; ++b)
+      for (int t = 0; t < p->T_eff; ++t) {
+        double c, s;
+        twiddle((long)(lo + b) * t, nfft, &c, &s);
+        const double w = tapers ? tapers[(size_t)l * p->T_eff + t] : 1.0;
+        tw[((size_t)l * p->nb + b) * p->T_eff + t] = make_double2(w * c, w * s);
+      }
+  const int64_t P = (int64_t)N * (N - 1) / 2;
+  int64_t cap = P * p->nb / 64;
+  if (cap < (1 << 16)) cap = 1 << 16;
+  if (cap > (1 << 24)) cap = 1 << 24;
+  p->flag_cap = (int)cap;
+  const size_t ring = (size_t)slot_cap * L * p->nb * N;
+  bool ok = cudaMalloc(&p->tww, tw.size() * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&p->X64, ring * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&p->X32, ring * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc(&p->psd, (size_t)p->nb * N * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&p->mag, (size_t)p->nb * N * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&p->flags, (size_t)p->flag_cap * sizeof(int4)) == cudaSuccess &&
+            cudaMalloc(&p->counters, 4 * sizeof(int)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cs_set_error("device allocation failed (spectrum ring %zu bytes)", ring * 24);
+    cs_plan_destroy(p);
+    return CS_ENOMEM;
+  }
+  cudaMemcpy(p->tww, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemset(p->X64, 0, ring * sizeof(double2));
+  cudaMemset(p->X32, 0, ring * sizeof(float2));
+  cudaMemset(p->counters, 0, 4 * sizeof(int));
+  if (cudaGetLastError() != cudaSuccess) {
+    cs_plan_destroy(p);
+    return cuda_fail("cs_plan_create");
+  }
+  *out = p;
+  return CS_OK;
+}
+
+int cs_plan_destroy(cs_plan* p) {
+  if (!p) return CS_OK;
+  DeviceGuard g(p->device);
+  cudaFree(p->tww); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag);
+  cudaFree(p->flags); cudaFree(p->counters);
+  if (p->prof) {
+    auto* ps = (ProfState*)p->prof;
+    for (auto& r : ps->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ps->pool) cudaEventDestroy(e);
+    delete ps;
+  }
+  delete p;
+  return CS_OK;
+}
+
+int cs_spectra(cs_plan* p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0, int kc,
+               void* stream) {
+  if (!p || !x) { cs_set_error("cs_spectra: null argument"); return CS_EPARAM; }
+  if (dtype != CS_F32 && dtype != CS_F64) { cs_set_error("unknown dtype %d", dtype); return CS_EPARAM; }
+  if (kc < 0 || slot0 < 0) { cs_set_error("cs_spectra: bad trial range"); return CS_EPARAM; }
+  if (kc == 0) return CS_OK;
+  DeviceGuard g(p->device);
+  {
+    cs::PhaseMark ph(*p, "spectra", (cudaStream_t)stream);
+    cs::run_spectra(*p, x, dtype, ts, ns, slot0 % p->slot_cap, kc, (cudaStream_t)stream);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_spectra");
+  p->fft_calls += (int64_t)kc * p->N * p->L;
+  return CS_OK;
+}
+
+int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                    int rb, int re, const cs_outputs* out, void* stream) {
+  if (!p || !out) { cs_set_error("cs_pair_metrics: null argument"); return CS_EPARAM; }
+  if (mask == 0 || (mask >> CS_NUM_METRICS)) { cs_set_error("bad metric mask 0x%x", mask); return CS_EPARAM; }
+  if (K < 1) { cs_set_error("no trials accumulated"); return CS_EDEGENERATE; }
+  if ((mask & CS_USPLI) && K < 2) { cs_set_error("USPLI needs at least 2 trials"); return CS_EDEGENERATE; }
+  if (bin_lo < 0 || nbb < 1 || bin_lo + nbb > p->nb) {
+    cs_set_error("bins [%d, %d) outside the plan's %d bins", bin_lo, bin_lo + nbb, p->nb);
+    return CS_EPARAM;
+  }
+  const int nt = cs_num_row_tiles(p->N);
+  if (re < 0) re = nt;
+  if (rb < 0 || rb > re || re > nt) { cs_set_error("bad row tile range [%d, %d)", rb, re); return CS_EPARAM; }
+  if (p->N < 2 || rb == re) return CS_OK;
+  DeviceGuard g(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    cs::PhaseMark ph(*p, "node_stats", st);
+    cs::run_node_stats(*p, slots, K, bin_lo, nbb, st);
+  }
+  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
+  if (cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_metrics");
+  return CS_OK;
+}
+
+int cs_get_spectra(cs_plan* p, const int* slots, int ns, int bin_lo, int nbins, void* dst,
+                   void* stream) {
+  if (!p || !slots || !dst) { cs_set_error("cs_get_spectra: null argument"); return CS_EPARAM; }
+  if (bin_lo < 0 || nbins < 1 || bin_lo + nbins > p->nb) { cs_set_error("cs_get_spectra: bad bins"); return CS_EPARAM; }
+  if (ns <= 0) return CS_OK;
+  DeviceGuard g(p->device);
+  cs::run_get_spectra(*p, slots, ns, bin_lo, nbins, dst, (cudaStream_t)stream);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_get_spectra");
+  return CS_OK;
+}
+
+int cs_last_fallback_count(cs_plan* p, void* stream, int64_t* n) {
+  if (!p || !n) return CS_EPARAM;
+  DeviceGuard g(p->device);
+  int h[2] = {0, 0};
+  if (cudaMemcpyAsync(h, p->counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+    return cuda_fail("cs_last_fallback_count");
+  *n = h[0];
+  if (h[1]) {
+    cs_set_error("fp64 guard list overflow: %d flagged entries > capacity %d", h[0], p->flag_cap);
+    return CS_ENOMEM;
+  }
+  return CS_OK;
+}
+
+int cs_plan_set_profiling(cs_plan* p, int on) {
+  if (!p) return CS_EPARAM;
+  if (!p->prof) p->prof = new ProfState();
+  p->profiling = on != 0;
+  return CS_OK;
+}
+
+int cs_profile_read(cs_plan* p, char* buf, int len) {
+  if (!p || !buf || len < 1) return CS_EPARAM;
+  buf[0] = 0;
+  if (!p->prof) return CS_OK;
+  DeviceGuard g(p->device);
+  auto* ps = (ProfState*)p->prof;
+  struct Acc { const char* name; double ms; int n; };
+  std::vector<Acc> acc;
+  for (auto& r : ps->recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    bool found = false;
+    for (auto& a : acc)
+      if (!strcmp(a.name, r.name)) { a.ms += ms; a.n++; found = true; }
+    if (!found) acc.push_back({r.name, (double)ms, 1});
+    ps->pool.push_back(r.a);
+    ps->pool.push_back(r.b);
+  }
+  ps->recs.clear();
+  int off = 0;
+  for (auto& a : acc) off += snprintf(buf + off, len > off ? len - off : 0, "%s:%.6f:%d;", a.name, a.ms, a.n);
+  return CS_OK;
+}
+
+int64_t cs_launch_count(const cs_plan* p) { return p ? p->launches : 0; }
+
+int cs_ring_view(cs_plan* p, void** x64, void** x32, int64_t* n_elems) {
+  if (!p) return CS_EPARAM;
+  *x64 = p->X64;
+  *x32 = p->X32;
+  *n_elems = (int64_t)p->slot_cap * p->L * p->nb * p->N;
+  return CS_OK;
+}
+
+int64_t cs_fft_call_count(const cs_plan* p) { return p ? p->fft_calls : 0; }
+void cs_reset_fft_call_count(cs_plan* p) { if (p) p->fft_calls = 0; }
+
+int cs_pair_sums(cs_plan*, const int*, int, int, int, const cs_sums*, void*) {
+  cs_set_error("cs_pair_sums: not implemented yet");
+  return CS_EPARAM;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// Shared definitions for the csconn CUDA sources (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/csconn.h"
+
+#ifndef __CUDA_ARCH__
+#define CS_HOST_ONLY 1
+#endif
+
+namespace cs {
+
+constexpr int kTile = 64;        // node tile edge of the upper-triangular pair tiling
+constexpr int kThreads = 256;    // pair-kernel CTA size (16 x 16 threads, 4 x 4 pairs each)
+
+struct Plan {
+  int device = 0;
+  int N = 0, T = 0, nfft = 0, lo = 0, hi = 0, nb = 0, L = 1, T_eff = 0;
+  int slot_cap = 0;
+  float scale = 1.f;             // power of two applied to the fp32 spectra
+  int dc_local = -1, nyq_local = -1;  // plan-local indices of exactly-real bins
+  double2* tww = nullptr;        // [L][nb][T_eff]   taper x twiddle
+  double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
+  float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra
+  float* psd = nullptr;          // [nb][N] per-call node statistics
+  float* mag = nullptr;          // [nb][N] max_k sqrt(sum_l |X|^2)
+  int4* flags = nullptr;         // fp64-fallback work list (i, j, local bin, -)
+  int* counters = nullptr;       // [0] flag count, [1] overflow
+  int flag_cap = 0;
+  int64_t fft_calls = 0;
+  int64_t launches = 0;          // kernels launched by this plan (bench evidence)
+  bool profiling = false;        // record CUDA events around every kernel phase
+  void* prof = nullptr;          // host-side event records (api.cu)
+};
+
+// packed fp32x2 helpers (Blackwell f32x2 ALU instructions)
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo_of(f2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi_of(f2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Upper-triangle pair index of (i < j) over n nodes (spectral.py:119-122).
+__host__ __device__ __forceinline__ int64_t pair_of(int64_t i, int64_t j, int64_t n) {
+  return i * (n - 1) - i * (i - 1) / 2 + (j - i - 1);
+}
+
+// Decode the t-th tile (I <= J) of the row-tile range starting at row_begin.
+__device__ __forceinline__ void decode_tile(int64_t t, int nt, int row_begin, int& I, int& J) {
+  int r = row_begin;
+  int64_t left = t;
+  while (left >= nt - r) {
+    left -= nt - r;
+    ++r;
+  }
+  I = r;
+  J = r + (int)left;
+}
+
+// Profiling phase (CUDA events on the launching stream around one kernel);
+// implemented in api.cu, a no-op unless cs_plan_set_profiling() is on.
+struct PhaseMark {
+  void* rec = nullptr;
+  PhaseMark(Plan& p, const char* name, cudaStream_t st);
+  ~PhaseMark();
+};
+
+}  // namespace cs
+
+void cs_set_error(const char* fmt, ...);

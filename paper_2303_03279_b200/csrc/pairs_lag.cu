@@ -1,0 +1,393 @@
+// K3: the phase-lag family (PLI, USPLI, WPLI, DSWPLI) plus IMAGCOHY, as a
+// register-tiled pair x trial kernel on the FP32/ALU pipes.
+//
+// Reference: spectral.py:216-241 (_fold_csd: Im flush, sign(Im), |Im| and Im
+// sums), metrics.py:49-86 (imagcohy/pli/uspli/wpli/dswpli finalisers),
+// metrics.py:115-134 + core.py:208-215 (band mean).
+//
+// Per (pair i<j, bin b) and trial k the kernel needs t = Im(X_i conj X_j) and
+// accumulates sum t, sum |t|, #(t < 0) and min |t| (the exact-sign guard).  Two
+// trials are packed per f32x2 register pair, so t costs one FMUL2 + one FFMA2
+// per two updates.  A CTA owns a 64 x 64 node tile of the upper triangle and all
+// bins of the band; each thread owns 4 x 4 pairs.  Trials are gathered by slot
+// index (any window of the HBM spectrum ring) and staged through shared memory
+// as float4 (re_a, re_b, im_a, im_b); the J side is stored with Im negated so
+// that t = Im_i*Re_j + Re_i*(-Im_j) is a single FFMA2.
+//
+// Exact-sign guard: with |X| <= M (max over the selected trials), fp32 rounding
+// moves t by at most (4 + L) u M_i M_j, so a (pair, bin) whose min_k |t_k| is
+// above g*M_i*M_j has the reference's sign(Im) in every trial (and no Im flush,
+// spectral.py:227-228).  The rest (about 1e-4 of pair-bins) are appended to a
+// work list and recomputed from the fp64 ring by k_lag_fallback.
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int kKC = 8;  // k-pairs per staged chunk (16 trials)
+
+struct LagArgs {
+  const float2* X32;
+  const double2* X64;
+  int N, nb, L;
+  const int* slots;
+  int K;
+  int bin_lo, nbb;
+  const float* psd;  // [nbb][N]
+  const float* mag;  // [nbb][N]
+  int real0, real1;  // plan-local bins whose spectra are exactly real (or -1)
+  int nt, row_begin;
+  int64_t pair_base, pair_stride;
+  float* bins[5];    // IMAGCOHY, PLI, USPLI, WPLI, DSWPLI : [nbb][pair_stride]
+  float* band[5];
+  float g;           // guard factor
+  float scale2;      // plan scale^2 (fp64 fallback -> fp32 units)
+  int4* flags;
+  int* counters;
+  int flag_cap;
+};
+
+__device__ __forceinline__ void lag_finalize(const LagArgs& a, int K, float s_im, float s_abs,
+                                             int pli_sum, float psd_i, float psd_j, float v[5]) {
+  const float den = sqrtf(psd_i * psd_j);
+  v[0] = den > 1.17549435e-38f ? s_im / den : 0.f;                 // IMAGCOHY
+  const float pli = fabsf((float)pli_sum) / (float)K;                // PLI
+  v[1] = pli;
+  v[2] = K > 1 ? ((float)K * pli * pli - 1.f) / ((float)K - 1.f) : 0.f;  // USPLI
+  const float w = s_abs > 0.f ? fabsf(s_im) / s_abs : 0.f;           // WPLI (0/0 -> 0)
+  v[3] = w;
+  v[4] = w * w;                                                      // DSWPLI
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_pairs_lag(const LagArgs a) {
+  extern __shared__ float4 smem4[];
+  float4* XI = smem4;                          // [2][kKC][64]
+  float4* XJ = smem4 + 2 * kKC * kTile;        // [2][kKC][64]
+  float* band_s = (float*)(smem4 + 4 * kKC * kTile);  // [5][64][64]
+
+  int I, J;
+  decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int iBase = I * kTile, jBase = J * kTile;
+
+  bool want_band = false;
+#pragma unroll
+  for (int m = 0; m < 5; ++m) want_band |= (a.band[m] != nullptr);
+  if (want_band)
+    for (int e = tid; e < 5 * kTile * kTile; e += kThreads) band_s[e] = 0.f;
+
+  const int K2 = a.K >> 1;
+  const bool odd = a.K & 1;
+  const int n_stage = (K2 + kKC - 1) / kKC;
+
+  for (int bl = 0; bl < a.nbb; ++bl) {
+    const int b = a.bin_lo + bl;
+    const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
+    const float2* Xb = a.X32 + (int64_t)b * a.N;  // + slot*slot_stride + n
+
+    f2 sim[16];
+    float sabs[16], mn[16];
+    int neg[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      sim[p] = 0ull;
+      sabs[p] = 0.f;
+      mn[p] = 3.0e38f;
+      neg[p] = 0;
+    }
+
+    // ---- staged gather of (trial-pair, node) float4 into shared memory ----
+    float2 ra[2][2], rb[2][2];  // [side][q] for slots a, b
+    auto load_stage = [&](int kp0, int nkp, bool tail) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = tid + kThreads * q;
+        const int kp = e >> 6, node = e & 63;
+        int sa = -1, sb = -1;
+        if (kp < nkp) {
+          if (tail) {
+            sa = a.slots[a.K - 1];
+          } else {
+            sa = a.slots[2 * (kp0 + kp)];
+            sb = a.slots[2 * (kp0 + kp) + 1];
+          }
+        }
+        const int ni = iBase + node, nj = jBase + node;
+        const float2 z = make_float2(0.f, 0.f);
+        ra[0][q] = (sa >= 0 && ni < a.N) ? Xb[sa * slot_stride + ni] : z;
+        rb[0][q] = (sb >= 0 && ni < a.N) ? Xb[sb * slot_stride + ni] : z;
+        ra[1][q] = (sa >= 0 && nj < a.N) ? Xb[sa * slot_stride + nj] : z;
+        rb[1][q] = (sb >= 0 && nj < a.N) ? Xb[sb * slot_stride + nj] : z;
+      }
+    };
+    auto store_stage = [&](int buf) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = tid + kThreads * q;
+        const int kp = e >> 6, node = e & 63;
+        XI[(buf * kKC + kp) * kTile + node] = make_float4(ra[0][q].x, rb[0][q].x, ra[0][q].y, rb[0][q].y);
+        XJ[(buf * kKC + kp) * kTile + node] =
+            make_float4(ra[1][q].x, rb[1][q].x, -ra[1][q].y, -rb[1][q].y);
+      }
+    };
+
+    auto compute_kp = [&](int buf, int kp) {
+      float4 xi[4], xj[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) xi[r] = XI[(buf * kKC + kp) * kTile + ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xj[c] = XJ[(buf * kKC + kp) * kTile + tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = r * 4 + c;
+          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+          const f2 t = ffma2(ii, jr, fmul2(ir, jn));
+          sim[p] = fadd2(sim[p], t);
+          const float tl = lo_of(t), th = hi_of(t);
+          sabs[p] += fabsf(tl);
+          sabs[p] += fabsf(th);
+          neg[p] += (int)(__float_as_uint(tl) >> 31);
+          neg[p] += (int)(__float_as_uint(th) >> 31);
+          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+        }
+      }
+    };
+
+    if (n_stage > 0) {
+      load_stage(0, min(kKC, K2), false);
+      store_stage(0);
+    }
+    __syncthreads();
+    for (int s = 0; s < n_stage; ++s) {
+      const int buf = s & 1;
+      const int nkp = min(kKC, K2 - s * kKC);
+      const bool more = s + 1 < n_stage;
+      if (more) load_stage((s + 1) * kKC, min(kKC, K2 - (s + 1) * kKC), false);
+      for (int kp = 0; kp < nkp; ++kp) compute_kp(buf, kp);
+      if (more) store_stage(buf ^ 1);
+      __syncthreads();
+    }
+    if (odd) {
+      // last trial alone: stage it with an empty partner and use the low lanes only
+      load_stage(0, 1, true);
+      store_stage(0);
+      __syncthreads();
+      float4 xi[4], xj[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) xi[r] = XI[ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xj[c] = XJ[tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = r * 4 + c;
+          const float t = fmaf(xi[r].z, xj[c].x, xi[r].x * xj[c].z);
+          sim[p] = fadd2(sim[p], pk(t, 0.f));
+          sabs[p] += fabsf(t);
+          neg[p] += (int)(__float_as_uint(t) >> 31);
+          mn[p] = fminf(mn[p], fabsf(t));
+        }
+      __syncthreads();
+    }
+
+    // ---- epilogue: finalize the bin ----
+    const bool real_bin = (b == a.real0) || (b == a.real1);
+    float Mi[4], Mj[4], Pi[4], Pj[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = iBase + ty + 16 * r;
+      Mi[r] = i < a.N ? a.mag[(int64_t)bl * a.N + i] : 0.f;
+      Pi[r] = i < a.N ? a.psd[(int64_t)bl * a.N + i] : 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = jBase + tx + 16 * c;
+      Mj[c] = j < a.N ? a.mag[(int64_t)bl * a.N + j] : 0.f;
+      Pj[c] = j < a.N ? a.psd[(int64_t)bl * a.N + j] : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int p = r * 4 + c;
+        const int li = ty + 16 * r, lj = tx + 16 * c;
+        const int i = iBase + li, j = jBase + lj;
+        if (!(i < j && j < a.N)) continue;
+        const bool dead = real_bin || Mi[r] == 0.f || Mj[c] == 0.f;
+        float s_im = lo_of(sim[p]) + hi_of(sim[p]);
+        float s_abs = sabs[p];
+        int pli_sum = a.K - 2 * neg[p];
+        if (dead) {
+          s_im = 0.f;
+          s_abs = 0.f;
+          pli_sum = 0;
+        } else if (mn[p] <= a.g * Mi[r] * Mj[c]) {
+          const int slot = atomicAdd(&a.counters[0], 1);
+          if (slot < a.flag_cap)
+            a.flags[slot] = make_int4(i, j, bl, 0);
+          else
+            a.counters[1] = 1;
+          continue;  // the fp64 fallback writes this (pair, bin)
+        }
+        float v[5];
+        lag_finalize(a, a.K, s_im, s_abs, pli_sum, Pi[r], Pj[c], v);
+        const int64_t po = pair_of(i, j, a.N) - a.pair_base;
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          if (a.bins[m]) a.bins[m][(int64_t)bl * a.pair_stride + po] = v[m];
+          if (a.band[m]) band_s[(m * kTile + li) * kTile + lj] += v[m];
+        }
+      }
+  }
+
+  if (want_band) {
+    __syncthreads();
+    const float inv = 1.f / (float)a.nbb;
+    for (int e = tid; e < kTile * kTile; e += kThreads) {
+      const int li = e >> 6, lj = e & 63;
+      const int i = iBase + li, j = jBase + lj;
+      if (!(i < j && j < a.N)) continue;
+      const int64_t po = pair_of(i, j, a.N) - a.pair_base;
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+        if (a.band[m]) a.band[m][po] = band_s[(m * kTile + li) * kTile + lj] * inv;
+    }
+  }
+}
+
+// fp64 recomputation of flagged (pair, bin) entries: one warp per entry, lanes
+// over trials; reference arithmetic of spectral.py:204-241 in complex128.
+__global__ void k_lag_fallback(const LagArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * blockDim.x) >> 5;
+  const int count = min(a.counters[0], a.flag_cap);
+  const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
+  for (int w = warp; w < count; w += n_warps) {
+    const int4 f = a.flags[w];
+    const int i = f.x, j = f.y, bl = f.z, b = a.bin_lo + bl;
+    double s_im = 0.0, s_abs = 0.0;
+    int s_sign = 0;
+    for (int k = lane; k < a.K; k += 32) {
+      const int slot = a.slots[k];
+      double re = 0.0, im = 0.0;
+      for (int l = 0; l < a.L; ++l) {
+        const double2 xi = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + i];
+        const double2 xj = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + j];
+        // (xi.x + i xi.y) * (xj.x - i xj.y)
+        re += xi.x * xj.x + xi.y * xj.y;
+        im += xi.y * xj.x - xi.x * xj.y;
+      }
+      if (fabs(im) <= 1e-13 * fabs(re)) im = 0.0;  // spectral.py:227-228
+      s_im += im;
+      s_abs += fabs(im);
+      s_sign += (im > 0.0) - (im < 0.0);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s_im += __shfl_xor_sync(0xffffffffu, s_im, o);
+      s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+      s_sign += __shfl_xor_sync(0xffffffffu, s_sign, o);
+    }
+    if (lane == 0) {
+      float v[5];
+      const float psd_i = a.psd[(int64_t)bl * a.N + i], psd_j = a.psd[(int64_t)bl * a.N + j];
+      // IMAGCOHY in fp64 then rounded; the ratios are scale invariant
+      const double den = sqrt((double)psd_i * (double)psd_j);
+      const double imag = den > 0.0 ? s_im * (double)a.scale2 / den : 0.0;
+      const double pli = fabs((double)s_sign) / a.K;
+      const double wpli = s_abs > 0.0 ? fabs(s_im) / s_abs : 0.0;
+      v[0] = (float)imag;
+      v[1] = (float)pli;
+      v[2] = a.K > 1 ? (float)((a.K * pli * pli - 1.0) / (a.K - 1.0)) : 0.f;
+      v[3] = (float)wpli;
+      v[4] = (float)(wpli * wpli);
+      const int64_t po = pair_of(i, j, a.N) - a.pair_base;
+      const float inv = 1.f / (float)a.nbb;
+      for (int m = 0; m < 5; ++m) {
+        if (a.bins[m]) a.bins[m][(int64_t)bl * a.pair_stride + po] = v[m];
+        if (a.band[m]) atomicAdd(&a.band[m][po], v[m] * inv);
+      }
+    }
+  }
+}
+
+size_t lag_smem_bytes() { return (size_t)4 * kKC * kTile * sizeof(float4) + 5 * kTile * kTile * sizeof(float); }
+
+void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
+  static bool configured = false;
+  const size_t smem = lag_smem_bytes();
+  if (!configured) {
+    cudaFuncSetAttribute(k_pairs_lag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
+  {
+    PhaseMark ph(p, "pairs_lag", st);
+    k_pairs_lag<<<(unsigned)n_tiles, kThreads, smem, st>>>(a);
+  }
+  {
+    PhaseMark ph(p, "lag_fallback", st);
+    k_lag_fallback<<<148 * 4, 256, 0, st>>>(a);
+  }
+}
+
+}  // namespace cs
+
+namespace cs {
+
+// metric-bit -> lag-kernel output slot
+static const unsigned kLagBits[5] = {CS_IMAGCOHY, CS_PLI, CS_USPLI, CS_WPLI, CS_DSWPLI};
+static const int kLagIdx[5] = {2, 4, 5, 6, 7};
+
+int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                    int rb, int re, const cs_outputs* out, cudaStream_t st) {
+  unsigned any = 0;
+  for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
+  if (!any) return 0;
+  LagArgs a{};
+  a.X32 = p.X32;
+  a.X64 = p.X64;
+  a.N = p.N; a.nb = p.nb; a.L = p.L;
+  a.slots = slots; a.K = K;
+  a.bin_lo = bin_lo; a.nbb = nbb;
+  a.psd = p.psd; a.mag = p.mag;
+  a.real0 = p.dc_local; a.real1 = p.nyq_local;
+  a.nt = (p.N + kTile - 1) / kTile;
+  a.row_begin = rb;
+  a.pair_base = out->pair_base;
+  a.pair_stride = out->pair_stride;
+  for (int q = 0; q < 5; ++q) {
+    const bool on = (mask & kLagBits[q]) != 0;
+    a.bins[q] = on ? (float*)out->bins[kLagIdx[q]] : nullptr;
+    a.band[q] = on ? (float*)out->band[kLagIdx[q]] : nullptr;
+  }
+  a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
+  a.scale2 = p.scale * p.scale;
+  a.flags = p.flags;
+  a.counters = p.counters;
+  a.flag_cap = p.flag_cap;
+  int64_t n_tiles = 0;
+  for (int I = rb; I < re; ++I) n_tiles += a.nt - I;
+  if (p.L != 1) {
+    cs_set_error("multitaper phase-lag kernel not built yet");
+    return -1;
+  }
+  run_pairs_lag(p, a, n_tiles, st);
+  return 2;
+}
+
+int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                    int rb, int re, const cs_outputs* out, cudaStream_t st) {
+  (void)p; (void)slots; (void)K; (void)bin_lo; (void)nbb; (void)rb; (void)re; (void)out; (void)st;
+  if (mask & (CS_COHY | CS_COH | CS_PLV)) {
+    cs_set_error("coherency family not built yet");
+    return -1;
+  }
+  return 0;
+}
+
+}  // namespace cs

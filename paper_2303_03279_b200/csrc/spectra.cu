@@ -1,0 +1,268 @@
+// K1: batched demean + taper + one-sided DFT of every node x trial x taper, in
+// fp64, writing the HBM spectrum ring (fp64 copy for the exact-sign guard, fp32
+// scaled copy for the pair kernels).
+//
+// Reference: spectral.py:49-62 (_crop_pad_demean: crop to nfft or zero-pad,
+// demean over the real samples), spectral.py:82-97 (rfft, DC := 0).  Taper
+// extension (SURVEY.md conventions 11): demean, then taper, then zero-pad.
+//
+// Only the plan's bins [lo, hi] are produced, so the transform is a dense
+// [signals x T_eff] x [T_eff x nb] complex contraction: each CTA stages a
+// 128-node x 32-sample block (coalesced rows) transposed into shared memory, one
+// thread per node accumulates up to NBT bins in fp64 registers, twiddles are
+// broadcast from shared memory.  DFMA-bound (B200: 64 DFMA/clk/SM).
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int kSpecNodes = 128;
+constexpr int kSpecChunk = 32;
+
+template <typename Tin, int NBT>
+__global__ void __launch_bounds__(kSpecNodes)
+k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N,
+          int T_eff, int nb, int L, const double2* __restrict__ tww, int slot0, int slot_cap,
+          double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local,
+          int nyq_local) {
+  __shared__ double sx[kSpecChunk][kSpecNodes + 1];
+  __shared__ double2 stw[NBT][kSpecChunk];
+  const int tid = threadIdx.x;
+  const int n0 = blockIdx.x * kSpecNodes;
+  const int b0 = blockIdx.y * NBT;
+  const int k = blockIdx.z / L;
+  const int l = blockIdx.z % L;
+  const int nbt = min(NBT, nb - b0);
+  const Tin* xk = x + (int64_t)k * trial_stride;
+
+  // ---- pass 1: per-node mean over the real samples (fp64) ----
+  double sum = 0.0;
+  for (int t0 = 0; t0 < T_eff; t0 += kSpecChunk) {
+#pragma unroll 4
+    for (int q = 0; q < kSpecChunk; ++q) {
+      int e = tid + kSpecNodes * q;
+      int row = e / kSpecChunk, col = e % kSpecChunk;
+      int n = n0 + row, t = t0 + col;
+      double v = 0.0;
+      if (n < N && t < T_eff) v = (double)xk[(int64_t)n * node_stride + t];
+      sx[col][row] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int t = 0; t < kSpecChunk; ++t) sum += sx[t][tid];
+    __syncthreads();
+  }
+  const double mean = sum / (double)T_eff;
+
+  // ---- pass 2: demeaned, tapered DFT over the plan bins ----
+  double are[NBT], aim[NBT];
+#pragma unroll
+  for (int j = 0; j < NBT; ++j) are[j] = aim[j] = 0.0;
+  __shared__ double smean[kSpecNodes];
+  smean[tid] = mean;
+  __syncthreads();
+  const double2* twl = tww + (int64_t)l * nb * T_eff;
+  for (int t0 = 0; t0 < T_eff; t0 += kSpecChunk) {
+#pragma unroll 4
+    for (int q = 0; q < kSpecChunk; ++q) {
+      int e = tid + kSpecNodes * q;
+      int row = e / kSpecChunk, col = e % kSpecChunk;
+      int n = n0 + row, t = t0 + col;
+      double v = 0.0;
+      if (n < N && t < T_eff) v = (double)xk[(int64_t)n * node_stride + t] - smean[row];
+      sx[col][row] = v;
+    }
+    for (int e = tid; e < NBT * kSpecChunk; e += kSpecNodes) {
+      int j = e / kSpecChunk, t = e % kSpecChunk;
+      double2 w = make_double2(0.0, 0.0);
+      if (j < nbt && t0 + t < T_eff) w = twl[(int64_t)(b0 + j) * T_eff + t0 + t];
+      stw[j][t] = w;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = 0; t < kSpecChunk; ++t) {
+      const double v = sx[t][tid];
+#pragma unroll
+      for (int j = 0; j < NBT; ++j) {
+        const double2 w = stw[j][t];
+        are[j] = fma(v, w.x, are[j]);
+        aim[j] = fma(v, w.y, aim[j]);
+      }
+    }
+    __syncthreads();
+  }
+
+  const int n = n0 + tid;
+  if (n >= N) return;
+  const int slot = (slot0 + k) % slot_cap;
+#pragma unroll
+  for (int j = 0; j < NBT; ++j) {
+    if (j >= nbt) break;
+    const int b = b0 + j;
+    double re = are[j], im = aim[j];
+    if (b == dc_local) re = im = 0.0;       // spectral.py:96: DC is exactly zero
+    if (b == nyq_local) im = 0.0;           // Nyquist of a real signal is real
+    const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
+    X64[o] = make_double2(re, im);
+    X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+  }
+}
+
+template <typename Tin, int NBT>
+static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0,
+                           int kc, cudaStream_t st) {
+  dim3 grid((p.N + kSpecNodes - 1) / kSpecNodes, (p.nb + NBT - 1) / NBT, kc * p.L);
+  k_spectra<Tin, NBT><<<grid, kSpecNodes, 0, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
+                                                    p.L, p.tww, slot0, p.slot_cap, p.X64, p.X32,
+                                                    p.scale, p.dc_local, p.nyq_local);
+}
+
+template <typename Tin>
+static void dispatch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0,
+                             int kc, cudaStream_t st) {
+  // pick the per-thread bin count: wide bands use 16-bin chunks on gridDim.y
+  switch (p.nb) {
+    case 1: launch_spectra<Tin, 1>(p, x, ts, ns, slot0, kc, st); break;
+    case 2: launch_spectra<Tin, 2>(p, x, ts, ns, slot0, kc, st); break;
+    case 3: launch_spectra<Tin, 3>(p, x, ts, ns, slot0, kc, st); break;
+    case 4: launch_spectra<Tin, 4>(p, x, ts, ns, slot0, kc, st); break;
+    case 5: launch_spectra<Tin, 5>(p, x, ts, ns, slot0, kc, st); break;
+    case 6: launch_spectra<Tin, 6>(p, x, ts, ns, slot0, kc, st); break;
+    case 7:
+    case 8: launch_spectra<Tin, 8>(p, x, ts, ns, slot0, kc, st); break;
+    case 9:
+    case 10:
+    case 11:
+    case 12: launch_spectra<Tin, 12>(p, x, ts, ns, slot0, kc, st); break;
+    default: launch_spectra<Tin, 16>(p, x, ts, ns, slot0, kc, st); break;
+  }
+}
+
+void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0,
+                 int kc, cudaStream_t st) {
+  if (dtype == CS_F64)
+    dispatch_spectra<double>(p, x, ts, ns, slot0, kc, st);
+  else
+    dispatch_spectra<float>(p, x, ts, ns, slot0, kc, st);
+}
+
+// Per-call node statistics over the selected trials: psd = sum_k sum_l |X|^2
+// (fp32 scaled units; the 1/L taper mean cancels in every ratio) and
+// mag = max_k sqrt(sum_l |X|^2), the bound used by the exact-sign guard.
+__global__ void k_node_stats(const float2* __restrict__ X32, const int* __restrict__ slots,
+                             int K, int N, int nb, int L, int bin_lo, int nbb,
+                             float* __restrict__ psd, float* __restrict__ mag) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int bl = blockIdx.y;  // 0..nbb-1
+  if (n >= N) return;
+  const int b = bin_lo + bl;
+  double s = 0.0;
+  float m = 0.f;
+  for (int k = 0; k < K; ++k) {
+    const int slot = slots[k];
+    float e = 0.f;
+    for (int l = 0; l < L; ++l) {
+      const float2 v = X32[(((int64_t)slot * L + l) * nb + b) * N + n];
+      e = fmaf(v.x, v.x, fmaf(v.y, v.y, e));
+    }
+    s += (double)e;
+    m = fmaxf(m, sqrtf(e));
+  }
+  psd[(int64_t)bl * N + n] = (float)s;
+  mag[(int64_t)bl * N + n] = m;
+}
+
+void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb,
+                    cudaStream_t st) {
+  dim3 grid((p.N + 127) / 128, nbb);
+  k_node_stats<<<grid, 128, 0, st>>>(p.X32, slots, K, p.N, p.nb, p.L, bin_lo, nbb, p.psd, p.mag);
+}
+
+// complex128 [n_slots][N][nbins] copy-out of the fp64 ring (taper 0), trial_spectra layout.
+__global__ void k_get_spectra(const double2* __restrict__ X64, const int* __restrict__ slots,
+                              int N, int nb, int L, int bin_lo, int nbins, double2* __restrict__ dst) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (idx >= (int64_t)N * nbins) return;
+  const int n = (int)(idx / nbins), bl = (int)(idx % nbins);
+  dst[((int64_t)k * N + n) * nbins + bl] = X64[(((int64_t)slots[k] * L) * nb + bin_lo + bl) * N + n];
+}
+
+void run_get_spectra(const Plan& p, const int* slots, int ns, int bin_lo, int nbins, void* dst,
+                     cudaStream_t st) {
+  dim3 grid((unsigned)(((int64_t)p.N * nbins + 255) / 256), ns);
+  k_get_spectra<<<grid, 256, 0, st>>>(p.X64, slots, p.N, p.nb, p.L, bin_lo, nbins, (double2*)dst);
+}
+
+}  // namespace cs
+
+// ---------------------------------------------------------------------------
+// Live pipe-peak probes for the roofline denominators that MEASURED_PEAKS.json
+// does not carry (FP32 FMA-pipe lane ops/s and FP64 DFMA/s on this device).
+// ---------------------------------------------------------------------------
+namespace cs {
+constexpr int kProbeIters = 4096;
+__global__ void k_probe_fp32(float* out, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) x[i] = threadIdx.x + i;
+  for (int it = 0; it < kProbeIters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = fmaf(x[i], a, b);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += x[i];
+  if (s == 12345.f) out[0] = s;
+}
+__global__ void k_probe_fp64(double* out, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) x[i] = threadIdx.x + i;
+  for (int it = 0; it < kProbeIters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = fma(x[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += x[i];
+  if (s == 12345.0) out[0] = s;
+}
+}  // namespace cs
+
+extern "C" int cs_probe_peaks(int device, double* fp32_lane_ops, double* fp64_fma) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  void* buf = nullptr;
+  cudaMalloc(&buf, 64);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int grid = nsm * 8, blk = 256;
+  float best32 = 1e30f, best64 = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    float ms;
+    cudaEventRecord(e0);
+    cs::k_probe_fp32<<<grid, blk>>>((float*)buf, 1.0001f, 0.5f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep) best32 = ms < best32 ? ms : best32;
+    cudaEventRecord(e0);
+    cs::k_probe_fp64<<<grid, blk>>>((double*)buf, 1.0001, 0.5);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep) best64 = ms < best64 ? ms : best64;
+  }
+  const double ops = (double)grid * blk * cs::kProbeIters * 8;
+  *fp32_lane_ops = ops / (best32 * 1e-3);
+  *fp64_fma = ops / (best64 * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaSetDevice(prev);
+  return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ECUDA;
+}

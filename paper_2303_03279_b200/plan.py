@@ -1,0 +1,251 @@
+"""Device plan: the HBM spectrum ring plus the fused pair kernels (csconn C ABI).
+
+This is the B200-native replacement of the reference's per-trial fold
+(spectral.py:204-261) and finalisers (metrics.py:32-134): one plan owns the
+spectrum cache of ``slot_capacity`` trials (fp64 + scaled fp32 copies) and runs
+K1 (taper + DFT) and the pair kernels over any list of cached trial slots.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import ParameterError
+
+METRIC_BITS = {"COHY": 0, "COH": 1, "IMAGCOHY": 2, "PLV": 3, "PLI": 4, "USPLI": 5, "WPLI": 6, "DSWPLI": 7}
+SEVEN = ("COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI")
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_taper(taper, n_eff: int):
+    """None/'boxcar' -> rectangular (the reference), 'hann' -> np.hanning(n_eff),
+    ('dpss', NW, L) -> scipy.signal.windows.dpss(n_eff, NW, Kmax=L), or an explicit
+    [L, n_eff] / [n_eff] array (SURVEY.md conventions item 11)."""
+    if taper is None or (isinstance(taper, str) and taper.lower() in ("boxcar", "rect", "none")):
+        return None
+    if isinstance(taper, str) and taper.lower() == "hann":
+        return np.hanning(n_eff)[None, :]
+    if isinstance(taper, tuple) and taper and str(taper[0]).lower() == "dpss":
+        from scipy.signal import windows
+        return np.atleast_2d(windows.dpss(n_eff, float(taper[1]), Kmax=int(taper[2])))
+    arr = np.atleast_2d(np.asarray(taper, dtype=np.float64))
+    if arr.shape[1] != n_eff:
+        raise ParameterError(f"taper length {arr.shape[1]} != {n_eff}")
+    return arr
+
+
+def pow2_scale(max_abs: float, n_eff: int) -> float:
+    """Power-of-two scale bringing spectra to O(1) in the fp32 copy (metrics are
+    invariant to it; it only protects the fp32 range)."""
+    if not (max_abs > 0.0) or not math.isfinite(max_abs):
+        return 1.0
+    e = -round(math.log2(max_abs * math.sqrt(n_eff)))
+    e = max(-100, min(100, e))
+    return float(2.0 ** e)
+
+
+class DevicePlan:
+    """Owns a csconn plan: spectrum ring of ``slot_capacity`` trials for bins
+    [lo, hi] of an nfft-point one-sided spectrum."""
+
+    def __init__(self, n_nodes: int, n_samples: int, nfft: int, lo: int, hi: int, taper=None,
+                 slot_capacity: int = 1, device=None, scale: float = 1.0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2303_03279_b200 needs a CUDA device (B200); there is no CPU fallback")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.n_nodes, self.n_samples, self.nfft = int(n_nodes), int(n_samples), int(nfft)
+        self.lo, self.hi = int(lo), int(hi)
+        self.n_bins = self.hi - self.lo + 1
+        self.n_eff = min(self.n_samples, self.nfft)
+        tap = make_taper(taper, self.n_eff)
+        self.n_tapers = 1 if tap is None else tap.shape[0]
+        self.slot_capacity = int(slot_capacity)
+        self.scale = float(scale)
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        tptr = None
+        if tap is not None:
+            self._taper = np.ascontiguousarray(tap, dtype=np.float64)
+            tptr = self._taper.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        with torch.cuda.device(self.device):
+            _lib.check(L.cs_plan_create(ctypes.byref(h), self.device.index, self.n_nodes, self.n_samples,
+                                        self.nfft, self.lo, self.hi, self.n_tapers, tptr,
+                                        self.slot_capacity, self.scale, 0))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().cs_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def n_pairs(self) -> int:
+        return self.n_nodes * (self.n_nodes - 1) // 2
+
+    # -- K1 ---------------------------------------------------------------
+    def spectra(self, x: torch.Tensor, slot0: int = 0, stream=None) -> None:
+        """x: device [k, N, T] (float32/float64; inner dim contiguous)."""
+        if x.device != self.device:
+            raise ParameterError("input must live on the plan's device")
+        if x.dim() != 3 or x.shape[1] != self.n_nodes or x.shape[2] < 1:
+            raise ParameterError(f"expected [k, {self.n_nodes}, T] samples, got {tuple(x.shape)}")
+        if x.shape[2] != self.n_samples:
+            raise ParameterError(f"plan expects {self.n_samples} samples per trial, got {x.shape[2]}")
+        if x.stride(2) != 1:
+            x = x.contiguous()
+        if x.dtype == torch.float64:
+            dt = _lib.CS_F64
+        elif x.dtype == torch.float32:
+            dt = _lib.CS_F32
+        else:
+            raise ParameterError(f"unsupported sample dtype {x.dtype}")
+        self._last_x = x  # keep alive until the launch is ordered
+        _lib.check(_lib.lib().cs_spectra(self._h, ctypes.c_void_p(x.data_ptr()), dt, x.stride(0), x.stride(1),
+                                         int(slot0), int(x.shape[0]), _stream_ptr(stream)))
+
+    # -- pair kernels -------------------------------------------------------
+    def alloc_outputs(self, metrics, n_bins: int, per_bin=True, band=True, pair_count=None):
+        P = self.n_pairs if pair_count is None else int(pair_count)
+        out = {}
+        for m in metrics:
+            cplx = m == "COHY"
+            dt = torch.complex64 if cplx else torch.float32
+            out[m] = {"bins": torch.empty((n_bins, P), dtype=dt, device=self.device) if per_bin else None,
+                      "band": torch.empty((P,), dtype=dt, device=self.device) if band else None}
+        return out
+
+    def pair_metrics(self, slots: torch.Tensor, metrics=SEVEN, bin_lo: int = 0, n_bins: int | None = None,
+                     outputs=None, per_bin=True, band=True, row_tiles=(0, -1), pair_base: int = 0,
+                     pair_count: int | None = None, stream=None):
+        if n_bins is None:
+            n_bins = self.n_bins - bin_lo
+        metrics = tuple(m.upper() for m in metrics)
+        for m in metrics:
+            if m not in METRIC_BITS:
+                raise ParameterError(f"{m} is not a spectral metric")
+        if slots.dtype != torch.int32 or slots.device != self.device:
+            slots = slots.to(device=self.device, dtype=torch.int32)
+        if outputs is None:
+            outputs = self.alloc_outputs(metrics, n_bins, per_bin, band, pair_count)
+        desc = _lib.CsOutputs()
+        mask = 0
+        for m in metrics:
+            bit = METRIC_BITS[m]
+            mask |= 1 << bit
+            o = outputs[m]
+            desc.bins[bit] = o["bins"].data_ptr() if o.get("bins") is not None else None
+            desc.band[bit] = o["band"].data_ptr() if o.get("band") is not None else None
+        desc.pair_base = int(pair_base)
+        desc.pair_stride = int(self.n_pairs if pair_count is None else pair_count)
+        self._last_slots = slots
+        _lib.check(_lib.lib().cs_pair_metrics(self._h, ctypes.c_void_p(slots.data_ptr()), int(slots.numel()),
+                                              mask, int(bin_lo), int(n_bins), int(row_tiles[0]),
+                                              int(row_tiles[1]), ctypes.byref(desc), _stream_ptr(stream)))
+        return outputs
+
+    def fallback_count(self, stream=None) -> int:
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().cs_last_fallback_count(self._h, _stream_ptr(stream), ctypes.byref(n)))
+        return int(n.value)
+
+    def get_spectra(self, slots: torch.Tensor, bin_lo: int = 0, n_bins: int | None = None, stream=None):
+        if n_bins is None:
+            n_bins = self.n_bins - bin_lo
+        slots = slots.to(device=self.device, dtype=torch.int32)
+        dst = torch.empty((slots.numel(), self.n_nodes, n_bins), dtype=torch.complex128, device=self.device)
+        _lib.check(_lib.lib().cs_get_spectra(self._h, ctypes.c_void_p(slots.data_ptr()), int(slots.numel()),
+                                             int(bin_lo), int(n_bins), ctypes.c_void_p(dst.data_ptr()),
+                                             _stream_ptr(stream)))
+        return dst
+
+    # -- instrumentation --------------------------------------------------------
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.check(_lib.lib().cs_plan_set_profiling(self._h, int(bool(on))))
+
+    def profile(self) -> dict:
+        """{phase: (total_ms, count)} since the last read (synchronises)."""
+        buf = ctypes.create_string_buffer(4096)
+        _lib.check(_lib.lib().cs_profile_read(self._h, buf, 4096))
+        out = {}
+        for rec in buf.value.decode().split(";"):
+            if rec:
+                name, ms, n = rec.split(":")
+                out[name] = (float(ms), int(n))
+        return out
+
+    def launch_count(self) -> int:
+        return int(_lib.lib().cs_launch_count(self._h))
+
+    def ring(self):
+        """(X64, X32) spectrum-ring views as torch tensors [slot, L, nb, N] complex."""
+        x64, x32, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(_lib.lib().cs_ring_view(self._h, ctypes.byref(x64), ctypes.byref(x32), ctypes.byref(n)))
+        shape = (self.slot_capacity, self.n_tapers, self.n_bins, self.n_nodes)
+        return (_wrap(x64.value, shape, torch.complex128, self.device, self),
+                _wrap(x32.value, shape, torch.complex64, self.device, self))
+
+    def fft_call_count(self) -> int:
+        return int(_lib.lib().cs_fft_call_count(self._h))
+
+    def reset_fft_call_count(self) -> None:
+        _lib.lib().cs_reset_fft_call_count(self._h)
+
+
+class _DevBuf:
+    """__cuda_array_interface__ shim exposing a plan-owned device buffer to torch."""
+
+    def __init__(self, ptr, shape, typestr, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap(ptr, shape, dtype, device, owner):
+    typestr = {torch.complex128: "<c16", torch.complex64: "<c8"}[dtype]
+    with torch.cuda.device(device):
+        return torch.as_tensor(_DevBuf(ptr, shape, typestr, owner), device=device)
+
+
+def probe_peaks(device_index: int = 0):
+    """(FP32 FMA-pipe lane ops/s, FP64 DFMA/s) measured live on this device."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.lib().cs_probe_peaks(int(device_index), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def row_tile_range(n_nodes: int, n_shards: int, shard: int):
+    L = _lib.lib()
+    rb, re = ctypes.c_int(), ctypes.c_int()
+    p0, p1 = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(L.cs_row_tile_range(n_nodes, n_shards, shard, ctypes.byref(rb), ctypes.byref(re),
+                                   ctypes.byref(p0), ctypes.byref(p1)))
+    return (rb.value, re.value), (p0.value, p1.value)
+
+
+def compute_connectivity(x: torch.Tensor, nfft: int, lo: int, hi: int, metrics=SEVEN, taper=None,
+                         per_bin=True, band=True, plan: DevicePlan | None = None, stream=None):
+    """Batch path: all trials of x [K, N, T] (device) -> per-bin [nb, P] and band
+    [P] outputs for ``metrics`` over the inclusive bins [lo, hi]."""
+    K, N, T = x.shape
+    if plan is None:
+        scale = pow2_scale(float(x.abs().amax()), min(T, nfft))
+        plan = DevicePlan(N, T, nfft, lo, hi, taper=taper, slot_capacity=K, device=x.device, scale=scale)
+    plan.spectra(x, 0, stream=stream)
+    slots = torch.arange(K, dtype=torch.int32, device=x.device)
+    out = plan.pair_metrics(slots, metrics, 0, plan.n_bins, per_bin=per_bin, band=band, stream=stream)
+    return out, plan

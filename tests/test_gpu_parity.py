@@ -1,0 +1,91 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference-generated
+golden vectors and the pinned oracle.
+
+Tolerances (north_star): max abs error <= 1e-4 for COH / IMAGCOHY / PLV and
+<= 1e-3 for the PLI family, fp32 results vs the float64 reference.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+
+TOL = {"COHY": 1e-4, "COH": 1e-4, "IMAGCOHY": 1e-4, "PLV": 1e-4,
+       "PLI": 1e-3, "USPLI": 1e-3, "WPLI": 1e-3, "DSWPLI": 1e-3}
+LAG = ("IMAGCOHY", "PLI", "USPLI", "WPLI", "DSWPLI")
+# Entries where two independent fp64 algorithms (the reference's rfft and a
+# direct DFT) already disagree by more than tol/2 are rounding noise in the
+# reference itself (Im flush at leakage-level bins of scaled copies); they are
+# excluded and counted.  Only the adversarial zero-lag cases have any.
+ADVERSARIAL = {"zerolag_dead", "zerolag_dead_hann"}
+
+pytestmark = pytest.mark.gpu
+
+
+def _load(name):
+    z = np.load(GOLDEN / f"{name}.npz")
+    return {k: z[k] for k in z.files}
+
+
+def _run(g, metrics, dtype=torch.float64):
+    from paper_2303_03279_b200 import compute_connectivity
+    taper = g["taper"] if g["taper"].size else None
+    x = torch.tensor(g["epochs"], dtype=dtype, device="cuda")
+    out, plan = compute_connectivity(x, int(g["nfft"]), int(g["lo"]), int(g["hi"]), metrics=metrics, taper=taper)
+    nfb = plan.fallback_count()
+    torch.cuda.synchronize()
+    return {m: {k: (v.cpu().numpy() if v is not None else None) for k, v in d.items()} for m, d in out.items()}, nfb
+
+
+CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg1like",
+         "dpss_small", "zerolag_dead", "zerolag_dead_hann", "sim2024_thresh"]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_lag_family_matches_reference(case):
+    g = _load(case)
+    if g["taper"].ndim == 2:
+        pytest.skip("multitaper phase-lag kernel pending")
+    K = g["epochs"].shape[0]
+    metrics = [m for m in LAG if not (m == "USPLI" and K < 2)]
+    out, _ = _run(g, metrics)
+    import oracle as O
+    taper = g["taper"] if g["taper"].size else None
+    ref = {m: {"bins": g["bins_" + m]} for m in metrics}
+    masks = O.well_conditioned(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), metrics, TOL,
+                               taper=taper, ref=ref)
+    sens = O.flush_sensitive(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), taper=taper)
+    masks = {m: v & ~sens for m, v in masks.items()}
+    for m in metrics:
+        want = g["bins_" + m]                      # [P, nb] reference layout
+        got = out[m]["bins"].T                     # stored bin-major [nb, P]
+        keep = masks[m]
+        if case not in ADVERSARIAL:
+            assert keep.all(), f"{case}/{m}: {np.size(keep) - keep.sum()} ill-conditioned entries"
+        full = np.where(keep, np.abs(got - want), 0.0)
+        w = np.unravel_index(np.argmax(full), full.shape)
+        assert full.max() <= TOL[m], f"{case}/{m}: max err {full.max():.3g} at (pair, bin) {w}: got {got[w]} want {want[w]}"
+        kb = keep.all(axis=1)
+        errb = np.abs(out[m]["band"] - g["band_" + m])[kb]
+        assert errb.max() <= TOL[m], f"{case}/{m} band: max err {errb.max():.3g}"
+
+
+def test_zero_lag_copies_are_exactly_zero():
+    g = _load("zerolag_dead")
+    out, nfb = _run(g, LAG)
+    assert nfb > 0  # the fp64 guard handled the copies
+    for m in ("IMAGCOHY", "PLI", "WPLI", "DSWPLI"):
+        for p in (0, 1):  # (0,1), (0,2): scaled copies of channel 0
+            assert np.all(out[m]["bins"][:, p] == 0.0), m
+
+
+def test_float32_input_path():
+    g = _load("sim2024_thresh")
+    x32 = g["epochs"].astype(np.float32)
+    import oracle as O
+    ref, _ = O.compute(list(x32.astype(np.float64)), 600, 15, 21, metrics=LAG)
+    g2 = dict(g)
+    g2["epochs"] = x32
+    out, _ = _run(g2, LAG, dtype=torch.float32)
+    for m in LAG:
+        assert np.abs(out[m]["bins"].T - ref[m]["bins"]).max() <= TOL[m], m
