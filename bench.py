@@ -185,7 +185,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--metrics", default=None, help="comma list (default: the config's metrics)")
-    ap.add_argument("--cpu-nodes", type=int, default=384, help="node subset for the CPU baseline")
+    ap.add_argument("--cpu-nodes", type=int, default=768, help="node subset for the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -191,15 +191,21 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   p->nyq_local = (nfft % 2 == 0 && hi == nfft / 2) ? (nfft / 2 - lo) : -1;
 
   // taper x twiddle table (host fp64, long double angles)
-  std::vector<double2> tw((size_t)L * p->nb * p->T_eff);
+  std::vector<double2> tw((size_t)L * p->nb * p->T_eff), ws((size_t)L * p->nb);
   for (int l = 0; l < L; ++l)
-    for (int b = 0; b < p->nb; ++b)
+    for (int b = 0; b < p->nb; ++b) {
+      long double sr = 0.0L, si = 0.0L;
       for (int t = 0; t < p->T_eff; ++t) {
         double c, s;
         twiddle((long)(lo + b) * t, nfft, &c, &s);
         const double w = tapers ? tapers[(size_t)l * p->T_eff + t] : 1.0;
-        tw[((size_t)l * p->nb + b) * p->T_eff + t] = make_double2(w * c, w * s);
+        const double2 v = make_double2(w * c, w * s);
+        tw[((size_t)l * p->nb + b) * p->T_eff + t] = v;
+        sr += v.x;
+        si += v.y;
       }
+      ws[(size_t)l * p->nb + b] = make_double2((double)sr, (double)si);
+    }
   const int64_t P = (int64_t)N * (N - 1) / 2;
   int64_t cap = P * p->nb / 64;
   if (cap < (1 << 16)) cap = 1 << 16;
@@ -207,10 +213,12 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   p->flag_cap = (int)cap;
   const size_t ring = (size_t)slot_cap * L * p->nb * N;
   bool ok = cudaMalloc(&p->tww, tw.size() * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&p->wsum, ws.size() * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&p->X64, ring * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&p->X32, ring * sizeof(float2)) == cudaSuccess &&
             cudaMalloc(&p->psd, (size_t)p->nb * N * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&p->mag, (size_t)p->nb * N * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&p->nscale, (size_t)p->nb * N * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&p->flags, (size_t)p->flag_cap * sizeof(int4)) == cudaSuccess &&
             cudaMalloc(&p->counters, 4 * sizeof(int)) == cudaSuccess;
   if (!ok) {
@@ -220,6 +228,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
     return CS_ENOMEM;
   }
   cudaMemcpy(p->tww, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->wsum, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice);
   cudaMemset(p->X64, 0, ring * sizeof(double2));
   cudaMemset(p->X32, 0, ring * sizeof(float2));
   cudaMemset(p->counters, 0, 4 * sizeof(int));
@@ -234,7 +243,8 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
 int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   DeviceGuard g(p->device);
-  cudaFree(p->tww); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag);
+  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
+  if (p->tc_ops) cudaFree(p->tc_ops);
   cudaFree(p->flags); cudaFree(p->counters);
   if (p->prof) {
     auto* ps = (ProfState*)p->prof;

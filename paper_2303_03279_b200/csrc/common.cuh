@@ -21,10 +21,14 @@ struct Plan {
   float scale = 1.f;             // power of two applied to the fp32 spectra
   int dc_local = -1, nyq_local = -1;  // plan-local indices of exactly-real bins
   double2* tww = nullptr;        // [L][nb][T_eff]   taper x twiddle
+  double2* wsum = nullptr;       // [L][nb]          sum_t tww (mean correction)
   double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
   float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra
   float* psd = nullptr;          // [nb][N] per-call node statistics
   float* mag = nullptr;          // [nb][N] max_k sqrt(sum_l |X|^2)
+  float* nscale = nullptr;       // [nb][N] 2^-ceil(log2 mag): per-node-bin fp16 operand scale
+  void* tc_ops = nullptr;        // tensor-core operand planes (grown on demand)
+  size_t tc_bytes = 0;
   int4* flags = nullptr;         // fp64-fallback work list (i, j, local bin, -)
   int* counters = nullptr;       // [0] flag count, [1] overflow
   int flag_cap = 0;

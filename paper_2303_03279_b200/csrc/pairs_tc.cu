@@ -1,0 +1,417 @@
+// K2: the coherency family (COH, COHY, PLV) as complex-as-real tcgen05 tensor-core
+// contractions over trials, per frequency bin, on 128 x 128 node tiles of the
+// upper-triangular pair space.
+//
+// Reference: spectral.py:204-241 (CSD = X_i conj X_j and unit phasor sums),
+// metrics.py:32-56 (cohy/coh/plv finalisers), metrics.py:115-134 (band mean).
+//
+// Per bin b and tile (I, J) the kernel accumulates, in TMEM (fp32),
+//   D_re = sum_k Re X_i Re X_j + Im X_i Im X_j      D_im = sum_k Im X_i Re X_j - Re X_i Im X_j
+// for X (pass 0: cross-spectra) and for the unit phasors U = X/|X| (pass 1: PLV).
+// Operands are fp16 hi/lo splits (x = h + l, |x| <= 1 after a per-node-bin power
+// of two) so each real product is h*h + h*l + l*h: ~22-bit products on the f16
+// tensor path (the plain fp16/bf16/tf32 product misses the 1e-4 COH tolerance;
+// SURVEY.md section 7, hard part 2).  The subtraction in D_im uses the
+// instruction descriptor's A-negate bit, so no negated copies are stored.
+//
+// Pipeline (warp specialised, one CTA per tile, all bins and both passes):
+//   warp 0: TMA producer (cp.async.bulk.tensor, 64B swizzle) into a 3-stage ring
+//   warp 1: single-thread tcgen05.mma issuer, tcgen05.commit to mbarriers
+//   warp 2: TMEM allocator (512 columns: pass 0 -> [0,256), pass 1 -> [256,512))
+//   warps 4-7: epilogue (tcgen05.ld 32x32b, one TMEM lane quadrant per warp)
+// The two passes use disjoint TMEM regions, so the epilogue of one pass overlaps
+// the MMAs of the next.
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int kTcTile = 128;          // node tile edge (M = N = 128)
+constexpr int kTcChunk = 32;          // trials per stage (64-byte fp16 rows)
+constexpr int kTcStages = 3;
+constexpr int kTcPlaneBytes = kTcTile * kTcChunk * 2;   // 8 KB
+constexpr int kTcStageBytes = 8 * kTcPlaneBytes;        // A: 4 planes, B: 4 planes
+constexpr int kTcThreads = 256;
+
+struct TcArgs {
+  int N, K, K_pad, nbb;
+  int i_lo, i_hi;            // row range [i_lo, i_hi) of pairs computed (shard)
+  int tile_row0, n_tiles;    // first 128-row tile and number of tiles in the launch
+  int nt;                    // 128-node tiles over N
+  const float* psd;          // [nbb][N] plan-scaled sum_k |X|^2
+  const float* nscale;       // [nbb][N] per-node-bin power of two used for the fp16 split
+  float invK;
+  int64_t pair_base, pair_stride;
+  float* coh_bins;  float* coh_band;
+  float2* cohy_bins; float2* cohy_band;
+  float* plv_bins;  float* plv_band;
+  int do_x, do_u;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(smem)), "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+// K-major operand tile [128 rows x 32 fp16] written by TMA with SWIZZLE_64B:
+// 64-byte rows, 8-row core groups 512 B apart (SBO), LBO unused, descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                             // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;                    // SBO
+  d |= (uint64_t)1 << 46;                             // version (Blackwell)
+  d |= (uint64_t)4 << 61;                             // SWIZZLE_64B
+  return d;
+}
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, K-major A and B, M = N = 128
+__host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
+  return (1u << 4)                     // D format f32
+         | (0u << 7) | (0u << 10)      // A, B format f16
+         | ((neg_a ? 1u : 0u) << 13)   // negate A
+         | ((uint32_t)(kTcTile >> 3) << 17)   // N >> 3
+         | ((uint32_t)(kTcTile >> 4) << 24);  // M >> 4
+}
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + kTcStages * kTcStageBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* tfull = empty + kTcStages;   // [2] per pass region
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // tile decode over the 128-node upper triangle, rows from tile_row0
+  int I, J;
+  decode_tile(blockIdx.x, a.nt, a.tile_row0, I, J);
+  const int iBase = I * kTcTile, jBase = J * kTcTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(&tfull[r], 1);
+      mbar_init(&tempty[r], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_chunk = a.K_pad / kTcChunk;
+  const int npass = a.do_x + a.do_u;
+  const int pass0 = a.do_x ? 0 : 1;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int bl = 0; bl < a.nbb; ++bl)
+        for (int ps = 0; ps < npass; ++ps) {
+          const int pass = pass0 + ps;
+          for (int c = 0; c < n_chunk; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            unsigned char* st = smem + stage * kTcStageBytes;
+            mbar_expect_tx(&full[stage], kTcStageBytes);
+            for (int pl = 0; pl < 4; ++pl) {
+              const int z = (bl * 2 + pass) * 4 + pl;
+              tma_load_3d(st + pl * kTcPlaneBytes, &gmap, &full[stage], c * kTcChunk, iBase, z);
+              tma_load_3d(st + (4 + pl) * kTcPlaneBytes, &gmap, &full[stage], c * kTcChunk, jBase, z);
+            }
+            if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+          }
+        }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // (A plane, B plane, negate A) for D_re and D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l
+      const int prod_a[12] = {0, 0, 1, 2, 2, 3, /* im */ 2, 2, 3, 0, 0, 1};
+      const int prod_b[12] = {0, 1, 0, 2, 3, 2, /* im */ 0, 1, 0, 2, 3, 2};
+      const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t tuse[2] = {0, 0};
+      for (int bl = 0; bl < a.nbb; ++bl)
+        for (int ps = 0; ps < npass; ++ps) {
+          const int pass = pass0 + ps;
+          const int reg = ps;  // TMEM region alternates with the pass slot
+          mbar_wait(&tempty[reg], (tuse[reg] & 1) ^ 1);
+          ++tuse[reg];
+          tc_fence_after();
+          const uint32_t d_re = tmem + reg * 256, d_im = d_re + 128;
+          for (int c = 0; c < n_chunk; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + stage * kTcStageBytes);
+#pragma unroll
+            for (int s = 0; s < kTcChunk / 16; ++s)
+#pragma unroll
+              for (int q = 0; q < 12; ++q) {
+                const uint64_t ad = umma_desc_sw64(base + prod_a[q] * kTcPlaneBytes + s * 32);
+                const uint64_t bd = umma_desc_sw64(base + (4 + prod_b[q]) * kTcPlaneBytes + s * 32);
+                const bool first = (c == 0 && s == 0 && (q == 0 || q == 6));
+                tc_mma(q < 6 ? d_re : d_im, ad, bd, (q >= 9) ? id_neg : id_pos, first ? 0u : 1u);
+              }
+            tc_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+            if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+          }
+          tc_commit(&tfull[reg]);      // accumulators of (bin, pass) complete
+          (void)pass;
+        }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;                  // TMEM lane quadrant
+    const int i = iBase + q * 32 + lane;     // this thread's row
+    const bool row_ok = i >= a.i_lo && i < a.i_hi && i < a.N;
+    const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+    const float inv_nb = 1.f / (float)a.nbb;
+    uint32_t tuse[2] = {0, 0};
+    for (int bl = 0; bl < a.nbb; ++bl) {
+      const float psd_i = row_ok ? a.psd[(int64_t)bl * a.N + i] : 0.f;
+      const float s_i = row_ok ? a.nscale[(int64_t)bl * a.N + i] : 0.f;
+      const float pi = psd_i * s_i * s_i;
+      const int64_t bo = (int64_t)bl * a.pair_stride;
+      for (int ps = 0; ps < npass; ++ps) {
+        const int pass = pass0 + ps;
+        const int reg = ps;
+        mbar_wait(&tfull[reg], tuse[reg] & 1);
+        ++tuse[reg];
+        tc_fence_after();
+        const uint32_t t_re = tmem + ((uint32_t)(q * 32) << 16) + reg * 256;
+        for (int c0 = 0; c0 < kTcTile; c0 += 16) {
+          float vr[16], vi[16];
+          tmem_ld16(t_re + c0, vr);
+          tmem_ld16(t_re + 128 + c0, vi);
+          if (!row_ok) continue;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = jBase + c0 + u;
+            if (j <= i || j >= a.N) continue;
+            const int64_t po = rowoff + j;
+            if (pass == 0) {
+              const float psd_j = a.psd[(int64_t)bl * a.N + j];
+              const float s_j = a.nscale[(int64_t)bl * a.N + j];
+              const float pp = pi * psd_j * s_j * s_j;
+              const float r = pp > 0.f ? rsqrtf(pp) : 0.f;
+              const float cr = vr[u] * r, ci = vi[u] * r;
+              const float coh = sqrtf(cr * cr + ci * ci);
+              if (a.coh_bins) a.coh_bins[bo + po] = coh;
+              if (a.cohy_bins) a.cohy_bins[bo + po] = make_float2(cr, ci);
+              if (a.coh_band) a.coh_band[po] = (bl ? a.coh_band[po] : 0.f) + coh * inv_nb;
+              if (a.cohy_band) {
+                float2 o = bl ? a.cohy_band[po] : make_float2(0.f, 0.f);
+                a.cohy_band[po] = make_float2(o.x + cr * inv_nb, o.y + ci * inv_nb);
+              }
+            } else {
+              const float plv = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
+              if (a.plv_bins) a.plv_bins[bo + po] = plv;
+              if (a.plv_band) a.plv_band[po] = (bl ? a.plv_band[po] : 0.f) + plv * inv_nb;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[reg]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- operand prep
+// G[z = (bl*2 + pass)*4 + plane][n][k] fp16, k < K_pad (zero padded):
+//   pass 0: X * 2^-e(n,b) (|.| <= 1), pass 1: U = X/|X|; planes re_h, re_l, im_h, im_l.
+__global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int K_pad,
+                          int N, int nb, int L, int bin_lo, int nbb, const float* __restrict__ nscale,
+                          __half* __restrict__ G) {
+  const int k = blockIdx.x * 32 + threadIdx.x;
+  const int n = blockIdx.y * 8 + threadIdx.y;
+  const int bl = blockIdx.z;
+  if (n >= N || k >= K_pad) return;
+  float xr = 0.f, xi = 0.f;
+  if (k < K) {
+    const float2 v = X32[(((int64_t)slots[k] * L) * nb + bin_lo + bl) * N + n];
+    const float s = nscale[(int64_t)bl * N + n];
+    xr = v.x * s;
+    xi = v.y * s;
+  }
+  const float m2 = xr * xr + xi * xi;
+  const float inv = m2 > 0.f ? rsqrtf(m2) : 0.f;
+  float vals[2][2] = {{xr, xi}, {xr * inv, xi * inv}};
+  const size_t plane = (size_t)N * K_pad;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float v = vals[pass][c];
+      const __half h = __float2half_rn(v);
+      const __half l = __float2half_rn(v - __half2float(h));
+      const size_t z = ((size_t)bl * 2 + pass) * 4 + c * 2;
+      G[(z + 0) * plane + (size_t)n * K_pad + k] = h;
+      G[(z + 1) * plane + (size_t)n * K_pad + k] = l;
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+size_t tc_smem_bytes() { return (size_t)kTcStages * kTcStageBytes + 1024 + 256; }
+
+bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
+                  const cs_outputs* out, const float* nscale, cudaStream_t st) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    cs_set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  const int K_pad = (K + kTcChunk - 1) / kTcChunk * kTcChunk;
+  const size_t need = (size_t)nbb * 8 * p.N * K_pad * sizeof(__half);
+  if (need > p.tc_bytes) {
+    if (p.tc_ops) cudaFreeAsync(p.tc_ops, st);
+    if (cudaMallocAsync(&p.tc_ops, need, st) != cudaSuccess) {
+      cs_set_error("device allocation failed (tensor-core operands %zu bytes)", need);
+      p.tc_ops = nullptr;
+      p.tc_bytes = 0;
+      return false;
+    }
+    p.tc_bytes = need;
+  }
+  __half* G = (__half*)p.tc_ops;
+  {
+    PhaseMark ph(p, "tc_prep", st);
+    dim3 grid(K_pad / 32, (p.N + 7) / 8, nbb);
+    k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, K, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
+  }
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 8};
+  cuuint64_t strides[2] = {(cuuint64_t)K_pad * 2, (cuuint64_t)p.N * K_pad * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTile, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, G, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    cs_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return false;
+  }
+  TcArgs a{};
+  a.N = p.N; a.K = K; a.K_pad = K_pad; a.nbb = nbb;
+  a.i_lo = rb * kTile;
+  a.i_hi = re * kTile < p.N ? re * kTile : p.N;
+  a.nt = (p.N + kTcTile - 1) / kTcTile;
+  a.tile_row0 = a.i_lo / kTcTile;
+  const int tile_row1 = (a.i_hi + kTcTile - 1) / kTcTile;
+  int64_t n_tiles = 0;
+  for (int t = a.tile_row0; t < tile_row1; ++t) n_tiles += a.nt - t;
+  a.psd = p.psd; a.nscale = nscale;
+  a.invK = 1.f / (float)K;
+  a.pair_base = out->pair_base; a.pair_stride = out->pair_stride;
+  a.cohy_bins = do_x ? (float2*)out->bins[0] : nullptr;
+  a.cohy_band = do_x ? (float2*)out->band[0] : nullptr;
+  a.coh_bins = do_x ? (float*)out->bins[1] : nullptr;
+  a.coh_band = do_x ? (float*)out->band[1] : nullptr;
+  a.plv_bins = do_u ? (float*)out->bins[3] : nullptr;
+  a.plv_band = do_u ? (float*)out->band[3] : nullptr;
+  a.do_x = do_x; a.do_u = do_u;
+  const size_t smem = tc_smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_pairs_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  {
+    PhaseMark ph(p, "pairs_tc", st);
+    k_pairs_tc<<<(unsigned)n_tiles, kTcThreads, smem, st>>>(map, a);
+  }
+  return true;
+}
+
+}  // namespace cs

@@ -15,17 +15,37 @@
 
 namespace cs {
 
-constexpr int kSpecNodes = 128;
-constexpr int kSpecChunk = 32;
+constexpr int kSpecNodes = 128;   // one thread per node
+constexpr int kSpecRowBytes = 128; // staged samples per row per chunk (32 fp32 / 16 fp64)
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Single pass over the samples.  With d_t = x_t - c (c = first sample of the row,
+// exact in fp64 for fp32 input) the demeaned, tapered DFT is
+//   X_b = sum_t (d_t - mean(d)) w_t e_bt = Y_b - mean(d) W_b,  Y_b = sum_t d_t tww_bt,
+// W_b = sum_t tww_bt (host, long double), so the mean never needs a second read.
 template <typename Tin, int NBT>
 __global__ void __launch_bounds__(kSpecNodes)
 k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N,
-          int T_eff, int nb, int L, const double2* __restrict__ tww, int slot0, int slot_cap,
-          double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local,
-          int nyq_local) {
-  __shared__ double sx[kSpecChunk][kSpecNodes + 1];
-  __shared__ double2 stw[NBT][kSpecChunk];
+          int T_eff, int nb, int L, const double2* __restrict__ tww, const double2* __restrict__ wsum,
+          int slot0, int slot_cap, double2* __restrict__ X64, float2* __restrict__ X32, float scale,
+          int dc_local, int nyq_local, int vec16) {
+  constexpr int TC = kSpecRowBytes / sizeof(Tin);            // samples per chunk
+  constexpr int RS = TC + 16 / sizeof(Tin);                   // padded row stride (conflict-free LDS.128)
+  extern __shared__ __align__(16) unsigned char spec_smem[];
+  Tin* sx = (Tin*)spec_smem;                                  // [2][128][RS]
+  double2* stw = (double2*)(spec_smem + 2 * kSpecNodes * RS * sizeof(Tin));  // [2][NBT][TC]
+
   const int tid = threadIdx.x;
   const int n0 = blockIdx.x * kSpecNodes;
   const int b0 = blockIdx.y * NBT;
@@ -33,72 +53,112 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
   const int l = blockIdx.z % L;
   const int nbt = min(NBT, nb - b0);
   const Tin* xk = x + (int64_t)k * trial_stride;
+  const double2* twl = tww + ((int64_t)l * nb + b0) * T_eff;
+  const int n_chunk = (T_eff + TC - 1) / TC;
 
-  // ---- pass 1: per-node mean over the real samples (fp64) ----
-  double sum = 0.0;
-  for (int t0 = 0; t0 < T_eff; t0 += kSpecChunk) {
+  auto issue = [&](int ch, int buf) {
+    const int t0 = ch * TC;
+    Tin* dst = sx + buf * kSpecNodes * RS;
+    if (vec16) {
+      constexpr int PER_ROW = kSpecRowBytes / 16;   // 16-byte pieces per row
+      constexpr int EPP = 16 / sizeof(Tin);         // elements per piece
 #pragma unroll 4
-    for (int q = 0; q < kSpecChunk; ++q) {
-      int e = tid + kSpecNodes * q;
-      int row = e / kSpecChunk, col = e % kSpecChunk;
-      int n = n0 + row, t = t0 + col;
-      double v = 0.0;
-      if (n < N && t < T_eff) v = (double)xk[(int64_t)n * node_stride + t];
-      sx[col][row] = v;
+      for (int q = 0; q < PER_ROW; ++q) {
+        const int e = tid + kSpecNodes * q;
+        const int row = e / PER_ROW, piece = e % PER_ROW;
+        const int n = n0 + row, t = t0 + piece * EPP;
+        int bytes = 0;
+        if (n < N && t < T_eff) bytes = min(EPP, T_eff - t) * (int)sizeof(Tin);
+        const Tin* src = bytes ? xk + (int64_t)n * node_stride + t : xk;
+        cp_async16(dst + row * RS + piece * EPP, src, bytes);
+      }
+    } else {
+      for (int q = 0; q < TC; ++q) {
+        const int e = tid + kSpecNodes * q;
+        const int row = e / TC, col = e % TC;
+        const int n = n0 + row, t = t0 + col;
+        const bool ok = n < N && t < T_eff;
+        const Tin* src = ok ? xk + (int64_t)n * node_stride + t : xk;
+        if (sizeof(Tin) == 4) {
+          cp_async4(dst + row * RS + col, src, ok ? 4 : 0);
+        } else {
+          cp_async4(dst + row * RS + col, src, ok ? 4 : 0);
+          cp_async4((char*)(dst + row * RS + col) + 4, (const char*)src + 4, ok ? 4 : 0);
+        }
+      }
     }
-    __syncthreads();
-#pragma unroll 8
-    for (int t = 0; t < kSpecChunk; ++t) sum += sx[t][tid];
-    __syncthreads();
-  }
-  const double mean = sum / (double)T_eff;
+    double2* tdst = stw + buf * NBT * TC;
+    for (int e = tid; e < NBT * TC; e += kSpecNodes) {
+      const int j = e / TC, t = e % TC;
+      const bool ok = j < nbt && t0 + t < T_eff;
+      cp_async16(tdst + e, ok ? (const void*)(twl + (int64_t)j * T_eff + t0 + t) : (const void*)twl, ok ? 16 : 0);
+    }
+    cp_async_commit();
+  };
 
-  // ---- pass 2: demeaned, tapered DFT over the plan bins ----
   double are[NBT], aim[NBT];
 #pragma unroll
   for (int j = 0; j < NBT; ++j) are[j] = aim[j] = 0.0;
-  __shared__ double smean[kSpecNodes];
-  smean[tid] = mean;
-  __syncthreads();
-  const double2* twl = tww + (int64_t)l * nb * T_eff;
-  for (int t0 = 0; t0 < T_eff; t0 += kSpecChunk) {
-#pragma unroll 4
-    for (int q = 0; q < kSpecChunk; ++q) {
-      int e = tid + kSpecNodes * q;
-      int row = e / kSpecChunk, col = e % kSpecChunk;
-      int n = n0 + row, t = t0 + col;
-      double v = 0.0;
-      if (n < N && t < T_eff) v = (double)xk[(int64_t)n * node_stride + t] - smean[row];
-      sx[col][row] = v;
-    }
-    for (int e = tid; e < NBT * kSpecChunk; e += kSpecNodes) {
-      int j = e / kSpecChunk, t = e % kSpecChunk;
-      double2 w = make_double2(0.0, 0.0);
-      if (j < nbt && t0 + t < T_eff) w = twl[(int64_t)(b0 + j) * T_eff + t0 + t];
-      stw[j][t] = w;
+  double c = 0.0, sum = 0.0;
+
+  issue(0, 0);
+  for (int ch = 0; ch < n_chunk; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < n_chunk) {
+      issue(ch + 1, buf ^ 1);
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
     }
     __syncthreads();
-#pragma unroll 4
-    for (int t = 0; t < kSpecChunk; ++t) {
-      const double v = sx[t][tid];
+    const Tin* row = sx + buf * kSpecNodes * RS + tid * RS;
+    const double2* tw = stw + buf * NBT * TC;
+    if (ch == 0) c = (double)row[0];
+    const int tn = min(TC, T_eff - ch * TC);
+    double csum = 0.0;
+    if (tn == TC) {
+#pragma unroll 2
+      for (int t = 0; t < TC; t += 16 / (int)sizeof(Tin)) {
+        Tin v[16 / sizeof(Tin)];
+        *(float4*)v = *(const float4*)(row + t);
 #pragma unroll
-      for (int j = 0; j < NBT; ++j) {
-        const double2 w = stw[j][t];
-        are[j] = fma(v, w.x, are[j]);
-        aim[j] = fma(v, w.y, aim[j]);
+        for (int u = 0; u < (int)(16 / sizeof(Tin)); ++u) {
+          const double d = (double)v[u] - c;
+          csum += d;
+#pragma unroll
+          for (int j = 0; j < NBT; ++j) {
+            const double2 w = tw[j * TC + t + u];
+            are[j] = fma(d, w.x, are[j]);
+            aim[j] = fma(d, w.y, aim[j]);
+          }
+        }
+      }
+    } else {
+      for (int t = 0; t < tn; ++t) {
+        const double d = (double)row[t] - c;
+        csum += d;
+#pragma unroll
+        for (int j = 0; j < NBT; ++j) {
+          const double2 w = tw[j * TC + t];
+          are[j] = fma(d, w.x, are[j]);
+          aim[j] = fma(d, w.y, aim[j]);
+        }
       }
     }
+    sum += csum;
     __syncthreads();
   }
 
   const int n = n0 + tid;
   if (n >= N) return;
+  const double mean = sum / (double)T_eff;
   const int slot = (slot0 + k) % slot_cap;
 #pragma unroll
   for (int j = 0; j < NBT; ++j) {
     if (j >= nbt) break;
     const int b = b0 + j;
-    double re = are[j], im = aim[j];
+    const double2 W = wsum[(int64_t)l * nb + b];
+    double re = fma(-mean, W.x, are[j]), im = fma(-mean, W.y, aim[j]);
     if (b == dc_local) re = im = 0.0;       // spectral.py:96: DC is exactly zero
     if (b == nyq_local) im = 0.0;           // Nyquist of a real signal is real
     const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
@@ -110,16 +170,26 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
 template <typename Tin, int NBT>
 static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0,
                            int kc, cudaStream_t st) {
+  constexpr int TC = kSpecRowBytes / sizeof(Tin);
+  constexpr int RS = TC + 16 / sizeof(Tin);
+  const size_t smem = 2 * kSpecNodes * RS * sizeof(Tin) + 2 * NBT * TC * sizeof(double2);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_spectra<Tin, NBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int vec16 = ((uintptr_t)x % 16 == 0) && ((ns * (int64_t)sizeof(Tin)) % 16 == 0) &&
+                    ((ts * (int64_t)sizeof(Tin)) % 16 == 0);
   dim3 grid((p.N + kSpecNodes - 1) / kSpecNodes, (p.nb + NBT - 1) / NBT, kc * p.L);
-  k_spectra<Tin, NBT><<<grid, kSpecNodes, 0, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
-                                                    p.L, p.tww, slot0, p.slot_cap, p.X64, p.X32,
-                                                    p.scale, p.dc_local, p.nyq_local);
+  k_spectra<Tin, NBT><<<grid, kSpecNodes, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
+                                                       p.L, p.tww, p.wsum, slot0, p.slot_cap, p.X64,
+                                                       p.X32, p.scale, p.dc_local, p.nyq_local, vec16);
 }
 
 template <typename Tin>
 static void dispatch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0,
                              int kc, cudaStream_t st) {
-  // pick the per-thread bin count: wide bands use 16-bin chunks on gridDim.y
+  // per-thread bin count: wide bands use 16-bin chunks on gridDim.y
   switch (p.nb) {
     case 1: launch_spectra<Tin, 1>(p, x, ts, ns, slot0, kc, st); break;
     case 2: launch_spectra<Tin, 2>(p, x, ts, ns, slot0, kc, st); break;
@@ -150,7 +220,7 @@ void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns
 // mag = max_k sqrt(sum_l |X|^2), the bound used by the exact-sign guard.
 __global__ void k_node_stats(const float2* __restrict__ X32, const int* __restrict__ slots,
                              int K, int N, int nb, int L, int bin_lo, int nbb,
-                             float* __restrict__ psd, float* __restrict__ mag) {
+                             float* __restrict__ psd, float* __restrict__ mag, float* __restrict__ nscale) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int bl = blockIdx.y;  // 0..nbb-1
   if (n >= N) return;
@@ -169,12 +239,15 @@ __global__ void k_node_stats(const float2* __restrict__ X32, const int* __restri
   }
   psd[(int64_t)bl * N + n] = (float)s;
   mag[(int64_t)bl * N + n] = m;
+  int e = 0;
+  if (m > 0.f) frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)  ->  m * 2^-e <= 1
+  nscale[(int64_t)bl * N + n] = m > 0.f ? ldexpf(1.f, -e) : 1.f;
 }
 
 void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb,
                     cudaStream_t st) {
   dim3 grid((p.N + 127) / 128, nbb);
-  k_node_stats<<<grid, 128, 0, st>>>(p.X32, slots, K, p.N, p.nb, p.L, bin_lo, nbb, p.psd, p.mag);
+  k_node_stats<<<grid, 128, 0, st>>>(p.X32, slots, K, p.N, p.nb, p.L, bin_lo, nbb, p.psd, p.mag, p.nscale);
 }
 
 // complex128 [n_slots][N][nbins] copy-out of the fp64 ring (taper 0), trial_spectra layout.
