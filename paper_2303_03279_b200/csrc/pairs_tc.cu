@@ -17,8 +17,11 @@
 // Pipeline (warp specialised, one CTA per tile, all bins and both passes):
 //   warp 0: TMA producer (cp.async.bulk.tensor, 64B swizzle) into a 3-stage ring
 //   warp 1: single-thread tcgen05.mma issuer, tcgen05.commit to mbarriers
-//   warp 2: TMEM allocator (512 columns: pass 0 -> [0,256), pass 1 -> [256,512))
-//   warps 4-7: epilogue (tcgen05.ld 32x32b, one TMEM lane quadrant per warp)
+//   warp 2: TMEM allocator (512 columns: pass 0 -> [0,128), pass 1 -> [128,256),
+//           band-mean accumulators -> [256,512))
+//   warps 4-7: epilogue (tcgen05.ld/st 32x32b, one TMEM lane quadrant per warp),
+//           per-bin values leave through a shared-memory transpose buffer as
+//           coalesced row stores; band means accumulate in TMEM across bins.
 // The two passes use disjoint TMEM regions, so the epilogue of one pass overlaps
 // the MMAs of the next.
 #include <cuda.h>
@@ -28,18 +31,24 @@
 
 namespace cs {
 
-constexpr int kTcTile = 128;          // node tile edge (M = N = 128)
+constexpr int kTcTile = 128;          // i rows per tile (UMMA M)
+constexpr int kTcTileJ = 64;          // j columns per tile (UMMA N)
 constexpr int kTcChunk = 32;          // trials per stage (64-byte fp16 rows)
 constexpr int kTcStages = 3;
-constexpr int kTcPlaneBytes = kTcTile * kTcChunk * 2;   // 8 KB
-constexpr int kTcStageBytes = 8 * kTcPlaneBytes;        // A: 4 planes, B: 4 planes
+constexpr int kTcPlaneA = kTcTile * kTcChunk * 2;       // 8 KB
+constexpr int kTcPlaneB = kTcTileJ * kTcChunk * 2;      // 4 KB
+constexpr int kTcStageBytes = 4 * kTcPlaneA + 4 * kTcPlaneB;  // 48 KB
+constexpr int kTcXStride = kTcTileJ + 1;                // transpose buffer row stride (float2)
 constexpr int kTcThreads = 256;
+// TMEM columns: [0,128) pass-0 accumulators (re | im), [128,256) pass-1,
+// [256,512) band sums: COH, PLV, COHY re, COHY im (64 each)
+constexpr int kTmBand = 256;
 
 struct TcArgs {
   int N, K, K_pad, nbb;
   int i_lo, i_hi;            // row range [i_lo, i_hi) of pairs computed (shard)
   int tile_row0, n_tiles;    // first 128-row tile and number of tiles in the launch
-  int nt;                    // 128-node tiles over N
+  int nt;                    // 64-node column tiles over N
   const float* psd;          // [nbb][N] plan-scaled sum_k |X|^2
   const float* nscale;       // [nbb][N] per-node-bin power of two used for the fp16 split
   float invK;
@@ -123,27 +132,73 @@ __host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
   return (1u << 4)                     // D format f32
          | (0u << 7) | (0u << 10)      // A, B format f16
          | ((neg_a ? 1u : 0u) << 13)   // negate A
-         | ((uint32_t)(kTcTile >> 3) << 17)   // N >> 3
+         | ((uint32_t)(kTcTileJ >> 3) << 17)  // N >> 3
          | ((uint32_t)(kTcTile >> 4) << 24);  // M >> 4
 }
 
 // ---------------------------------------------------------------- the kernel
+// Tile (I, J): rows i in [128 I, 128 I + 128), columns j in [64 J, 64 J + 64),
+// J >= 2 I (upper triangle).  decode over the row range starting at tile_row0.
+__device__ __forceinline__ void decode_tc_tile(int64_t t, int nt64, int row0, int& I, int& J) {
+  int r = row0;
+  int64_t left = t;
+  while (left >= nt64 - 2 * r) {
+    left -= nt64 - 2 * r;
+    ++r;
+  }
+  I = r;
+  J = 2 * r + (int)left;
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])));
+}
+__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// Coalesced store of the [128 rows x 64 cols] transpose buffer: each epilogue warp
+// writes its 32 rows; a row's 64 pairs (i, j..j+63) are contiguous in the output.
+template <typename T>
+__device__ __forceinline__ void store_tile(const T* xb, T* dst, int64_t bin_off, const TcArgs& a, int iBase,
+                                           int jBase, int q, int lane) {
+  for (int rr = 0; rr < 32; ++rr) {
+    const int r = q * 32 + rr;
+    const int i = iBase + r;
+    if (i < a.i_lo || i >= a.i_hi || i >= a.N) continue;
+    const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + bin_off;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      const int j = jBase + c;
+      if (j > i && j < a.N) dst[rowoff + j] = xb[r * kTcXStride + c];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1)
-k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
+k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + kTcStages * kTcStageBytes);
+  float2* xbuf = (float2*)(smem + kTcStages * kTcStageBytes);          // [128][65] transpose buffer
+  float* colfac = (float*)(xbuf + kTcTile * kTcXStride);               // [64] psd_j * s_j^2
+  uint64_t* full = (uint64_t*)(colfac + kTcTileJ);
   uint64_t* empty = full + kTcStages;
   uint64_t* tfull = empty + kTcStages;   // [2] per pass region
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // tile decode over the 128-node upper triangle, rows from tile_row0
   int I, J;
-  decode_tile(blockIdx.x, a.nt, a.tile_row0, I, J);
-  const int iBase = I * kTcTile, jBase = J * kTcTile;
+  decode_tc_tile(blockIdx.x, a.nt, a.tile_row0, I, J);
+  const int iBase = I * kTcTile, jBase = J * kTcTileJ;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -183,8 +238,8 @@ k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
             mbar_expect_tx(&full[stage], kTcStageBytes);
             for (int pl = 0; pl < 4; ++pl) {
               const int z = (bl * 2 + pass) * 4 + pl;
-              tma_load_3d(st + pl * kTcPlaneBytes, &gmap, &full[stage], c * kTcChunk, iBase, z);
-              tma_load_3d(st + (4 + pl) * kTcPlaneBytes, &gmap, &full[stage], c * kTcChunk, jBase, z);
+              tma_load_3d(st + pl * kTcPlaneA, &mapA, &full[stage], c * kTcChunk, iBase, z);
+              tma_load_3d(st + 4 * kTcPlaneA + pl * kTcPlaneB, &mapB, &full[stage], c * kTcChunk, jBase, z);
             }
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
@@ -193,21 +248,21 @@ k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      // (A plane, B plane, negate A) for D_re and D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l
-      const int prod_a[12] = {0, 0, 1, 2, 2, 3, /* im */ 2, 2, 3, 0, 0, 1};
-      const int prod_b[12] = {0, 1, 0, 2, 3, 2, /* im */ 0, 1, 0, 2, 3, 2};
+      // (A plane, B plane) for D_re then D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l;
+      // the last three D_im products are -(Re_i Im_j) via the A-negate bit
+      const int prod_a[12] = {0, 0, 1, 2, 2, 3, 2, 2, 3, 0, 0, 1};
+      const int prod_b[12] = {0, 1, 0, 2, 3, 2, 0, 1, 0, 2, 3, 2};
       const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tuse[2] = {0, 0};
       for (int bl = 0; bl < a.nbb; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
-          const int pass = pass0 + ps;
-          const int reg = ps;  // TMEM region alternates with the pass slot
+          const int reg = ps;
           mbar_wait(&tempty[reg], (tuse[reg] & 1) ^ 1);
           ++tuse[reg];
           tc_fence_after();
-          const uint32_t d_re = tmem + reg * 256, d_im = d_re + 128;
+          const uint32_t d_re = tmem + reg * 128, d_im = d_re + 64;
           for (int c = 0; c < n_chunk; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
@@ -216,8 +271,8 @@ k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
             for (int s = 0; s < kTcChunk / 16; ++s)
 #pragma unroll
               for (int q = 0; q < 12; ++q) {
-                const uint64_t ad = umma_desc_sw64(base + prod_a[q] * kTcPlaneBytes + s * 32);
-                const uint64_t bd = umma_desc_sw64(base + (4 + prod_b[q]) * kTcPlaneBytes + s * 32);
+                const uint64_t ad = umma_desc_sw64(base + prod_a[q] * kTcPlaneA + s * 32);
+                const uint64_t bd = umma_desc_sw64(base + 4 * kTcPlaneA + prod_b[q] * kTcPlaneB + s * 32);
                 const bool first = (c == 0 && s == 0 && (q == 0 || q == 6));
                 tc_mma(q < 6 ? d_re : d_im, ad, bd, (q >= 9) ? id_neg : id_pos, first ? 0u : 1u);
               }
@@ -225,63 +280,165 @@ k_pairs_tc(const __grid_constant__ CUtensorMap gmap, const TcArgs a) {
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
           tc_commit(&tfull[reg]);      // accumulators of (bin, pass) complete
-          (void)pass;
         }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;                  // TMEM lane quadrant
-    const int i = iBase + q * 32 + lane;     // this thread's row
-    const bool row_ok = i >= a.i_lo && i < a.i_hi && i < a.N;
-    const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+    const int r = q * 32 + lane;             // tile row
+    const int i = iBase + r;
     const float inv_nb = 1.f / (float)a.nbb;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t tuse[2] = {0, 0};
+    const bool want_coh = a.coh_bins || a.coh_band, want_cohy = a.cohy_bins || a.cohy_band;
     for (int bl = 0; bl < a.nbb; ++bl) {
-      const float psd_i = row_ok ? a.psd[(int64_t)bl * a.N + i] : 0.f;
-      const float s_i = row_ok ? a.nscale[(int64_t)bl * a.N + i] : 0.f;
-      const float pi = psd_i * s_i * s_i;
       const int64_t bo = (int64_t)bl * a.pair_stride;
+      const bool last = bl + 1 == a.nbb;
+      float pi = 0.f;
+      if (a.do_x) {
+        const int t = threadIdx.x - 128;
+        if (t < kTcTileJ) {
+          const int j = jBase + t;
+          float f = 0.f;
+          if (j < a.N) {
+            const float sj = a.nscale[(int64_t)bl * a.N + j];
+            f = a.psd[(int64_t)bl * a.N + j] * sj * sj;
+          }
+          colfac[t] = f;
+        }
+        if (i < a.N) {
+          const float si = a.nscale[(int64_t)bl * a.N + i];
+          pi = a.psd[(int64_t)bl * a.N + i] * si * si;
+        }
+        epi_bar();
+      }
       for (int ps = 0; ps < npass; ++ps) {
         const int pass = pass0 + ps;
         const int reg = ps;
         mbar_wait(&tfull[reg], tuse[reg] & 1);
         ++tuse[reg];
         tc_fence_after();
-        const uint32_t t_re = tmem + ((uint32_t)(q * 32) << 16) + reg * 256;
-        for (int c0 = 0; c0 < kTcTile; c0 += 16) {
+        const uint32_t t_acc = tmem + lane_addr + reg * 128;
+        // pass 0 -> COH (band col 0..63), COHY (band 128.., 192..); pass 1 -> PLV (band 64..)
+        for (int c0 = 0; c0 < kTcTileJ; c0 += 16) {
           float vr[16], vi[16];
-          tmem_ld16(t_re + c0, vr);
-          tmem_ld16(t_re + 128 + c0, vi);
-          if (!row_ok) continue;
+          tmem_ld16(t_acc + c0, vr);
+          tmem_ld16(t_acc + 64 + c0, vi);
+          if (pass == 0) {
+            float m[16], br[16], bi[16];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int j = jBase + c0 + u;
-            if (j <= i || j >= a.N) continue;
-            const int64_t po = rowoff + j;
-            if (pass == 0) {
-              const float psd_j = a.psd[(int64_t)bl * a.N + j];
-              const float s_j = a.nscale[(int64_t)bl * a.N + j];
-              const float pp = pi * psd_j * s_j * s_j;
-              const float r = pp > 0.f ? rsqrtf(pp) : 0.f;
-              const float cr = vr[u] * r, ci = vi[u] * r;
-              const float coh = sqrtf(cr * cr + ci * ci);
-              if (a.coh_bins) a.coh_bins[bo + po] = coh;
-              if (a.cohy_bins) a.cohy_bins[bo + po] = make_float2(cr, ci);
-              if (a.coh_band) a.coh_band[po] = (bl ? a.coh_band[po] : 0.f) + coh * inv_nb;
-              if (a.cohy_band) {
-                float2 o = bl ? a.cohy_band[po] : make_float2(0.f, 0.f);
-                a.cohy_band[po] = make_float2(o.x + cr * inv_nb, o.y + ci * inv_nb);
+            for (int u = 0; u < 16; ++u) {
+              const float pp = pi * colfac[c0 + u];
+              const float rs = pp > 0.f ? rsqrtf(pp) : 0.f;
+              vr[u] *= rs;
+              vi[u] *= rs;
+              m[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]);
+              xbuf[r * kTcXStride + c0 + u] = make_float2(vr[u], vi[u]);
+            }
+            if (a.coh_band) {
+              float b[16];
+              if (bl) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
+#pragma unroll
+              for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + m[u] * inv_nb;
+              tmem_st16(tmem + lane_addr + kTmBand + c0, b);
+            }
+            if (a.cohy_band) {
+              if (bl) {
+                tmem_ld16(tmem + lane_addr + kTmBand + 128 + c0, br);
+                tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
               }
-            } else {
-              const float plv = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
-              if (a.plv_bins) a.plv_bins[bo + po] = plv;
-              if (a.plv_band) a.plv_band[po] = (bl ? a.plv_band[po] : 0.f) + plv * inv_nb;
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                br[u] = (bl ? br[u] : 0.f) + vr[u] * inv_nb;
+                bi[u] = (bl ? bi[u] : 0.f) + vi[u] * inv_nb;
+              }
+              tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
+              tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const float v = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
+              vr[u] = v;
+              xbuf[r * kTcXStride + c0 + u] = make_float2(v, 0.f);
+            }
+            if (a.plv_band) {
+              float b[16];
+              if (bl) tmem_ld16(tmem + lane_addr + kTmBand + 64 + c0, b);
+#pragma unroll
+              for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + vr[u] * inv_nb;
+              tmem_st16(tmem + lane_addr + kTmBand + 64 + c0, b);
             }
           }
         }
+        // accumulators drained: hand the region back to the MMA warp
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[reg]);
+        // per-bin outputs through the transpose buffer (coalesced row stores)
+        epi_bar();
+        if (pass == 0) {
+          if (a.cohy_bins) store_tile<float2>(xbuf, a.cohy_bins, bo, a, iBase, jBase, q, lane);
+          if (a.coh_bins) {
+            for (int rr = 0; rr < 32; ++rr) {
+              const int row = q * 32 + rr, ii = iBase + row;
+              if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
+              const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base + bo;
+              for (int h = 0; h < 2; ++h) {
+                const int c = lane + 32 * h, j = jBase + c;
+                if (j > ii && j < a.N) {
+                  const float2 v = xbuf[row * kTcXStride + c];
+                  a.coh_bins[ro + j] = sqrtf(v.x * v.x + v.y * v.y);
+                }
+              }
+            }
+          }
+        } else if (a.plv_bins) {
+          for (int rr = 0; rr < 32; ++rr) {
+            const int row = q * 32 + rr, ii = iBase + row;
+            if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
+            const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base + bo;
+            for (int h = 0; h < 2; ++h) {
+              const int c = lane + 32 * h, j = jBase + c;
+              if (j > ii && j < a.N) a.plv_bins[ro + j] = xbuf[row * kTcXStride + c].x;
+            }
+          }
+        }
+        epi_bar();
+        (void)want_coh;
+        (void)want_cohy;
+        (void)last;
+      }
+    }
+    // band means: TMEM -> transpose buffer -> coalesced stores
+    if (a.coh_band || a.plv_band || a.cohy_band) {
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      for (int kind = 0; kind < 3; ++kind) {
+        if ((kind == 0 && !a.coh_band) || (kind == 1 && !a.plv_band) || (kind == 2 && !a.cohy_band)) continue;
+        for (int c0 = 0; c0 < kTcTileJ; c0 += 16) {
+          float b0[16], b1[16];
+          tmem_ld16(tmem + lane_addr + kTmBand + (kind == 2 ? 128 : kind * 64) + c0, b0);
+          if (kind == 2) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, b1);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(b0[u], kind == 2 ? b1[u] : 0.f);
+        }
+        epi_bar();
+        if (kind == 2) {
+          store_tile<float2>(xbuf, a.cohy_band, 0, a, iBase, jBase, q, lane);
+        } else {
+          float* dst = kind == 0 ? a.coh_band : a.plv_band;
+          for (int rr = 0; rr < 32; ++rr) {
+            const int row = q * 32 + rr, ii = iBase + row;
+            if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
+            const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base;
+            for (int h = 0; h < 2; ++h) {
+              const int c = lane + 32 * h, j = jBase + c;
+              if (j > ii && j < a.N) dst[ro + j] = xbuf[row * kTcXStride + c].x;
+            }
+          }
+        }
+        epi_bar();
       }
     }
   }
@@ -343,7 +500,9 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-size_t tc_smem_bytes() { return (size_t)kTcStages * kTcStageBytes + 1024 + 256; }
+size_t tc_smem_bytes() {
+  return (size_t)kTcStages * kTcStageBytes + (size_t)kTcTile * kTcXStride * sizeof(float2) + kTcTileJ * 4 + 1024 + 256;
+}
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
                   const cs_outputs* out, const float* nscale, cudaStream_t st) {
@@ -370,14 +529,18 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     dim3 grid(K_pad / 32, (p.N + 7) / 8, nbb);
     k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, K, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
   }
-  CUtensorMap map;
+  CUtensorMap mapA, mapB;
   cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 8};
   cuuint64_t strides[2] = {(cuuint64_t)K_pad * 2, (cuuint64_t)p.N * K_pad * 2};
-  cuuint32_t box[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTile, 1};
+  cuuint32_t boxA[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTile, 1};
+  cuuint32_t boxB[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTileJ, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, G, dims, strides, box, estr,
+  CUresult r = enc(&mapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, G, dims, strides, boxA, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS)
+    r = enc(&mapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, G, dims, strides, boxB, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     cs_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return false;
@@ -386,11 +549,11 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.N = p.N; a.K = K; a.K_pad = K_pad; a.nbb = nbb;
   a.i_lo = rb * kTile;
   a.i_hi = re * kTile < p.N ? re * kTile : p.N;
-  a.nt = (p.N + kTcTile - 1) / kTcTile;
+  a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
   a.tile_row0 = a.i_lo / kTcTile;
   const int tile_row1 = (a.i_hi + kTcTile - 1) / kTcTile;
   int64_t n_tiles = 0;
-  for (int t = a.tile_row0; t < tile_row1; ++t) n_tiles += a.nt - t;
+  for (int t = a.tile_row0; t < tile_row1; ++t) n_tiles += a.nt - 2 * t > 0 ? a.nt - 2 * t : 0;
   a.psd = p.psd; a.nscale = nscale;
   a.invK = 1.f / (float)K;
   a.pair_base = out->pair_base; a.pair_stride = out->pair_stride;
@@ -409,7 +572,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   }
   {
     PhaseMark ph(p, "pairs_tc", st);
-    k_pairs_tc<<<(unsigned)n_tiles, kTcThreads, smem, st>>>(map, a);
+    if (n_tiles > 0) k_pairs_tc<<<(unsigned)n_tiles, kTcThreads, smem, st>>>(mapA, mapB, a);
   }
   return true;
 }
