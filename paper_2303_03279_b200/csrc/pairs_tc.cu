@@ -19,13 +19,16 @@
 //   warp 1: single-thread tcgen05.mma issuer, tcgen05.commit to mbarriers
 //   warp 2: TMEM allocator (512 columns: pass 0 -> [0,128), pass 1 -> [128,256),
 //           band-mean accumulators -> [256,512))
-//   warps 4-7: epilogue (tcgen05.ld/st 32x32b, one TMEM lane quadrant per warp),
+//   warps 4-11: epilogue (tcgen05.ld/st 32x32b; TMEM lane quadrant = warp % 4,
+//           two warps per quadrant split the 64 columns),
 //           per-bin values leave through a shared-memory transpose buffer as
 //           coalesced row stores; band means accumulate in TMEM across bins.
 // The two passes use disjoint TMEM regions, so the epilogue of one pass overlaps
 // the MMAs of the next.
 #include <cuda.h>
 #include <cuda_fp16.h>
+
+#include <vector>
 
 #include "common.cuh"
 
@@ -39,7 +42,8 @@ constexpr int kTcPlaneA = kTcTile * kTcChunk * 2;       // 8 KB
 constexpr int kTcPlaneB = kTcTileJ * kTcChunk * 2;      // 4 KB
 constexpr int kTcStageBytes = 4 * kTcPlaneA + 4 * kTcPlaneB;  // 48 KB
 constexpr int kTcXStride = kTcTileJ + 1;                // transpose buffer row stride (float2)
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 384;   // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-11: epilogue
+constexpr int kTcEpiWarps = 8;
 // TMEM columns: [0,128) pass-0 accumulators (re | im), [128,256) pass-1,
 // [256,512) band sums: COH, PLV, COHY re, COHY im (64 each)
 constexpr int kTmBand = 256;
@@ -48,6 +52,7 @@ struct TcArgs {
   int N, K, K_pad, nbb;
   int i_lo, i_hi;            // row range [i_lo, i_hi) of pairs computed (shard)
   int tile_row0, n_tiles;    // first 128-row tile and number of tiles in the launch
+  const int2* tiles;         // (I, J) per CTA, L2-friendly grouped order
   int nt;                    // 64-node column tiles over N
   const float* psd;          // [nbb][N] plan-scaled sum_k |X|^2
   const float* nscale;       // [nbb][N] per-node-bin power of two used for the fp16 split
@@ -160,27 +165,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
       "r"(__float_as_uint(v[15])));
 }
-__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-}
-
-// Coalesced store of the [128 rows x 64 cols] transpose buffer: each epilogue warp
-// writes its 32 rows; a row's 64 pairs (i, j..j+63) are contiguous in the output.
-template <typename T>
-__device__ __forceinline__ void store_tile(const T* xb, T* dst, int64_t bin_off, const TcArgs& a, int iBase,
-                                           int jBase, int q, int lane) {
-  for (int rr = 0; rr < 32; ++rr) {
-    const int r = q * 32 + rr;
-    const int i = iBase + r;
-    if (i < a.i_lo || i >= a.i_hi || i >= a.N) continue;
-    const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + bin_off;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      const int j = jBase + c;
-      if (j > i && j < a.N) dst[rowoff + j] = xb[r * kTcXStride + c];
-    }
-  }
+__device__ __forceinline__ void epi_bar() {  // the epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kTcEpiWarps * 32) : "memory");
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -189,16 +175,16 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   unsigned char* smem = (unsigned char*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
   float2* xbuf = (float2*)(smem + kTcStages * kTcStageBytes);          // [128][65] transpose buffer
   float* colfac = (float*)(xbuf + kTcTile * kTcXStride);               // [64] psd_j * s_j^2
-  uint64_t* full = (uint64_t*)(colfac + kTcTileJ);
+  int64_t* rowoff_s = (int64_t*)(colfac + kTcTileJ);                   // [128] output row offsets
+  uint64_t* full = (uint64_t*)(rowoff_s + kTcTile);
   uint64_t* empty = full + kTcStages;
   uint64_t* tfull = empty + kTcStages;   // [2] per pass region
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int I, J;
-  decode_tc_tile(blockIdx.x, a.nt, a.tile_row0, I, J);
-  const int iBase = I * kTcTile, jBase = J * kTcTileJ;
+  const int2 tij = a.tiles[blockIdx.x];
+  const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -207,7 +193,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     }
     for (int r = 0; r < 2; ++r) {
       mbar_init(&tfull[r], 1);
-      mbar_init(&tempty[r], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[r], kTcEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -220,7 +206,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int n_chunk = a.K_pad / kTcChunk;
+  const int n_chunk = (a.K_pad + kTcChunk - 1) / kTcChunk;
   const int npass = a.do_x + a.do_u;
   const int pass0 = a.do_x ? 0 : 1;
 
@@ -267,8 +253,8 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t base = smem_u32(smem + stage * kTcStageBytes);
-#pragma unroll
-            for (int s = 0; s < kTcChunk / 16; ++s)
+            const int n_steps = min(kTcChunk / 16, (a.K_pad - c * kTcChunk) / 16);
+            for (int s = 0; s < n_steps; ++s)
 #pragma unroll
               for (int q = 0; q < 12; ++q) {
                 const uint64_t ad = umma_desc_sw64(base + prod_a[q] * kTcPlaneA + s * 32);
@@ -284,34 +270,41 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp - 4;                  // TMEM lane quadrant
-    const int r = q * 32 + lane;             // tile row
+    // warp e = warp - 4: TMEM lane quadrant q = warp % 4 (hardware rule), column half h
+    const int e = warp - 4, q = warp & 3, h = e >> 2;
+    const int r = q * 32 + lane;             // tile row owned in the TMEM phase
     const int i = iBase + r;
+    const int cb = h * 32;                   // first tile column owned in the TMEM phase
     const float inv_nb = 1.f / (float)a.nbb;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const int et = e * 32 + lane;            // 0..255 within the epilogue group
+    if (et < kTcTile) {
+      const int ii = iBase + et;
+      const bool ok = ii >= a.i_lo && ii < a.i_hi && ii < a.N;
+      // pair (ii, j) -> rowoff + j; row 0 legitimately has offset -1, so INT64_MIN marks skipped rows
+      rowoff_s[et] = ok ? (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base : INT64_MIN;
+    }
+    const bool cohy = a.cohy_bins || a.cohy_band;
     uint32_t tuse[2] = {0, 0};
-    const bool want_coh = a.coh_bins || a.coh_band, want_cohy = a.cohy_bins || a.cohy_band;
     for (int bl = 0; bl < a.nbb; ++bl) {
       const int64_t bo = (int64_t)bl * a.pair_stride;
-      const bool last = bl + 1 == a.nbb;
       float pi = 0.f;
       if (a.do_x) {
-        const int t = threadIdx.x - 128;
-        if (t < kTcTileJ) {
-          const int j = jBase + t;
+        if (et < kTcTileJ) {
+          const int j = jBase + et;
           float f = 0.f;
           if (j < a.N) {
             const float sj = a.nscale[(int64_t)bl * a.N + j];
             f = a.psd[(int64_t)bl * a.N + j] * sj * sj;
           }
-          colfac[t] = f;
+          colfac[et] = f;
         }
         if (i < a.N) {
           const float si = a.nscale[(int64_t)bl * a.N + i];
           pi = a.psd[(int64_t)bl * a.N + i] * si * si;
         }
-        epi_bar();
       }
+      epi_bar();
       for (int ps = 0; ps < npass; ++ps) {
         const int pass = pass0 + ps;
         const int reg = ps;
@@ -319,48 +312,58 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         ++tuse[reg];
         tc_fence_after();
         const uint32_t t_acc = tmem + lane_addr + reg * 128;
-        // pass 0 -> COH (band col 0..63), COHY (band 128.., 192..); pass 1 -> PLV (band 64..)
-        for (int c0 = 0; c0 < kTcTileJ; c0 += 16) {
+#pragma unroll
+        for (int c1 = 0; c1 < 32; c1 += 16) {
+          const int c0 = cb + c1;
           float vr[16], vi[16];
           tmem_ld16(t_acc + c0, vr);
           tmem_ld16(t_acc + 64 + c0, vi);
           if (pass == 0) {
-            float m[16], br[16], bi[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
               const float pp = pi * colfac[c0 + u];
               const float rs = pp > 0.f ? rsqrtf(pp) : 0.f;
               vr[u] *= rs;
               vi[u] *= rs;
-              m[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]);
-              xbuf[r * kTcXStride + c0 + u] = make_float2(vr[u], vi[u]);
             }
-            if (a.coh_band) {
-              float b[16];
-              if (bl) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
+            if (a.coh_band || !cohy) {
+              float m[16];
 #pragma unroll
-              for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + m[u] * inv_nb;
-              tmem_st16(tmem + lane_addr + kTmBand + c0, b);
+              for (int u = 0; u < 16; ++u) m[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]);
+              if (!cohy)
+#pragma unroll
+                for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u].x = m[u];
+              if (a.coh_band) {
+                float b[16];
+                if (bl) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + m[u] * inv_nb;
+                tmem_st16(tmem + lane_addr + kTmBand + c0, b);
+              }
             }
-            if (a.cohy_band) {
-              if (bl) {
-                tmem_ld16(tmem + lane_addr + kTmBand + 128 + c0, br);
-                tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
-              }
+            if (cohy) {
 #pragma unroll
-              for (int u = 0; u < 16; ++u) {
-                br[u] = (bl ? br[u] : 0.f) + vr[u] * inv_nb;
-                bi[u] = (bl ? bi[u] : 0.f) + vi[u] * inv_nb;
+              for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(vr[u], vi[u]);
+              if (a.cohy_band) {
+                float br[16], bi[16];
+                if (bl) {
+                  tmem_ld16(tmem + lane_addr + kTmBand + 128 + c0, br);
+                  tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                  br[u] = (bl ? br[u] : 0.f) + vr[u] * inv_nb;
+                  bi[u] = (bl ? bi[u] : 0.f) + vi[u] * inv_nb;
+                }
+                tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
+                tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
               }
-              tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
-              tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
             }
           } else {
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-              const float v = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
-              vr[u] = v;
-              xbuf[r * kTcXStride + c0 + u] = make_float2(v, 0.f);
+              vr[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
+              xbuf[r * kTcXStride + c0 + u].x = vr[u];
             }
             if (a.plv_band) {
               float b[16];
@@ -376,39 +379,27 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[reg]);
-        // per-bin outputs through the transpose buffer (coalesced row stores)
         epi_bar();
-        if (pass == 0) {
-          if (a.cohy_bins) store_tile<float2>(xbuf, a.cohy_bins, bo, a, iBase, jBase, q, lane);
-          if (a.coh_bins) {
-            for (int rr = 0; rr < 32; ++rr) {
-              const int row = q * 32 + rr, ii = iBase + row;
-              if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
-              const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base + bo;
-              for (int h = 0; h < 2; ++h) {
-                const int c = lane + 32 * h, j = jBase + c;
-                if (j > ii && j < a.N) {
-                  const float2 v = xbuf[row * kTcXStride + c];
-                  a.coh_bins[ro + j] = sqrtf(v.x * v.x + v.y * v.y);
-                }
-              }
-            }
-          }
-        } else if (a.plv_bins) {
-          for (int rr = 0; rr < 32; ++rr) {
-            const int row = q * 32 + rr, ii = iBase + row;
-            if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
-            const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base + bo;
-            for (int h = 0; h < 2; ++h) {
-              const int c = lane + 32 * h, j = jBase + c;
-              if (j > ii && j < a.N) a.plv_bins[ro + j] = xbuf[row * kTcXStride + c].x;
+        // per-bin outputs: warp e stores rows [16 e, 16 e + 16), 64 contiguous pairs each
+        for (int rr = 0; rr < 16; ++rr) {
+          const int row = e * 16 + rr;
+          const int64_t ro = rowoff_s[row];
+          if (ro == INT64_MIN) continue;
+          const int ii = iBase + row;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int c = lane + 32 * hh, j = jBase + c;
+            if (j <= ii || j >= a.N) continue;
+            const float2 v = xbuf[row * kTcXStride + c];
+            if (pass == 0) {
+              if (cohy && a.cohy_bins) a.cohy_bins[bo + ro + j] = v;
+              if (a.coh_bins) a.coh_bins[bo + ro + j] = cohy ? sqrtf(v.x * v.x + v.y * v.y) : v.x;
+            } else if (a.plv_bins) {
+              a.plv_bins[bo + ro + j] = v.x;
             }
           }
         }
         epi_bar();
-        (void)want_coh;
-        (void)want_cohy;
-        (void)last;
       }
     }
     // band means: TMEM -> transpose buffer -> coalesced stores
@@ -416,7 +407,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       for (int kind = 0; kind < 3; ++kind) {
         if ((kind == 0 && !a.coh_band) || (kind == 1 && !a.plv_band) || (kind == 2 && !a.cohy_band)) continue;
-        for (int c0 = 0; c0 < kTcTileJ; c0 += 16) {
+#pragma unroll
+        for (int c1 = 0; c1 < 32; c1 += 16) {
+          const int c0 = cb + c1;
           float b0[16], b1[16];
           tmem_ld16(tmem + lane_addr + kTmBand + (kind == 2 ? 128 : kind * 64) + c0, b0);
           if (kind == 2) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, b1);
@@ -424,18 +417,19 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
           for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(b0[u], kind == 2 ? b1[u] : 0.f);
         }
         epi_bar();
-        if (kind == 2) {
-          store_tile<float2>(xbuf, a.cohy_band, 0, a, iBase, jBase, q, lane);
-        } else {
-          float* dst = kind == 0 ? a.coh_band : a.plv_band;
-          for (int rr = 0; rr < 32; ++rr) {
-            const int row = q * 32 + rr, ii = iBase + row;
-            if (ii < a.i_lo || ii >= a.i_hi || ii >= a.N) continue;
-            const int64_t ro = (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base;
-            for (int h = 0; h < 2; ++h) {
-              const int c = lane + 32 * h, j = jBase + c;
-              if (j > ii && j < a.N) dst[ro + j] = xbuf[row * kTcXStride + c].x;
-            }
+        for (int rr = 0; rr < 16; ++rr) {
+          const int row = e * 16 + rr;
+          const int64_t ro = rowoff_s[row];
+          if (ro == INT64_MIN) continue;
+          const int ii = iBase + row;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int c = lane + 32 * hh, j = jBase + c;
+            if (j <= ii || j >= a.N) continue;
+            const float2 v = xbuf[row * kTcXStride + c];
+            if (kind == 2) a.cohy_band[ro + j] = v;
+            else if (kind == 0) a.coh_band[ro + j] = v.x;
+            else a.plv_band[ro + j] = v.x;
           }
         }
         epi_bar();
@@ -501,7 +495,8 @@ static EncodeTiledFn get_encode() {
 }
 
 size_t tc_smem_bytes() {
-  return (size_t)kTcStages * kTcStageBytes + (size_t)kTcTile * kTcXStride * sizeof(float2) + kTcTileJ * 4 + 1024 + 256;
+  return (size_t)kTcStages * kTcStageBytes + (size_t)kTcTile * kTcXStride * sizeof(float2) + kTcTileJ * 4 +
+         kTcTile * 8 + 1024 + 256;
 }
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
@@ -511,7 +506,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     cs_set_error("cuTensorMapEncodeTiled unavailable");
     return false;
   }
-  const int K_pad = (K + kTcChunk - 1) / kTcChunk * kTcChunk;
+  const int K_pad = (K * 1 + 15) / 16 * 16;  // UMMA K granularity; the last TMA box is zero-filled
   const size_t need = (size_t)nbb * 8 * p.N * K_pad * sizeof(__half);
   if (need > p.tc_bytes) {
     if (p.tc_ops) cudaFreeAsync(p.tc_ops, st);
@@ -526,7 +521,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   __half* G = (__half*)p.tc_ops;
   {
     PhaseMark ph(p, "tc_prep", st);
-    dim3 grid(K_pad / 32, (p.N + 7) / 8, nbb);
+    dim3 grid((K_pad + 31) / 32, (p.N + 7) / 8, nbb);
     k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, K, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
   }
   CUtensorMap mapA, mapB;
@@ -552,8 +547,30 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
   a.tile_row0 = a.i_lo / kTcTile;
   const int tile_row1 = (a.i_hi + kTcTile - 1) / kTcTile;
-  int64_t n_tiles = 0;
-  for (int t = a.tile_row0; t < tile_row1; ++t) n_tiles += a.nt - 2 * t > 0 ? a.nt - 2 * t : 0;
+  // grouped tile order: bands of 8 row tiles swept column by column, so the CTAs
+  // resident at once touch ~8 x 128 + 18 x 64 nodes of operands (L2 resident)
+  const uint64_t key = ((uint64_t)a.tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)a.nt;
+  if (key != p.tc_tiles_key || !p.tc_tiles) {
+    std::vector<int2> tl;
+    constexpr int GR = 8;
+    for (int b0 = a.tile_row0; b0 < tile_row1; b0 += GR)
+      for (int J = 0; J < a.nt; ++J)
+        for (int I = b0; I < b0 + GR && I < tile_row1; ++I)
+          if (J >= 2 * I) tl.push_back(make_int2(I, J));
+    if (p.tc_tiles) cudaFree(p.tc_tiles);
+    p.tc_tiles = nullptr;
+    p.tc_ntiles = (int64_t)tl.size();
+    if (!tl.empty()) {
+      if (cudaMalloc(&p.tc_tiles, tl.size() * sizeof(int2)) != cudaSuccess) {
+        cs_set_error("device allocation failed (tile list)");
+        return false;
+      }
+      cudaMemcpy(p.tc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    }
+    p.tc_tiles_key = key;
+  }
+  const int64_t n_tiles = p.tc_ntiles;
+  a.tiles = (const int2*)p.tc_tiles;
   a.psd = p.psd; a.nscale = nscale;
   a.invK = 1.f / (float)K;
   a.pair_base = out->pair_base; a.pair_stride = out->pair_stride;
