@@ -246,6 +246,7 @@ int cs_plan_destroy(cs_plan* p) {
   cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
   if (p->tc_ops) cudaFree(p->tc_ops);
   if (p->tc_tiles) cudaFree(p->tc_tiles);
+  if (p->lag_ops) cudaFree(p->lag_ops);
   cudaFree(p->flags); cudaFree(p->counters);
   if (p->prof) {
     auto* ps = (ProfState*)p->prof;

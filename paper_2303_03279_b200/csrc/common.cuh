@@ -29,6 +29,8 @@ struct Plan {
   float* nscale = nullptr;       // [nb][N] 2^-ceil(log2 mag): per-node-bin fp16 operand scale
   void* tc_ops = nullptr;        // tensor-core operand planes (grown on demand)
   size_t tc_bytes = 0;
+  void* lag_ops = nullptr;       // packed trial-pair operands of the phase-lag kernel
+  size_t lag_bytes = 0;
   void* tc_tiles = nullptr;      // tensor-core tile order (int2 list) for the cached row range
   int64_t tc_ntiles = 0;
   uint64_t tc_tiles_key = 0;

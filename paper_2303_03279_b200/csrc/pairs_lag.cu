@@ -23,14 +23,17 @@
 
 namespace cs {
 
-constexpr int kKC = 8;  // k-pairs per staged chunk (16 trials)
+constexpr int kKC = 16;    // k-pairs per pipeline stage (32 trials)
+constexpr int kLagStages = 3;
 
 struct LagArgs {
   const float2* X32;
   const double2* X64;
-  int N, nb, L;
+  const float4* PkI;  // [nbb][Kp][N64] (re_a, re_b, im_a, im_b)
+  const float4* PkJ;  // [nbb][Kp][N64] (re_a, re_b, -im_a, -im_b)
+  int N, N64, nb, L;
   const int* slots;
-  int K;
+  int K, Kp;
   int bin_lo, nbb;
   const float* psd;  // [nbb][N]
   const float* mag;  // [nbb][N]
@@ -46,6 +49,42 @@ struct LagArgs {
   int flag_cap;
 };
 
+// Trial-pair packing of the selected trials (k = 2 kp, 2 kp + 1) into the layouts the
+// pair kernel stages with cp.async.  Odd K: the last pair's second trial is a
+// phantom with I side (0, M_i 2^-10) and J side (M_j 2^-10, 0), i.e. t = M_i M_j 2^-20
+// > g M_i M_j: it never trips the exact-sign guard, adds no negative sign, and its
+// contribution to sum t and sum |t| is removed exactly in the epilogue.
+constexpr float kPhantom = 9.765625e-4f;  // 2^-10
+__global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int Kp,
+                           int N, int N64, int nb, int L, int bin_lo, const float* __restrict__ mag,
+                           float4* __restrict__ PkI, float4* __restrict__ PkJ) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kp = blockIdx.y, bl = blockIdx.z;
+  if (n >= N64) return;
+  float2 va = make_float2(0.f, 0.f), vb = make_float2(0.f, 0.f);
+  float2 wb = make_float2(0.f, 0.f);  // J-side value of trial b (phantom differs)
+  if (n < N) {
+    const int b = bin_lo + bl;
+    va = X32[(((int64_t)slots[2 * kp] * L) * nb + b) * N + n];
+    if (2 * kp + 1 < K) {
+      vb = X32[(((int64_t)slots[2 * kp + 1] * L) * nb + b) * N + n];
+      wb = make_float2(vb.x, -vb.y);
+    } else {
+      const float m = mag[(int64_t)bl * N + n] * kPhantom;
+      vb = make_float2(0.f, m);
+      wb = make_float2(m, -0.f);
+    }
+  }
+  const int64_t o = ((int64_t)bl * Kp + kp) * N64 + n;
+  PkI[o] = make_float4(va.x, vb.x, va.y, vb.y);
+  PkJ[o] = make_float4(va.x, wb.x, -va.y, wb.y);
+}
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
 // CTA tile 64 x 64 nodes; thread micro-tile kTR rows x kTC cols (rows i = ty + 16 r,
 // cols j = tx + 32 c) so a warp shares one i row (broadcast loads) and writes 32
 // consecutive pairs of that row (coalesced 128 B stores).
@@ -53,12 +92,13 @@ constexpr int kTR = 4, kTC = 2;
 constexpr int kTY = kTile / kTR, kTX = kTile / kTC;  // 16 x 32 = 512 threads
 constexpr int kLagThreads = kTY * kTX;
 constexpr int kNP = kTR * kTC;
+constexpr int kStageF4 = kKC * kTile;                 // float4 per side per stage
 
 __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
   extern __shared__ float4 smem4[];
-  float4* XI = smem4;                          // [2][kKC][64]
-  float4* XJ = smem4 + 2 * kKC * kTile;        // [2][kKC][64]
-  float* band_s = (float*)(smem4 + 4 * kKC * kTile);  // [5][64][64]
+  float4* XI = smem4;                                  // [stages][kKC][64]
+  float4* XJ = smem4 + kLagStages * kStageF4;          // [stages][kKC][64]
+  float* band_s = (float*)(smem4 + 2 * kLagStages * kStageF4);  // [5][64][64]
 
   int I, J;
   decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
@@ -74,29 +114,37 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
   if (band_mask)
     for (int e = tid; e < 5 * kTile * kTile; e += kLagThreads) band_s[e] = 0.f;
 
-  const int K2 = a.K >> 1;
+  const int n_stage = (a.Kp + kKC - 1) / kKC;   // stages per bin
+  const int total = n_stage * a.nbb;            // flat (bin, stage) sequence
   const bool odd = a.K & 1;
-  const int n_stage = (K2 + kKC - 1) / kKC;
   const float invK = 1.f / (float)a.K;
   const float uspA = a.K > 1 ? (float)a.K / (float)(a.K - 1) : 0.f;
   const float uspB = a.K > 1 ? 1.f / (float)(a.K - 1) : 0.f;
-  const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
 
-  // output offsets: pair (i, j) -> rowoff[r] + j
-  int64_t rowoff[kTR];
+  // cp.async staging of flat step t into buffer t % stages (2 float4 per side per thread)
+  auto issue = [&](int t) {
+    if (t < total) {
+      const int bl = t / n_stage, st = t % n_stage;
+      const int kp0 = st * kKC;
+      float4* dI = XI + (t % kLagStages) * kStageF4;
+      float4* dJ = XJ + (t % kLagStages) * kStageF4;
 #pragma unroll
-  for (int r = 0; r < kTR; ++r) {
-    const int64_t i = iBase + ty + kTY * r;
-    rowoff[r] = i * (a.N - 1) - i * (i - 1) / 2 - i - 1 - a.pair_base;
-  }
+      for (int q = 0; q < kStageF4 / kLagThreads; ++q) {
+        const int e = tid + kLagThreads * q;
+        const int kp = e >> 6, node = e & 63;
+        const int kpg = min(kp0 + kp, a.Kp - 1);  // clamp: rows past Kp are never read
+        const int64_t ob = ((int64_t)bl * a.Kp + kpg) * a.N64;
+        cpa16(dI + e, a.PkI + ob + iBase + node);
+        cpa16(dJ + e, a.PkJ + ob + jBase + node);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
 
-  for (int bl = 0; bl < a.nbb; ++bl) {
-    const int b = a.bin_lo + bl;
-    const float2* Xb = a.X32 + (int64_t)b * a.N;  // + slot*slot_stride + n
-
-    f2 sim[kNP];
-    float sabs[kNP], mn[kNP];
-    int neg[kNP];
+  f2 sim[kNP];
+  float sabs[kNP], mn[kNP];
+  int neg[kNP];
+  auto reset_acc = [&]() {
 #pragma unroll
     for (int p = 0; p < kNP; ++p) {
       sim[p] = 0ull;
@@ -104,102 +152,54 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
       mn[p] = 3.0e38f;
       neg[p] = 0;
     }
-
-    // ---- staged gather of (trial-pair, node) float4 into shared memory ----
-    // thread -> (kp, node) = (tid / 64, tid % 64): one float4 per side per stage
-    float2 ra[2], rb[2];  // [side] for slots a, b
-    const int skp = tid >> 6, snode = tid & 63;
-    auto load_stage = [&](int kp0, int nkp, bool tail) {
-      int sa = -1, sb = -1;
-      if (skp < nkp) {
-        if (tail) {
-          sa = a.slots[a.K - 1];
-        } else {
-          sa = a.slots[2 * (kp0 + skp)];
-          sb = a.slots[2 * (kp0 + skp) + 1];
-        }
+  };
+  auto compute_kp = [&](const float4* sI, const float4* sJ, int kp) {
+    float4 xi[kTR], xj[kTC];
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) xi[r] = sI[kp * kTile + ty + kTY * r];
+#pragma unroll
+    for (int c = 0; c < kTC; ++c) xj[c] = sJ[kp * kTile + tx + kTX * c];
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+#pragma unroll
+      for (int c = 0; c < kTC; ++c) {
+        const int p = r * kTC + c;
+        const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+        const f2 t = ffma2(ii, jr, fmul2(ir, jn));   // Im(X_i conj X_j) for trials a, b
+        sim[p] = fadd2(sim[p], t);
+        const float tl = lo_of(t), th = hi_of(t);
+        sabs[p] += fabsf(tl);
+        sabs[p] += fabsf(th);
+        neg[p] += (int)(__float_as_uint(tl) >> 31);
+        neg[p] += (int)(__float_as_uint(th) >> 31);
+        mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
       }
-      const int ni = iBase + snode, nj = jBase + snode;
-      const float2 z = make_float2(0.f, 0.f);
-      ra[0] = (sa >= 0 && ni < a.N) ? Xb[sa * slot_stride + ni] : z;
-      rb[0] = (sb >= 0 && ni < a.N) ? Xb[sb * slot_stride + ni] : z;
-      ra[1] = (sa >= 0 && nj < a.N) ? Xb[sa * slot_stride + nj] : z;
-      rb[1] = (sb >= 0 && nj < a.N) ? Xb[sb * slot_stride + nj] : z;
-    };
-    auto store_stage = [&](int buf) {
-      XI[(buf * kKC + skp) * kTile + snode] = make_float4(ra[0].x, rb[0].x, ra[0].y, rb[0].y);
-      XJ[(buf * kKC + skp) * kTile + snode] = make_float4(ra[1].x, rb[1].x, -ra[1].y, -rb[1].y);
-    };
-
-    auto compute_kp = [&](int buf, int kp) {
-      float4 xi[kTR], xj[kTC];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r) xi[r] = XI[(buf * kKC + kp) * kTile + ty + kTY * r];
-#pragma unroll
-      for (int c = 0; c < kTC; ++c) xj[c] = XJ[(buf * kKC + kp) * kTile + tx + kTX * c];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r) {
-        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
-#pragma unroll
-        for (int c = 0; c < kTC; ++c) {
-          const int p = r * kTC + c;
-          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-          const f2 t = ffma2(ii, jr, fmul2(ir, jn));
-          sim[p] = fadd2(sim[p], t);
-          const float tl = lo_of(t), th = hi_of(t);
-          sabs[p] += fabsf(tl);
-          sabs[p] += fabsf(th);
-          neg[p] += (int)(__float_as_uint(tl) >> 31);
-          neg[p] += (int)(__float_as_uint(th) >> 31);
-          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
-        }
-      }
-    };
-
-    if (n_stage > 0) {
-      load_stage(0, min(kKC, K2), false);
-      store_stage(0);
     }
-    __syncthreads();
-    for (int s = 0; s < n_stage; ++s) {
-      const int buf = s & 1;
-      const int nkp = min(kKC, K2 - s * kKC);
-      const bool more = s + 1 < n_stage;
-      if (more) load_stage((s + 1) * kKC, min(kKC, K2 - (s + 1) * kKC), false);
-      if (nkp == kKC) {
-#pragma unroll 2
-        for (int kp = 0; kp < kKC; ++kp) compute_kp(buf, kp);
-      } else {
-        for (int kp = 0; kp < nkp; ++kp) compute_kp(buf, kp);
-      }
-      if (more) store_stage(buf ^ 1);
-      __syncthreads();
-    }
-    if (odd) {
-      // last trial alone: stage it with an empty partner and use the low lanes only
-      load_stage(0, 1, true);
-      store_stage(0);
-      __syncthreads();
-      float4 xi[kTR], xj[kTC];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r) xi[r] = XI[ty + kTY * r];
-#pragma unroll
-      for (int c = 0; c < kTC; ++c) xj[c] = XJ[tx + kTX * c];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r)
-#pragma unroll
-        for (int c = 0; c < kTC; ++c) {
-          const int p = r * kTC + c;
-          const float t = fmaf(xi[r].z, xj[c].x, xi[r].x * xj[c].z);
-          sim[p] = fadd2(sim[p], pk(t, 0.f));
-          sabs[p] += fabsf(t);
-          neg[p] += (int)(__float_as_uint(t) >> 31);
-          mn[p] = fminf(mn[p], fabsf(t));
-        }
-      __syncthreads();
-    }
+  };
 
-    // ---- epilogue: finalize the bin (fast-math intrinsics; fp32 outputs) ----
+#pragma unroll
+  for (int t = 0; t < kLagStages - 1; ++t) issue(t);
+  reset_acc();
+
+  for (int t = 0; t < total; ++t) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kLagStages - 2));
+    __syncthreads();                       // stage t visible; stage t-1 fully consumed
+    issue(t + kLagStages - 1);
+    const int bl = t / n_stage, st = t % n_stage;
+    const float4* sI = XI + (t % kLagStages) * kStageF4;
+    const float4* sJ = XJ + (t % kLagStages) * kStageF4;
+    const int nkp = min(kKC, a.Kp - st * kKC);
+    if (nkp == kKC) {
+#pragma unroll 4
+      for (int kp = 0; kp < kKC; ++kp) compute_kp(sI, sJ, kp);
+    } else {
+      for (int kp = 0; kp < nkp; ++kp) compute_kp(sI, sJ, kp);
+    }
+    if (st + 1 < n_stage) continue;
+
+    // ---- epilogue: finalize bin bl (fast-math intrinsics; fp32 outputs) ----
+    const int b = a.bin_lo + bl;
     const bool real_bin = (b == a.real0) || (b == a.real1);
     float Mi[kTR], Mj[kTC], Pi[kTR], Pj[kTC];
 #pragma unroll
@@ -236,8 +236,9 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
           else
             a.counters[1] = 1;
         }
-        const float s_im = dead ? 0.f : lo_of(sim[p]) + hi_of(sim[p]);
-        const float s_abs = dead ? 0.f : sabs[p];
+        const float tph = odd ? (Mi[r] * kPhantom) * (Mj[c] * kPhantom) : 0.f;
+        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+        const float s_abs = dead ? 0.f : sabs[p] - tph;
         const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
         const float pp = Pi[r] * Pj[c];
         float v[5];
@@ -246,10 +247,10 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
         v[1] = pli;
         v[2] = pli * pli * uspA - uspB;                              // USPLI
         const float w = s_abs > 0.f ? __fdividef(fabsf(s_im), s_abs) : 0.f;  // WPLI, 0/0 -> 0
-        v[3] = w;
-        v[4] = w * w;                                                // DSWPLI
+        v[3] = fminf(w, 1.f);
+        v[4] = v[3] * v[3];                                          // DSWPLI
         if (valid && !flagged) {
-          const int64_t po = rowoff[r] + j;
+          const int64_t po = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + j;
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
@@ -258,7 +259,9 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
           }
         }
       }
+    reset_acc();
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 
   if (band_mask) {
     __syncthreads();
@@ -332,7 +335,9 @@ __global__ void k_lag_fallback(const LagArgs a) {
   }
 }
 
-size_t lag_smem_bytes() { return (size_t)4 * kKC * kTile * sizeof(float4) + 5 * kTile * kTile * sizeof(float); }
+size_t lag_smem_bytes() {
+  return (size_t)2 * kLagStages * kStageF4 * sizeof(float4) + 5 * kTile * kTile * sizeof(float);
+}
 
 void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   static bool configured = false;
@@ -342,6 +347,12 @@ void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
     configured = true;
   }
   cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
+  {
+    PhaseMark ph(p, "lag_prep", st);
+    dim3 grid((a.N64 + 127) / 128, a.Kp, a.nbb);
+    k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag,
+                                     (float4*)a.PkI, (float4*)a.PkJ);
+  }
   {
     PhaseMark ph(p, "pairs_lag", st);
     k_pairs_lag<<<(unsigned)n_tiles, kLagThreads, smem, st>>>(a);
@@ -369,7 +380,24 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.X32 = p.X32;
   a.X64 = p.X64;
   a.N = p.N; a.nb = p.nb; a.L = p.L;
+  a.N64 = (p.N + kTile - 1) / kTile * kTile;
   a.slots = slots; a.K = K;
+  a.Kp = (K + 1) / 2;
+  {
+    const size_t need = (size_t)2 * nbb * a.Kp * a.N64 * sizeof(float4);
+    if (need > p.lag_bytes) {
+      if (p.lag_ops) cudaFreeAsync(p.lag_ops, st);
+      if (cudaMallocAsync(&p.lag_ops, need, st) != cudaSuccess) {
+        p.lag_ops = nullptr;
+        p.lag_bytes = 0;
+        cs_set_error("device allocation failed (phase-lag operands %zu bytes)", need);
+        return -1;
+      }
+      p.lag_bytes = need;
+    }
+    a.PkI = (const float4*)p.lag_ops;
+    a.PkJ = a.PkI + (size_t)nbb * a.Kp * a.N64;
+  }
   a.bin_lo = bin_lo; a.nbb = nbb;
   a.psd = p.psd; a.mag = p.mag;
   a.real0 = p.dc_local; a.real1 = p.nyq_local;
