@@ -127,6 +127,12 @@ int cs_pair_sums(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo, i
 int cs_get_spectra(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo, int n_bins,
                    void* dst_dev, void* stream);
 
+/* Upload externally computed spectra (complex128 [n][n_nodes][n_bins], the
+ * trial_spectra layout) into slots slot0.. of a single-taper plan: the drop-in
+ * for accumulate_spectra(acc, spectra) (spectral.py:244-261). */
+int cs_put_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, int n_bins, int slot0,
+                   void* stream);
+
 /* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
  * range of shard `shard` of `n_shards` (balanced by tile count) and the
  * contiguous global pair range [pair_begin, pair_end) it covers. */

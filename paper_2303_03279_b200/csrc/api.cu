@@ -14,6 +14,7 @@ void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns
 void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb, cudaStream_t st);
 void run_get_spectra(const Plan& p, const int* slots, int ns, int bin_lo, int nbins, void* dst,
                      cudaStream_t st);
+void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, cudaStream_t st);
 struct LagArgs;
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st);
@@ -308,6 +309,23 @@ int cs_get_spectra(cs_plan* p, const int* slots, int ns, int bin_lo, int nbins, 
   DeviceGuard g(p->device);
   cs::run_get_spectra(*p, slots, ns, bin_lo, nbins, dst, (cudaStream_t)stream);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_get_spectra");
+  return CS_OK;
+}
+
+int cs_put_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbins, int slot0, void* stream) {
+  if (!p || !src) { cs_set_error("cs_put_spectra: null argument"); return CS_EPARAM; }
+  if (p->L != 1) { cs_set_error("cs_put_spectra: single-taper plans only"); return CS_EPARAM; }
+  if (bin_lo < 0 || nbins < 1 || bin_lo + nbins > p->nb || slot0 < 0) {
+    cs_set_error("cs_put_spectra: bad bins/slot");
+    return CS_EPARAM;
+  }
+  if (n <= 0) return CS_OK;
+  DeviceGuard g(p->device);
+  {
+    cs::PhaseMark ph(*p, "put_spectra", (cudaStream_t)stream);
+    cs::run_put_spectra(*p, src, n, bin_lo, nbins, slot0 % p->slot_cap, (cudaStream_t)stream);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_put_spectra");
   return CS_OK;
 }
 

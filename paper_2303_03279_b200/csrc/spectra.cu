@@ -339,3 +339,26 @@ extern "C" int cs_probe_peaks(int device, double* fp32_lane_ops, double* fp64_fm
   cudaSetDevice(prev);
   return cudaGetLastError() == cudaSuccess ? CS_OK : CS_ECUDA;
 }
+
+// Externally computed spectra (complex128 [n][N][nbins], trial_spectra layout) into
+// ring slots slot0.. (taper 0, plan-local bins [bin_lo, bin_lo + nbins)).
+namespace cs {
+__global__ void k_put_spectra(const double2* __restrict__ src, int n, int N, int nb, int L, int bin_lo,
+                              int nbins, int slot0, int slot_cap, float scale, double2* __restrict__ X64,
+                              float2* __restrict__ X32) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (idx >= (int64_t)N * nbins) return;
+  const int node = (int)(idx / nbins), bl = (int)(idx % nbins);
+  const double2 v = src[((int64_t)k * N + node) * nbins + bl];
+  const int slot = (slot0 + k) % slot_cap;
+  const int64_t o = (((int64_t)slot * L) * nb + bin_lo + bl) * N + node;
+  X64[o] = v;
+  X32[o] = make_float2((float)(v.x * (double)scale), (float)(v.y * (double)scale));
+}
+void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, cudaStream_t st) {
+  dim3 grid((unsigned)(((int64_t)p.N * nbins + 255) / 256), n);
+  k_put_spectra<<<grid, 256, 0, st>>>((const double2*)src, n, p.N, p.nb, p.L, bin_lo, nbins, slot0, p.slot_cap,
+                                       p.scale, p.X64, p.X32);
+}
+}  // namespace cs

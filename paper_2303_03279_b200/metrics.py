@@ -1,0 +1,367 @@
+"""Drop-in for connstream.metrics (reference src/metrics.py) on the B200 path.
+
+Per-bin finalisers, band-averaged networks, the batch entry point and the
+storage-mode engine, with the reference's names, signatures and errors.  Every
+spectral metric is computed by the fused device kernels (cs_pair_metrics):
+  COH / COHY / PLV      -> tcgen05 tensor-core kernel (K2)
+  IMAGCOHY / PLI family -> FP32 pair x trial kernel with fp64 exact-sign guard (K3)
+
+Reference anchors: metrics.py:32-98 (*_bins, _SPECTRAL_BINS), :101-134
+(_build_network, finalize_spectral), :267-460 (TrialCache, ConnectivityEngine),
+:465-498 (one-shot wrappers), :501-528 (convergence_curve), :531-551
+(compute_metric).  COR / XCOR (time-domain, :137-260) are not built yet.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import spectral
+from .core import (ConnectivityNetwork, DegenerateTrialCountError, EpochMatrix, FrequencyBand, MetricId,
+                   ParameterError, default_positions)
+from .plan import DevicePlan, pow2_scale
+from .spectral import SpectrumSet, pair_index
+
+
+def _full_band(acc, band):
+    return band if band is not None else FrequencyBand(0, acc.n_bins - 1, 0.0)
+
+
+def _check_k(K: int, metric: str):
+    if K < 1:
+        raise DegenerateTrialCountError("no trials accumulated")
+    if metric == "USPLI" and K < 2:
+        raise DegenerateTrialCountError("USPLI needs at least 2 trials")
+
+
+def _device_bins(acc: SpectrumSet, metric: str, band, want_band=False):
+    """Run the pair kernels for ``metric`` over acc's folded trials -> device
+    tensors (bins [nb, P], band [P])."""
+    band = _full_band(acc, band)
+    _check_k(acc.n_trials_accumulated, metric)
+    if band.hi_bin >= acc.n_bins:
+        raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {acc.n_bins} bins")
+    slots = acc.slots_for(band.lo_bin, band.hi_bin)
+    if slots is None or len(slots) != acc.n_trials_accumulated:
+        raise ParameterError("accumulator columns were folded from different trial sets; "
+                             "read the running sums (acc.csd_sum, ...) instead")
+    plan = acc.plan
+    st = torch.tensor(slots, dtype=torch.int32, device=plan.device)
+    out = plan.pair_metrics(st, (metric,), band.lo_bin, band.n_bins, per_bin=True, band=want_band)
+    return out[metric]
+
+
+def _host_bins(acc, metric, band):
+    o = _device_bins(acc, metric, band)["bins"]
+    arr = o.t().contiguous().cpu().numpy()
+    return arr.astype(np.complex128 if metric == "COHY" else np.float64)
+
+
+def cohy_bins(acc: SpectrumSet, band: FrequencyBand | None = None) -> np.ndarray:
+    """Complex coherency per pair and bin [P, nb] (metrics.py:32-42)."""
+    return _host_bins(acc, "COHY", band)
+
+
+def coh_bins(acc, band=None):
+    return _host_bins(acc, "COH", band)
+
+
+def imagcohy_bins(acc, band=None):
+    return _host_bins(acc, "IMAGCOHY", band)
+
+
+def plv_bins(acc, band=None):
+    return _host_bins(acc, "PLV", band)
+
+
+def pli_bins(acc, band=None):
+    return _host_bins(acc, "PLI", band)
+
+
+def uspli_bins(acc, band=None):
+    return _host_bins(acc, "USPLI", band)
+
+
+def wpli_bins(acc, band=None):
+    return _host_bins(acc, "WPLI", band)
+
+
+def dswpli_bins(acc, band=None):
+    return _host_bins(acc, "DSWPLI", band)
+
+
+_SPECTRAL_BINS = {
+    MetricId.COHY: cohy_bins,
+    MetricId.COH: coh_bins,
+    MetricId.IMAGCOHY: imagcohy_bins,
+    MetricId.PLV: plv_bins,
+    MetricId.PLI: pli_bins,
+    MetricId.USPLI: uspli_bins,
+    MetricId.WPLI: wpli_bins,
+    MetricId.DSWPLI: dswpli_bins,
+}
+
+
+def _build_network(metric, band, n_trials, n_channels, weights, complex_weights=None, lags=None, positions=None,
+                   node_ids=None, warnings=()):
+    if positions is None:
+        positions = default_positions(n_channels)
+    if node_ids is None:
+        node_ids = tuple(range(n_channels))
+    return ConnectivityNetwork(metric=metric, band=band, n_trials=n_trials, node_ids=node_ids,
+                               positions=positions, weights=weights, complex_weights=complex_weights,
+                               lags=lags, warnings=tuple(warnings))
+
+
+def _network_from_band(metric: MetricId, band, n_trials, n_channels, band_out, positions, node_ids):
+    if metric is MetricId.COHY:
+        cm = band_out.to(torch.complex128)
+        return _build_network(metric, band, n_trials, n_channels, cm.abs(), cm, positions=positions,
+                              node_ids=node_ids)
+    return _build_network(metric, band, n_trials, n_channels, band_out.double(), positions=positions,
+                          node_ids=node_ids)
+
+
+def finalize_spectral(acc: SpectrumSet, metric: MetricId, band: FrequencyBand, positions=None,
+                      node_ids=None) -> ConnectivityNetwork:
+    """Band-averaged network for one spectral metric (metrics.py:115-134)."""
+    if metric not in _SPECTRAL_BINS:
+        raise ParameterError(f"{metric} is not a spectral metric")
+    band = _full_band(acc, band)
+    _check_k(acc.n_trials_accumulated, metric.value)
+    slots = acc.slots_for(band.lo_bin, band.hi_bin)
+    if slots is None or len(slots) != acc.n_trials_accumulated:
+        raise ParameterError("accumulator columns were folded from different trial sets")
+    plan = acc.plan
+    st = torch.tensor(slots, dtype=torch.int32, device=plan.device)
+    out = plan.pair_metrics(st, (metric.value,), band.lo_bin, band.n_bins, per_bin=False, band=True)
+    return _network_from_band(metric, band, acc.n_trials_accumulated, acc.n_channels, out[metric.value]["band"],
+                              positions, node_ids)
+
+
+# one-shot wrappers (metrics.py:465-498)
+def cohy(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.COHY, _full_band(acc, band), **kw)
+
+
+def coh(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.COH, _full_band(acc, band), **kw)
+
+
+def imagcohy(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.IMAGCOHY, _full_band(acc, band), **kw)
+
+
+def plv(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.PLV, _full_band(acc, band), **kw)
+
+
+def pli(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.PLI, _full_band(acc, band), **kw)
+
+
+def uspli(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.USPLI, _full_band(acc, band), **kw)
+
+
+def wpli(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.WPLI, _full_band(acc, band), **kw)
+
+
+def dswpli(acc, band=None, **kw):
+    return finalize_spectral(acc, MetricId.DSWPLI, _full_band(acc, band), **kw)
+
+
+def _stack_epochs(epochs):
+    ts = [e.data if isinstance(e.data, torch.Tensor) else torch.as_tensor(e.data) for e in epochs]
+    T = ts[0].shape[1]
+    if any(t.shape != ts[0].shape for t in ts):
+        raise ParameterError("epochs must have equal shapes")
+    dt = torch.float32 if all(t.dtype == torch.float32 for t in ts) else torch.float64
+    return torch.stack([t.to(dt) for t in ts]).to(spectral._device()), T
+
+
+def compute_metric(epochs, metric: MetricId, nfft: int, band: FrequencyBand | None = None,
+                   max_lag: int | None = None, positions=None, node_ids=None, taper=None) -> ConnectivityNetwork:
+    """One-shot batch computation over a list of epochs (metrics.py:531-551):
+    K1 over every node x trial, then the fused pair kernels over all trials."""
+    metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
+    if not metric.is_spectral:
+        raise ParameterError(f"{metric.value} (time-domain) is not built on the device path yet")
+    if not epochs:
+        raise ParameterError("need at least one epoch")
+    if nfft < 2:
+        raise ParameterError(f"nfft must be >= 2, got {nfft}")
+    x, T = _stack_epochs(epochs)
+    K, C = x.shape[0], x.shape[1]
+    if band is None:
+        band = FrequencyBand(0, nfft // 2, epochs[0].sfreq / nfft)
+    if band.hi_bin > nfft // 2:
+        raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {nfft // 2 + 1} bins")
+    _check_k(K, metric.value)
+    plan = DevicePlan(C, T, nfft, band.lo_bin, band.hi_bin, taper=taper, slot_capacity=K, device=x.device,
+                      scale=pow2_scale(float(x.abs().amax()), min(T, nfft)))
+    plan.spectra(x, 0)
+    spectral._count_ffts(K * C * plan.n_tapers)
+    slots = torch.arange(K, dtype=torch.int32, device=x.device)
+    out = plan.pair_metrics(slots, (metric.value,), 0, plan.n_bins, per_bin=False, band=True)
+    return _network_from_band(metric, band, K, C, out[metric.value]["band"], positions, node_ids)
+
+
+@dataclass
+class TrialCache:
+    """Storage mode (metrics.py:267-282): trial_index -> ring slot of its spectra."""
+
+    enabled: bool = True
+    spectra: dict = field(default_factory=dict)
+    epochs: dict = field(default_factory=dict)
+    bytes_per_trial: int = 0
+
+    def memory_bytes(self) -> int:
+        return len(self.spectra) * self.bytes_per_trial
+
+
+class ConnectivityEngine:
+    """Storage-mode engine over an HBM spectrum ring (metrics.py:285-460).
+
+    Every added trial's full-bin spectra are computed once (K1) into a ring
+    slot.  finalize() runs the fused pair kernels over the slots of the trials
+    currently folded, so switching metric or band issues no new FFTs, and
+    rebuild_last(n) is a change of slot list (no re-fold).
+    """
+
+    def __init__(self, n_channels: int, nfft: int, sfreq: float, storage_mode: bool = True,
+                 max_lag: int | None = None, spectral_mode: str = "fixed", positions=None, node_ids=None,
+                 accumulate_band: tuple | None = None, taper=None, slot_capacity: int = 64):
+        if spectral_mode not in ("fixed", "welch"):
+            raise ParameterError(f"unknown spectral mode {spectral_mode!r}")
+        if spectral_mode == "welch":
+            raise ParameterError("welch spectral mode is not built on the device path yet")
+        self.n_channels = n_channels
+        self.nfft = nfft
+        self.sfreq = sfreq
+        self.bin_hz = sfreq / nfft
+        self.spectral_mode = spectral_mode
+        self.max_lag = max_lag
+        self.positions = positions
+        self.node_ids = node_ids
+        self.taper = taper
+        self.n_bins = nfft // 2 + 1
+        if accumulate_band is not None and storage_mode and spectral_mode == "fixed":
+            lo, hi = accumulate_band
+            if not (0 <= lo <= hi < self.n_bins):
+                raise ParameterError(f"accumulate_band [{lo}, {hi}] outside {self.n_bins} bins")
+        self._accumulate_band = accumulate_band
+        self.cache = TrialCache(enabled=storage_mode)
+        self._slot_capacity = max(int(slot_capacity), 1)
+        self._plan: DevicePlan | None = None
+        self._T = None
+        self._next_slot = 0
+        self._slot_of: dict = {}
+        self._sum_trials: list = []
+        self.n_trials = 0
+
+    # -- ring ------------------------------------------------------------------
+    def _ensure_plan(self, T: int, scale: float):
+        if self._plan is not None and T != self._T:
+            raise ParameterError("epochs of one engine must share n_samples")
+        need = self._next_slot + 1
+        if self._plan is None or need > self._plan.slot_capacity:
+            cap = self._slot_capacity if self._plan is None else 2 * self._plan.slot_capacity
+            new = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper,
+                             slot_capacity=cap, device=spectral._device(),
+                             scale=self._plan.scale if self._plan is not None else scale)
+            if self._plan is not None:
+                o64, o32 = self._plan.ring()
+                n64, n32 = new.ring()
+                n64[: o64.shape[0]].copy_(o64)
+                n32[: o32.shape[0]].copy_(o32)
+            self._plan = new
+            self._T = T
+            self.cache.bytes_per_trial = self.n_channels * self.n_bins * 24 * new.n_tapers
+
+    # -- accumulation -------------------------------------------------------------
+    def add_trial(self, epoch: EpochMatrix) -> None:
+        if epoch.n_channels != self.n_channels:
+            raise ParameterError(f"epoch has {epoch.n_channels} channels, engine expects {self.n_channels}")
+        idx = epoch.trial_index
+        if not (self.cache.enabled and idx in self._slot_of):
+            x = spectral._as_device_samples(epoch.data)
+            scale = pow2_scale(float(x.abs().amax()), min(x.shape[1], self.nfft))
+            self._ensure_plan(x.shape[1], scale)
+            slot = self._next_slot
+            self._next_slot += 1
+            self._plan.spectra(x[None].contiguous(), slot)
+            spectral._count_ffts(self.n_channels * self._plan.n_tapers)
+            self._slot_of[idx] = slot
+            if self.cache.enabled:
+                self.cache.spectra[idx] = slot
+        if self.cache.enabled:
+            self.cache.epochs[idx] = epoch
+        self._sum_trials.append(idx)
+        self.n_trials += 1
+
+    def ensure_band(self, band: FrequencyBand) -> None:
+        """All bins are cached on the device, so back-fill is a no-op (metrics.py:363-380)."""
+        if band.hi_bin >= self.n_bins:
+            raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {self.n_bins} bins")
+
+    # -- finalization ---------------------------------------------------------------
+    def _slots(self):
+        return torch.tensor([self._slot_of[i] for i in self._sum_trials], dtype=torch.int32,
+                            device=self._plan.device)
+
+    def finalize(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
+        metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
+        if not metric.is_spectral:
+            if self.n_trials < 1:
+                raise DegenerateTrialCountError("no trials accumulated")
+            raise ParameterError(f"{metric.value} (time-domain) is not built on the device path yet")
+        self.ensure_band(band)
+        _check_k(len(self._sum_trials), metric.value)
+        out = self._plan.pair_metrics(self._slots(), (metric.value,), band.lo_bin, band.n_bins, per_bin=False,
+                                      band=True)
+        return _network_from_band(metric, band, len(self._sum_trials), self.n_channels, out[metric.value]["band"],
+                                  self.positions, self.node_ids)
+
+    def update_and_finalize(self, new_epoch: EpochMatrix, metric: MetricId, band: FrequencyBand):
+        self.add_trial(new_epoch)
+        return self.finalize(metric, band)
+
+    def reset(self) -> None:
+        self.__init__(self.n_channels, self.nfft, self.sfreq, storage_mode=self.cache.enabled,
+                      max_lag=self.max_lag, spectral_mode=self.spectral_mode, positions=self.positions,
+                      node_ids=self.node_ids, accumulate_band=self._accumulate_band, taper=self.taper,
+                      slot_capacity=self._slot_capacity)
+
+    def rebuild_last(self, n_last: int) -> None:
+        """Sums over the most recent ``n_last`` cached trials (metrics.py:450-460):
+        a new slot list over the cached spectra, no FFTs and no re-fold."""
+        if not self.cache.enabled:
+            raise ParameterError("trial-window rebuild requires storage mode")
+        keep = sorted(self.cache.epochs)[-n_last:] if n_last > 0 else []
+        self._sum_trials = list(keep)
+        self.n_trials = len(keep)
+
+
+def convergence_curve(epochs, metric: MetricId, nfft: int, band: FrequencyBand, n_top: int = 20,
+                      max_lag: int | None = None):
+    """Stability-of-the-final-network curve over trial count (metrics.py:501-528)."""
+    engine = ConnectivityEngine(epochs[0].n_channels, nfft, epochs[0].sfreq, storage_mode=True, max_lag=max_lag,
+                                slot_capacity=len(epochs))
+    snapshots, counts = [], []
+    for k, ep in enumerate(epochs, start=1):
+        engine.add_trial(ep)
+        try:
+            net = engine.finalize(metric, band)
+        except DegenerateTrialCountError:
+            continue
+        w = np.abs(net.weights)
+        wmax = w.max()
+        snapshots.append(w / wmax if wmax > 0 else w)
+        counts.append(k)
+    top = np.argsort(-snapshots[-1])[:n_top]
+    curve = np.array([s[top].mean() for s in snapshots])
+    return np.array(counts), curve

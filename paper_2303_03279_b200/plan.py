@@ -199,6 +199,15 @@ class DevicePlan:
         return (_wrap(x64.value, shape, torch.complex128, self.device, self),
                 _wrap(x32.value, shape, torch.complex64, self.device, self))
 
+    def put_spectra(self, spectra: torch.Tensor, slot0: int, bin_lo: int = 0, stream=None) -> None:
+        """Upload complex128 spectra [n, N, nbins] (trial_spectra layout) into slots slot0..."""
+        spectra = spectra.to(device=self.device, dtype=torch.complex128).contiguous()
+        if spectra.dim() != 3 or spectra.shape[1] != self.n_nodes:
+            raise ParameterError(f"spectra must be [n, {self.n_nodes}, bins], got {tuple(spectra.shape)}")
+        self._last_put = spectra
+        _lib.check(_lib.lib().cs_put_spectra(self._h, ctypes.c_void_p(spectra.data_ptr()), int(spectra.shape[0]),
+                                             int(bin_lo), int(spectra.shape[2]), int(slot0), _stream_ptr(stream)))
+
     def fft_call_count(self) -> int:
         return int(_lib.lib().cs_fft_call_count(self._h))
 

@@ -1,0 +1,344 @@
+"""Drop-in for connstream.spectral (reference src/spectral.py) on the B200 path.
+
+Same names, arguments and errors; the arithmetic runs in libcsconn.so:
+  * trial_spectra / fft_real      -> K1 (cs_spectra), fp64 demean + taper + DFT
+  * SpectrumSet                    -> a device accumulator: the folded trials'
+    spectra live in an HBM slot ring; metric finalisers run the fused pair
+    kernels over those slots (the reference's running sums are materialised
+    only when an attribute such as ``csd_sum`` is read).
+  * accumulate_spectra / accumulate_epoch keep the bins/count semantics of
+    spectral.py:244-286 (fixed mode; welch mode is not built yet).
+
+Reference anchors: spectral.py:18-30 (FFT counter), :49-97 (spectra),
+:114-122 (pair order), :125-201 (SpectrumSet), :204-286 (fold).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+from .core import EpochMatrix, ParameterError
+from .plan import DevicePlan, pow2_scale
+
+_FFT_CALLS = 0
+
+
+def fft_call_count() -> int:
+    return _FFT_CALLS
+
+
+def reset_fft_call_count() -> None:
+    global _FFT_CALLS
+    _FFT_CALLS = 0
+
+
+def _count_ffts(n: int) -> None:
+    global _FFT_CALLS
+    _FFT_CALLS += int(n)
+
+
+def n_bins_for(nfft: int) -> int:
+    return nfft // 2 + 1
+
+
+def worker_count() -> int:
+    """CONNSTREAM_THREADS-capped pool size (spectral.py:37-46); kept for callers
+    that size host pools -- the device path does not use host threads."""
+    n = os.cpu_count() or 1
+    cap = os.environ.get("CONNSTREAM_THREADS")
+    if cap:
+        try:
+            n = min(n, max(1, int(cap)))
+        except ValueError:
+            pass
+    return n
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2303_03279_b200 needs a CUDA device; there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _as_device_samples(data) -> torch.Tensor:
+    if isinstance(data, torch.Tensor):
+        t = data
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.double()
+        return t.to(_device())
+    return torch.as_tensor(np.asarray(data, dtype=np.float64), device=_device())
+
+
+_SPEC_PLANS: dict = {}
+
+
+def _spectra_plan(C: int, T: int, nfft: int, taper) -> DevicePlan:
+    key = (C, T, nfft, None if taper is None else (taper if isinstance(taper, str) else id(taper)))
+    plan = _SPEC_PLANS.get(key)
+    if plan is None:
+        if len(_SPEC_PLANS) > 16:
+            _SPEC_PLANS.clear()
+        plan = DevicePlan(C, T, nfft, 0, nfft // 2, taper=taper, slot_capacity=1, device=_device())
+        _SPEC_PLANS[key] = plan
+    return plan
+
+
+def device_trial_spectra(data, nfft: int, taper=None) -> torch.Tensor:
+    """complex128 [C, nfft//2+1] on the device (K1 over all bins)."""
+    x = _as_device_samples(data)
+    if x.dim() == 1:
+        x = x[None]
+    C, T = x.shape
+    plan = _spectra_plan(C, T, nfft, taper)
+    plan.spectra(x[None].contiguous(), 0)
+    _count_ffts(C)
+    return plan.get_spectra(torch.zeros(1, dtype=torch.int32, device=plan.device))[0]
+
+
+def fft_real(signal, nfft: int, taper=None) -> np.ndarray:
+    """One-sided DFT of a real signal after mean removal (spectral.py:65-79)."""
+    if nfft < 2:
+        raise ParameterError(f"nfft must be >= 2, got {nfft}")
+    sig = np.asarray(signal, dtype=np.float64).reshape(-1)
+    if sig.size < 1:
+        raise ParameterError("empty signal")
+    return device_trial_spectra(sig[None], nfft, taper)[0].cpu().numpy()
+
+
+def trial_spectra(epoch: EpochMatrix, nfft: int, mode: str = "fixed", taper=None) -> np.ndarray:
+    """Per-channel one-sided spectra, rows = channels (spectral.py:82-97)."""
+    if nfft < 2:
+        raise ParameterError(f"nfft must be >= 2, got {nfft}")
+    if mode not in ("fixed", "welch"):
+        raise ParameterError(f"unknown spectral mode {mode!r}")
+    if mode == "welch":
+        raise ParameterError("welch spectral mode is not built on the device path yet")
+    return device_trial_spectra(epoch.data, nfft, taper).cpu().numpy()
+
+
+def pair_index(n_channels: int):
+    """Upper-triangle (i < j) channel pairs in row-major order (spectral.py:114-116)."""
+    return np.triu_indices(n_channels, k=1)
+
+
+def pair_row_slice(n_channels: int, i: int) -> slice:
+    """Slice of the pair axis holding pairs (i, i+1) .. (i, n-1) (spectral.py:119-122)."""
+    off = i * (n_channels - 1) - i * (i - 1) // 2
+    return slice(off, off + n_channels - 1 - i)
+
+
+class SpectrumSet:
+    """Device accumulator with the reference's SpectrumSet interface.
+
+    The folded trials' full-bin spectra are held in an HBM slot ring together
+    with the column mask each fold covered (``bins``) and whether it counted
+    (``count``).  Metric finalisers (metrics.py) run the fused pair kernels over
+    the slots; the reference's [P, B] running sums are built on first access.
+    """
+
+    def __init__(self, n_channels: int, nfft: int):
+        if nfft < 2:
+            raise ParameterError("nfft must be >= 2")
+        if n_channels < 1:
+            raise ParameterError("need at least one channel")
+        self.n_channels = int(n_channels)
+        self.nfft = int(nfft)
+        self.n_trials_accumulated = 0
+        self._entries: list[tuple[int, np.ndarray]] = []   # (slot, column mask)
+        self._plan: DevicePlan | None = None
+        self._next_slot = 0
+        self._sums_cache = None
+
+    # -- shape -------------------------------------------------------------
+    @property
+    def n_bins(self) -> int:
+        return n_bins_for(self.nfft)
+
+    @property
+    def n_pairs(self) -> int:
+        return self.n_channels * (self.n_channels - 1) // 2
+
+    # -- storage -------------------------------------------------------------
+    def _ensure_capacity(self, extra: int, scale: float = 1.0) -> None:
+        need = self._next_slot + extra
+        if self._plan is not None and need <= self._plan.slot_capacity:
+            return
+        cap = max(8, 1 << max(need - 1, 1).bit_length())
+        new = DevicePlan(self.n_channels, self.nfft, self.nfft, 0, self.n_bins - 1, slot_capacity=cap,
+                         device=_device(), scale=self._plan.scale if self._plan is not None else scale)
+        if self._plan is not None and self._next_slot:
+            o64, o32 = self._plan.ring()
+            n64, n32 = new.ring()
+            n64[: self._next_slot].copy_(o64[: self._next_slot])
+            n32[: self._next_slot].copy_(o32[: self._next_slot])
+        self._plan = new
+
+    def _fold(self, spectra: torch.Tensor, cols: np.ndarray, count: bool) -> None:
+        """spectra: complex128 device [C, n_bins] (zeros outside ``cols``)."""
+        if self._plan is None:
+            amax = float(spectra.abs().amax()) if spectra.numel() else 0.0
+            scale = pow2_scale(amax / max(self.nfft, 1) ** 0.5, self.nfft) if amax > 0 else 1.0
+            self._ensure_capacity(1, scale)
+        else:
+            self._ensure_capacity(1)
+        slot = self._next_slot
+        self._plan.put_spectra(spectra[None], slot)
+        self._next_slot += 1
+        self._entries.append((slot, cols.copy()))
+        if count:
+            self.n_trials_accumulated += 1
+        self._sums_cache = None
+
+    def slots_for(self, lo: int, hi: int):
+        """Slots whose folds cover every column of [lo, hi] (or None if the
+        column sets differ inside the band)."""
+        sel = [s for s, m in self._entries if m[lo:hi + 1].all()]
+        part = [s for s, m in self._entries if m[lo:hi + 1].any() and not m[lo:hi + 1].all()]
+        return None if part else sel
+
+    @property
+    def plan(self) -> DevicePlan | None:
+        return self._plan
+
+    # -- reference attributes (materialised on access) ----------------------
+    def _sums(self):
+        if self._sums_cache is None:
+            self._sums_cache = _materialise_sums(self)
+        return self._sums_cache
+
+    @property
+    def csd_sum(self):
+        return self._sums()["csd"]
+
+    @property
+    def psd_sum(self):
+        return self._sums()["psd"]
+
+    @property
+    def plv_sum(self):
+        return self._sums()["plv"]
+
+    @property
+    def pli_sum(self):
+        return self._sums()["pli"]
+
+    @property
+    def abs_im_sum(self):
+        return self._sums()["abs_im"]
+
+    @property
+    def im_sum(self):
+        return self.csd_sum.imag
+
+    def csd_entry(self, i: int, j: int) -> np.ndarray:
+        if i == j:
+            return self.psd_sum[i].astype(np.complex128)
+        if i < j:
+            return self.csd_sum[pair_row_slice(self.n_channels, i)][j - i - 1]
+        return np.conj(self.csd_entry(j, i))
+
+    def nbytes(self) -> int:
+        if self._plan is None:
+            return 0
+        return self._next_slot * self.n_channels * self.n_bins * (16 + 8)
+
+    def copy(self) -> "SpectrumSet":
+        out = SpectrumSet(self.n_channels, self.nfft)
+        out.merge(self)
+        out.n_trials_accumulated = self.n_trials_accumulated
+        return out
+
+    def merge(self, other: "SpectrumSet") -> None:
+        """Fold another partial accumulation into this one (associative)."""
+        if (other.n_channels, other.nfft) != (self.n_channels, self.nfft):
+            raise ParameterError("cannot merge accumulators of different shape")
+        if other._plan is not None and other._entries:
+            slots = torch.tensor([s for s, _ in other._entries], dtype=torch.int32, device=other._plan.device)
+            spec = other._plan.get_spectra(slots)
+            for k, (_, m) in enumerate(other._entries):
+                if self._plan is None:
+                    self._ensure_capacity(len(other._entries), other._plan.scale)
+                self._ensure_capacity(1)
+                self._plan.put_spectra(spec[k:k + 1], self._next_slot)
+                self._entries.append((self._next_slot, m.copy()))
+                self._next_slot += 1
+        self.n_trials_accumulated += other.n_trials_accumulated
+        self._sums_cache = None
+
+
+def _materialise_sums(acc: SpectrumSet) -> dict:
+    """The reference's running sums (spectral.py:136-141, fold of :216-241) from
+    the cached spectra, evaluated on the device in complex128 (an accessor for
+    callers that read the sums directly; the finalisers never use it)."""
+    C, B = acc.n_channels, acc.n_bins
+    P = acc.n_pairs
+    out = {"csd": np.zeros((P, B), np.complex128), "psd": np.zeros((C, B)), "plv": np.zeros((P, B), np.complex128),
+           "pli": np.zeros((P, B)), "abs_im": np.zeros((P, B))}
+    if not acc._entries:
+        return out
+    dev = acc._plan.device
+    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.int32, device=dev)
+    X = acc._plan.get_spectra(slots)                       # [K, C, B] complex128
+    masks = torch.tensor(np.stack([m for _, m in acc._entries]), device=dev)  # [K, B]
+    pi, pj = (torch.as_tensor(a, device=dev) for a in pair_index(C))
+    tiny = np.finfo(np.float64).tiny
+    psd = (X.abs() ** 2 * masks[:, None, :]).sum(0)
+    csd_s = torch.zeros((P, B), dtype=torch.complex128, device=dev)
+    plv_s = torch.zeros_like(csd_s)
+    pli_s = torch.zeros((P, B), dtype=torch.float64, device=dev)
+    abs_s = torch.zeros_like(pli_s)
+    step = max(1, (1 << 24) // max(B, 1))
+    for p0 in range(0, P, step):
+        a, b = pi[p0:p0 + step], pj[p0:p0 + step]
+        csd = X[:, a, :] * torch.conj(X[:, b, :])          # [K, p, B]
+        im = csd.imag.clone()
+        im[im.abs() <= 1e-13 * csd.real.abs()] = 0.0
+        csd = torch.complex(csd.real, im)
+        mag = csd.abs()
+        unit = torch.where(mag > tiny, csd / torch.where(mag > tiny, mag, torch.ones_like(mag)), torch.zeros_like(csd))
+        w = masks[:, None, :].to(torch.float64)
+        csd_s[p0:p0 + step] = (csd * w).sum(0)
+        plv_s[p0:p0 + step] = (unit * w).sum(0)
+        pli_s[p0:p0 + step] = (torch.sign(im) * w).sum(0)
+        abs_s[p0:p0 + step] = (im.abs() * w).sum(0)
+    out["csd"], out["psd"], out["plv"] = csd_s.cpu().numpy(), psd.cpu().numpy(), plv_s.cpu().numpy()
+    out["pli"], out["abs_im"] = pli_s.cpu().numpy(), abs_s.cpu().numpy()
+    return out
+
+
+def _cols_mask(n_bins: int, bins) -> np.ndarray:
+    m = np.zeros(n_bins, dtype=bool)
+    if bins is None:
+        m[:] = True
+    else:
+        m[np.arange(n_bins)[bins]] = True
+    return m
+
+
+def accumulate_spectra(acc: SpectrumSet, spectra, bins=None, count: bool = True) -> SpectrumSet:
+    """Fold one trial's spectra into the accumulator (spectral.py:244-261)."""
+    if isinstance(spectra, torch.Tensor):
+        shape = tuple(spectra.shape)
+    else:
+        spectra = np.asarray(spectra)
+        shape = spectra.shape
+    if shape != (acc.n_channels, acc.n_bins):
+        raise ParameterError(f"spectra shape {shape} does not match accumulator ({acc.n_channels}, {acc.n_bins})")
+    cols = _cols_mask(acc.n_bins, bins)
+    spec = torch.as_tensor(spectra, dtype=torch.complex128, device=_device())
+    if not cols.all():
+        spec = spec * torch.as_tensor(cols, device=spec.device)[None, :]
+    acc._fold(spec, cols, count)
+    return acc
+
+
+def accumulate_epoch(acc: SpectrumSet, epoch: EpochMatrix, mode: str = "fixed", bins=None, taper=None):
+    """Compute and accumulate one trial; returns the spectra (spectral.py:264-286)."""
+    if mode == "welch" and epoch.n_samples >= 2 * acc.nfft:
+        raise ParameterError("welch spectral mode is not built on the device path yet")
+    spec = device_trial_spectra(epoch.data, acc.nfft, taper)
+    cols = _cols_mask(acc.n_bins, bins)
+    acc._fold(spec if cols.all() else spec * torch.as_tensor(cols, device=spec.device)[None, :], cols, True)
+    return spec.cpu().numpy()

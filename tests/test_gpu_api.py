@@ -1,0 +1,294 @@
+"""The reference's own test strategy (pkg/tests/test_spectral.py, test_metrics.py,
+test_acceptance.py) replayed against the drop-in package on the GPU, with the
+pinned oracle as the checker.  Tolerances: north_star (1e-4 coherency family,
+1e-3 phase-lag family; fp32 outputs vs fp64)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2303_03279_b200 import core
+from paper_2303_03279_b200.core import (DegenerateTrialCountError, EpochMatrix, FrequencyBand, MetricId,
+                                        ParameterError)
+from paper_2303_03279_b200 import metrics as M
+from paper_2303_03279_b200 import spectral as S
+
+pytestmark = pytest.mark.gpu
+TOL = {"COHY": 1e-4, "COH": 1e-4, "IMAGCOHY": 1e-4, "PLV": 1e-4, "PLI": 1e-3, "USPLI": 1e-3, "WPLI": 1e-3,
+       "DSWPLI": 1e-3}
+
+
+def make_epochs(n_trials, n_channels, n_samples, seed=0, sfreq=600.0):
+    rng = np.random.default_rng(seed)
+    return [EpochMatrix(data=rng.standard_normal((n_channels, n_samples)), sfreq=sfreq, trial_index=k)
+            for k in range(n_trials)]
+
+
+def accumulated(epochs, nfft):
+    acc = S.SpectrumSet(epochs[0].n_channels, nfft)
+    for ep in epochs:
+        S.accumulate_epoch(acc, ep)
+    return acc
+
+
+# ---------------------------------------------------------------- spectral (test_spectral.py)
+class TestFftReal:
+    def test_matches_naive_dft(self):
+        rng = np.random.default_rng(0)
+        for n, nfft in [(64, 64), (100, 64), (40, 64)]:
+            x = rng.standard_normal(n)
+            got = S.fft_real(x, nfft)
+            want = O.trial_spectra(x[None], nfft, method="dft")[0]
+            np.testing.assert_allclose(got, want, atol=1e-9)
+
+    def test_mean_removed(self):
+        assert abs(S.fft_real(np.full(32, 3.7), 32)[0]) < 1e-12
+
+    def test_invalid(self):
+        with pytest.raises(ParameterError):
+            S.fft_real(np.ones(8), 1)
+        with pytest.raises(ParameterError):
+            S.fft_real(np.array([]), 8)
+
+    def test_trial_spectra_matches_numpy_rfft(self):
+        ep = make_epochs(1, 6, 300, seed=4)[0]
+        got = S.trial_spectra(ep, 256)
+        want = O.trial_spectra(ep.data, 256)
+        assert got.shape == (6, 129)
+        np.testing.assert_allclose(got, want, atol=1e-9)
+        assert np.all(got[:, 0] == 0)
+        assert np.all(got[:, -1].imag == 0)
+
+
+class TestSpectrumSet:
+    def test_shapes(self):
+        acc = S.SpectrumSet(4, 64)
+        assert acc.n_bins == 33 and acc.n_pairs == 6
+
+    def test_sums_match_direct_accumulation(self):
+        eps = make_epochs(4, 3, 24, seed=5)
+        acc = S.SpectrumSet(3, 24)
+        specs = [S.trial_spectra(ep, 24) for ep in eps]
+        for s in specs:
+            S.accumulate_spectra(acc, s)
+        pi, pj = S.pair_index(3)
+        np.testing.assert_allclose(acc.csd_sum, sum(s[pi] * np.conj(s[pj]) for s in specs), atol=1e-10)
+        np.testing.assert_allclose(acc.psd_sum, sum(np.abs(s) ** 2 for s in specs), atol=1e-10)
+        np.testing.assert_array_equal(acc.im_sum, acc.csd_sum.imag)
+        assert acc.n_trials_accumulated == 4
+
+    def test_merge_associative(self):
+        eps = make_epochs(6, 3, 24, seed=9)
+        whole = accumulated(eps, 24)
+        a, b = accumulated(eps[:2], 24), accumulated(eps[2:], 24)
+        a.merge(b)
+        np.testing.assert_allclose(a.csd_sum, whole.csd_sum, atol=1e-10)
+        np.testing.assert_allclose(M.wpli_bins(a), M.wpli_bins(whole), atol=1e-6)
+        assert a.n_trials_accumulated == 6
+        with pytest.raises(ParameterError):
+            S.SpectrumSet(3, 24).merge(S.SpectrumSet(4, 24))
+
+    def test_copy_independent(self):
+        acc = S.SpectrumSet(3, 16)
+        cp = acc.copy()
+        S.accumulate_epoch(acc, make_epochs(1, 3, 16)[0])
+        assert cp.n_trials_accumulated == 0
+
+    def test_fft_counter_counts_per_channel(self):
+        S.reset_fft_call_count()
+        S.accumulate_epoch(S.SpectrumSet(7, 32), make_epochs(1, 7, 32)[0])
+        assert S.fft_call_count() == 7
+
+    def test_pair_row_slices_tile_pair_axis(self):
+        for C in range(2, 31):
+            pi, pj = S.pair_index(C)
+            for i in range(C - 1):
+                sl = S.pair_row_slice(C, i)
+                assert pi[sl].tolist() == [i] * (C - 1 - i)
+
+
+# ---------------------------------------------------------------- metrics (test_metrics.py)
+class TestSpectralAgainstOracle:
+    @pytest.mark.parametrize("name", list(TOL))
+    def test_matches_reference_restatement(self, name):
+        epochs = make_epochs(6, 4, 32, seed=11)
+        acc = accumulated(epochs, 32)
+        got = M._SPECTRAL_BINS[MetricId[name]](acc)
+        want = O.compute([e.data for e in epochs], 32, 0, 16, metrics=(name,))[0][name]["bins"]
+        assert np.abs(got - want).max() <= TOL[name]
+
+
+class TestMetricBounds:
+    @pytest.mark.parametrize("seed", range(8))
+    def test_ranges(self, seed):
+        acc = accumulated(make_epochs(4, 3, 24, seed=seed), 24)
+        eps = 1e-6
+        assert np.all(M.coh_bins(acc) <= 1 + eps) and np.all(M.coh_bins(acc) >= 0)
+        assert np.all(np.abs(M.imagcohy_bins(acc)) <= 1 + eps)
+        assert np.all((M.plv_bins(acc) >= 0) & (M.plv_bins(acc) <= 1 + eps))
+        assert np.all((M.pli_bins(acc) >= 0) & (M.pli_bins(acc) <= 1 + eps))
+        assert np.all((M.wpli_bins(acc) >= 0) & (M.wpli_bins(acc) <= 1 + eps))
+        assert np.all(M.dswpli_bins(acc) <= M.wpli_bins(acc) + eps)
+        assert np.all(M.uspli_bins(acc) >= -1.0 / (acc.n_trials_accumulated - 1) - eps)
+
+    def test_uspli_needs_two_trials(self):
+        with pytest.raises(DegenerateTrialCountError):
+            M.uspli_bins(accumulated(make_epochs(1, 3, 24), 24))
+
+    def test_no_trials_degenerate(self):
+        acc = S.SpectrumSet(3, 24)
+        for fn in M._SPECTRAL_BINS.values():
+            with pytest.raises(DegenerateTrialCountError):
+                fn(acc)
+
+    def test_wpli_zero_over_zero_is_zero(self):
+        data = np.tile(np.sin(np.arange(32) * 0.3), (2, 1))
+        acc = accumulated([EpochMatrix(data=data, sfreq=100.0)] * 3, 32)
+        assert np.all(M.wpli_bins(acc) == 0.0)
+        assert np.all(M.pli_bins(acc) == 0.0)
+
+
+class TestFinalizeSpectral:
+    def test_band_average(self):
+        acc = accumulated(make_epochs(4, 3, 32, seed=51), 32)
+        band = FrequencyBand(3, 7, 600.0 / 32)
+        net = M.finalize_spectral(acc, MetricId.COH, band)
+        np.testing.assert_allclose(net.weights, M.coh_bins(acc)[:, 3:8].mean(axis=1), atol=1e-6)
+        assert net.n_trials == 4
+
+    def test_cohy_weight_is_magnitude_of_mean(self):
+        acc = accumulated(make_epochs(4, 3, 32, seed=52), 32)
+        band = FrequencyBand(2, 6, 600.0 / 32)
+        net = M.finalize_spectral(acc, MetricId.COHY, band)
+        cmean = M.cohy_bins(acc)[:, 2:7].mean(axis=1)
+        np.testing.assert_allclose(net.complex_weights, cmean, atol=1e-6)
+        np.testing.assert_allclose(net.weights, np.abs(cmean), atol=1e-6)
+
+    def test_band_limited_equals_full_then_crop(self):
+        acc = accumulated(make_epochs(4, 3, 32, seed=53), 32)
+        np.testing.assert_allclose(M.wpli_bins(acc, FrequencyBand(4, 9, 1.0)), M.wpli_bins(acc)[:, 4:10], atol=1e-6)
+
+    def test_non_spectral_rejected(self):
+        acc = accumulated(make_epochs(2, 3, 32), 32)
+        with pytest.raises(ParameterError):
+            M.finalize_spectral(acc, MetricId.COR, FrequencyBand(0, 3, 1.0))
+
+
+class TestEngine:
+    SPECTRAL = [m for m in MetricId if m.is_spectral]
+
+    def test_incremental_equals_batch_all_metrics(self):
+        epochs = make_epochs(8, 4, 40, seed=61)
+        band = FrequencyBand(2, 8, 600.0 / 48)
+        for metric in self.SPECTRAL:
+            engine = M.ConnectivityEngine(4, 48, 600.0, storage_mode=False)
+            net = None
+            for ep in epochs:
+                try:
+                    net = engine.update_and_finalize(ep, metric, band)
+                except DegenerateTrialCountError:
+                    assert metric is MetricId.USPLI and engine.n_trials == 1
+            batch = M.compute_metric(epochs, metric, 48, band)
+            np.testing.assert_allclose(net.weights, batch.weights, atol=1e-6, err_msg=metric.value)
+
+    def test_metric_switch_zero_new_ffts(self):
+        epochs = make_epochs(6, 4, 40, seed=62)
+        engine = M.ConnectivityEngine(4, 48, 600.0, storage_mode=True)
+        band = FrequencyBand(2, 8, 600.0 / 48)
+        for ep in epochs:
+            engine.add_trial(ep)
+        S.reset_fft_call_count()
+        for metric in (MetricId.COH, MetricId.WPLI, MetricId.PLV, MetricId.PLI, MetricId.DSWPLI):
+            engine.finalize(metric, band)
+        assert S.fft_call_count() == 0
+
+    def test_rebuild_last_window(self):
+        epochs = make_epochs(6, 3, 32, seed=64)
+        band = FrequencyBand(1, 6, 1.0)
+        engine = M.ConnectivityEngine(3, 32, 600.0, storage_mode=True)
+        for ep in epochs:
+            engine.add_trial(ep)
+        S.reset_fft_call_count()
+        engine.rebuild_last(3)
+        net = engine.finalize(MetricId.COH, band)
+        assert S.fft_call_count() == 0
+        batch = M.compute_metric(epochs[-3:], MetricId.COH, 32, band)
+        np.testing.assert_allclose(net.weights, batch.weights, atol=1e-6)
+        assert net.n_trials == 3
+
+    def test_rebuild_requires_storage(self):
+        with pytest.raises(ParameterError):
+            M.ConnectivityEngine(3, 32, 600.0, storage_mode=False).rebuild_last(2)
+
+    def test_reset_and_channel_mismatch(self):
+        engine = M.ConnectivityEngine(3, 32, 600.0)
+        engine.add_trial(make_epochs(1, 3, 32)[0])
+        engine.reset()
+        assert engine.n_trials == 0 and not engine.cache.spectra
+        with pytest.raises(ParameterError):
+            engine.add_trial(make_epochs(1, 4, 32)[0])
+
+    def test_band_limited_accumulation_matches_full(self):
+        epochs = make_epochs(6, 4, 40, seed=65)
+        limited = M.ConnectivityEngine(4, 48, 600.0, storage_mode=True, accumulate_band=(10, 15))
+        for ep in epochs:
+            limited.add_trial(ep)
+        S.reset_fft_call_count()
+        for band in (FrequencyBand(10, 15, 12.5), FrequencyBand(0, 24, 12.5)):
+            for metric in (MetricId.COH, MetricId.WPLI, MetricId.PLV):
+                got = limited.finalize(metric, band)
+                want = M.compute_metric(epochs, metric, 48, band)
+                np.testing.assert_allclose(got.weights, want.weights, atol=1e-6)
+        with pytest.raises(ParameterError):
+            M.ConnectivityEngine(4, 48, 600.0, accumulate_band=(10, 99))
+
+    def test_cache_memory_accounting(self):
+        engine = M.ConnectivityEngine(3, 32, 600.0, storage_mode=True)
+        assert engine.cache.memory_bytes() == 0
+        engine.add_trial(make_epochs(1, 3, 32)[0])
+        assert engine.cache.memory_bytes() > 0
+
+    def test_convergence_curve_final_value(self):
+        epochs = make_epochs(10, 4, 40, seed=71)
+        band = FrequencyBand(2, 8, 600.0 / 48)
+        counts, curve = M.convergence_curve(epochs, MetricId.COH, 48, band, n_top=3)
+        assert counts.tolist() == list(range(1, 11))
+        net = M.compute_metric(epochs, MetricId.COH, 48, band)
+        w = net.weights / net.weights.max()
+        assert np.isclose(curve[-1], np.sort(w)[-3:].mean(), atol=1e-6)
+
+
+# ---------------------------------------------------------------- acceptance (test_acceptance.py)
+def test_criterion_1_oracle_equivalence():
+    epochs = make_epochs(20, 8, 64, seed=101)
+    acc = accumulated(epochs, 64)
+    want, _ = O.compute([e.data for e in epochs], 64, 0, 32)
+    for metric, fn in M._SPECTRAL_BINS.items():
+        assert np.abs(fn(acc) - want[metric.value]["bins"]).max() <= TOL[metric.value], metric.value
+
+
+def test_criterion_3_zero_lag_copies():
+    rng = np.random.default_rng(7)
+    t = np.arange(96) / 600.0
+    eps = []
+    for k in range(60):
+        s = np.sin(2 * np.pi * 18.0 * t + rng.uniform(0, 2 * np.pi))
+        eps.append(EpochMatrix(data=np.vstack([s, 0.7 * s, 0.4 * s]), sfreq=600.0, trial_index=k))
+    band = FrequencyBand(15, 21, 1.0)
+    for metric in (MetricId.IMAGCOHY, MetricId.PLI, MetricId.WPLI):
+        net = M.compute_metric(eps, metric, 600, band)
+        assert np.all(np.abs(net.weights) <= 1e-9), (metric, net.weights)
+    for metric in (MetricId.COH, MetricId.PLV):
+        assert np.all(M.compute_metric(eps, metric, 600, band).weights >= 0.99)
+
+
+@pytest.mark.parametrize("metric", ["COH", "IMAGCOHY"])
+def test_reference_threshold_fixture(metric):
+    """The reference's golden network (export_threshold_fixtures.py) through compute_metric."""
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / "sim2024_thresh.npz")
+    eps = [EpochMatrix(data=e, sfreq=600.0, trial_index=k) for k, e in enumerate(g["epochs"])]
+    net = M.compute_metric(eps, MetricId[metric], 600, FrequencyBand(15, 21, 1.0))
+    want = g["band_" + metric]
+    assert np.abs(net.weights - want).max() <= 1e-4
+    assert np.abs(net.weights / np.abs(net.weights).max() - want / np.abs(want).max()).max() <= 1e-4
