@@ -42,6 +42,8 @@ struct LagArgs {
   int64_t pair_base, pair_stride;
   float* bins[5];    // IMAGCOHY, PLI, USPLI, WPLI, DSWPLI : [nbb][pair_stride]
   float* band[5];
+  float* plv_bins;   // multitaper only: PLV of the taper-mean CSD (not separable -> CUDA cores)
+  float* plv_band;
   float g;           // guard factor
   float scale2;      // plan scale^2 (fp64 fallback -> fp32 units)
   int4* flags;
@@ -58,24 +60,25 @@ constexpr float kPhantom = 9.765625e-4f;  // 2^-10
 __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int Kp,
                            int N, int N64, int nb, int L, int bin_lo, const float* __restrict__ mag,
                            float4* __restrict__ PkI, float4* __restrict__ PkJ) {
+  // layout [bl][kp][l][n]: taper l of trial pair kp
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int kp = blockIdx.y, bl = blockIdx.z;
+  const int kp = blockIdx.y / L, l = blockIdx.y % L, bl = blockIdx.z;
   if (n >= N64) return;
   float2 va = make_float2(0.f, 0.f), vb = make_float2(0.f, 0.f);
   float2 wb = make_float2(0.f, 0.f);  // J-side value of trial b (phantom differs)
   if (n < N) {
     const int b = bin_lo + bl;
-    va = X32[(((int64_t)slots[2 * kp] * L) * nb + b) * N + n];
+    va = X32[(((int64_t)slots[2 * kp] * L + l) * nb + b) * N + n];
     if (2 * kp + 1 < K) {
-      vb = X32[(((int64_t)slots[2 * kp + 1] * L) * nb + b) * N + n];
+      vb = X32[(((int64_t)slots[2 * kp + 1] * L + l) * nb + b) * N + n];
       wb = make_float2(vb.x, -vb.y);
-    } else {
+    } else if (l == 0) {  // phantom lives in taper 0 only: t = M_i M_j 2^-20, re = 0
       const float m = mag[(int64_t)bl * N + n] * kPhantom;
       vb = make_float2(0.f, m);
       wb = make_float2(m, -0.f);
     }
   }
-  const int64_t o = ((int64_t)bl * Kp + kp) * N64 + n;
+  const int64_t o = (((int64_t)bl * Kp + kp) * L + l) * N64 + n;
   PkI[o] = make_float4(va.x, vb.x, va.y, vb.y);
   PkJ[o] = make_float4(va.x, wb.x, -va.y, wb.y);
 }
@@ -92,13 +95,21 @@ constexpr int kTR = 4, kTC = 2;
 constexpr int kTY = kTile / kTR, kTX = kTile / kTC;  // 16 x 32 = 512 threads
 constexpr int kLagThreads = kTY * kTX;
 constexpr int kNP = kTR * kTC;
-constexpr int kStageF4 = kKC * kTile;                 // float4 per side per stage
+template <int L>
+struct LagShape {
+  static constexpr int KC = L == 1 ? kKC : kKC / L;  // trial pairs per stage
+  static constexpr int F4 = KC * L * kTile;           // float4 per side per stage
+};
 
+template <int L, bool PLVK>
 __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
+  constexpr int KC = LagShape<L>::KC;
+  constexpr int kStageF4 = LagShape<L>::F4;
+  constexpr int NM = PLVK ? 6 : 5;                     // band metrics kept in smem
   extern __shared__ float4 smem4[];
-  float4* XI = smem4;                                  // [stages][kKC][64]
-  float4* XJ = smem4 + kLagStages * kStageF4;          // [stages][kKC][64]
-  float* band_s = (float*)(smem4 + 2 * kLagStages * kStageF4);  // [5][64][64]
+  float4* XI = smem4;                                  // [stages][KC][L][64]
+  float4* XJ = smem4 + kLagStages * kStageF4;          // [stages][KC][L][64]
+  float* band_s = (float*)(smem4 + 2 * kLagStages * kStageF4);  // [NM][64][64]
 
   int I, J;
   decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
@@ -111,10 +122,14 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
     bin_mask |= (a.bins[m] != nullptr) << m;
     band_mask |= (a.band[m] != nullptr) << m;
   }
+  if (PLVK) {
+    bin_mask |= (a.plv_bins != nullptr) << 5;
+    band_mask |= (a.plv_band != nullptr) << 5;
+  }
   if (band_mask)
-    for (int e = tid; e < 5 * kTile * kTile; e += kLagThreads) band_s[e] = 0.f;
+    for (int e = tid; e < NM * kTile * kTile; e += kLagThreads) band_s[e] = 0.f;
 
-  const int n_stage = (a.Kp + kKC - 1) / kKC;   // stages per bin
+  const int n_stage = (a.Kp + KC - 1) / KC;     // stages per bin
   const int total = n_stage * a.nbb;            // flat (bin, stage) sequence
   const bool odd = a.K & 1;
   const float invK = 1.f / (float)a.K;
@@ -125,15 +140,14 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
   auto issue = [&](int t) {
     if (t < total) {
       const int bl = t / n_stage, st = t % n_stage;
-      const int kp0 = st * kKC;
+      const int kp0 = st * KC;
       float4* dI = XI + (t % kLagStages) * kStageF4;
       float4* dJ = XJ + (t % kLagStages) * kStageF4;
-#pragma unroll
-      for (int q = 0; q < kStageF4 / kLagThreads; ++q) {
-        const int e = tid + kLagThreads * q;
-        const int kp = e >> 6, node = e & 63;
+      for (int e = tid; e < kStageF4; e += kLagThreads) {
+        const int row = e >> 6, node = e & 63;          // row = kp * L + l
+        const int kp = row / L, l = row % L;
         const int kpg = min(kp0 + kp, a.Kp - 1);  // clamp: rows past Kp are never read
-        const int64_t ob = ((int64_t)bl * a.Kp + kpg) * a.N64;
+        const int64_t ob = (((int64_t)bl * a.Kp + kpg) * L + l) * a.N64;
         cpa16(dI + e, a.PkI + ob + iBase + node);
         cpa16(dJ + e, a.PkJ + ob + jBase + node);
       }
@@ -144,6 +158,7 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
   f2 sim[kNP];
   float sabs[kNP], mn[kNP];
   int neg[kNP];
+  f2 pvr[PLVK ? kNP : 1], pvi[PLVK ? kNP : 1];
   auto reset_acc = [&]() {
 #pragma unroll
     for (int p = 0; p < kNP; ++p) {
@@ -151,29 +166,85 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
       sabs[p] = 0.f;
       mn[p] = 3.0e38f;
       neg[p] = 0;
+      if (PLVK) {
+        pvr[p] = 0ull;
+        pvi[p] = 0ull;
+      }
     }
   };
   auto compute_kp = [&](const float4* sI, const float4* sJ, int kp) {
-    float4 xi[kTR], xj[kTC];
+    if (L == 1) {
+      float4 xi[kTR], xj[kTC];
 #pragma unroll
-    for (int r = 0; r < kTR; ++r) xi[r] = sI[kp * kTile + ty + kTY * r];
+      for (int r = 0; r < kTR; ++r) xi[r] = sI[kp * kTile + ty + kTY * r];
 #pragma unroll
-    for (int c = 0; c < kTC; ++c) xj[c] = sJ[kp * kTile + tx + kTX * c];
+      for (int c = 0; c < kTC; ++c) xj[c] = sJ[kp * kTile + tx + kTX * c];
 #pragma unroll
-    for (int r = 0; r < kTR; ++r) {
-      const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+      for (int r = 0; r < kTR; ++r) {
+        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
 #pragma unroll
-      for (int c = 0; c < kTC; ++c) {
-        const int p = r * kTC + c;
-        const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-        const f2 t = ffma2(ii, jr, fmul2(ir, jn));   // Im(X_i conj X_j) for trials a, b
-        sim[p] = fadd2(sim[p], t);
-        const float tl = lo_of(t), th = hi_of(t);
+        for (int c = 0; c < kTC; ++c) {
+          const int p = r * kTC + c;
+          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+          const f2 t = ffma2(ii, jr, fmul2(ir, jn));   // Im(X_i conj X_j) for trials a, b
+          sim[p] = fadd2(sim[p], t);
+          const float tl = lo_of(t), th = hi_of(t);
+          sabs[p] += fabsf(tl);
+          sabs[p] += fabsf(th);
+          neg[p] += (int)(__float_as_uint(tl) >> 31);
+          neg[p] += (int)(__float_as_uint(th) >> 31);
+          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+        }
+      }
+    } else {
+      // taper sum inside each trial: t = sum_l Im(X_il conj X_jl) (spectral.py:272-283
+      // precedent: the nonlinear terms act on the taper-mean CSD; 1/L cancels)
+      f2 t[kNP], re1[PLVK ? kNP : 1], re2[PLVK ? kNP : 1];
+#pragma unroll
+      for (int p = 0; p < kNP; ++p) {
+        t[p] = 0ull;
+        if (PLVK) re1[p] = re2[p] = 0ull;
+      }
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        float4 xi[kTR], xj[kTC];
+#pragma unroll
+        for (int r = 0; r < kTR; ++r) xi[r] = sI[(kp * L + l) * kTile + ty + kTY * r];
+#pragma unroll
+        for (int c = 0; c < kTC; ++c) xj[c] = sJ[(kp * L + l) * kTile + tx + kTX * c];
+#pragma unroll
+        for (int r = 0; r < kTR; ++r) {
+          const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+#pragma unroll
+          for (int c = 0; c < kTC; ++c) {
+            const int p = r * kTC + c;
+            const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+            t[p] = ffma2(ii, jr, ffma2(ir, jn, t[p]));
+            if (PLVK) {  // Re = sum ir jr + ii ji = re1 - re2 with re2 = sum ii (-ji)
+              re1[p] = ffma2(ir, jr, re1[p]);
+              re2[p] = ffma2(ii, jn, re2[p]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < kNP; ++p) {
+        sim[p] = fadd2(sim[p], t[p]);
+        const float tl = lo_of(t[p]), th = hi_of(t[p]);
         sabs[p] += fabsf(tl);
         sabs[p] += fabsf(th);
         neg[p] += (int)(__float_as_uint(tl) >> 31);
         neg[p] += (int)(__float_as_uint(th) >> 31);
         mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+        if (PLVK) {
+          f2 re;
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(re) : "l"(re1[p]), "l"(re2[p]));
+          const f2 m2 = ffma2(t[p], t[p], fmul2(re, re));
+          const float ml = lo_of(m2), mh = hi_of(m2);
+          const f2 rs = pk(ml > 0.f ? rsqrtf(ml) : 0.f, mh > 0.f ? rsqrtf(mh) : 0.f);
+          pvr[p] = ffma2(re, rs, pvr[p]);
+          pvi[p] = ffma2(t[p], rs, pvi[p]);
+        }
       }
     }
   };
@@ -189,10 +260,10 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
     const int bl = t / n_stage, st = t % n_stage;
     const float4* sI = XI + (t % kLagStages) * kStageF4;
     const float4* sJ = XJ + (t % kLagStages) * kStageF4;
-    const int nkp = min(kKC, a.Kp - st * kKC);
-    if (nkp == kKC) {
+    const int nkp = min(KC, a.Kp - st * KC);
+    if (nkp == KC) {
 #pragma unroll 4
-      for (int kp = 0; kp < kKC; ++kp) compute_kp(sI, sJ, kp);
+      for (int kp = 0; kp < KC; ++kp) compute_kp(sI, sJ, kp);
     } else {
       for (int kp = 0; kp < nkp; ++kp) compute_kp(sI, sJ, kp);
     }
@@ -249,6 +320,15 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
         const float w = s_abs > 0.f ? __fdividef(fabsf(s_im), s_abs) : 0.f;  // WPLI, 0/0 -> 0
         v[3] = fminf(w, 1.f);
         v[4] = v[3] * v[3];                                          // DSWPLI
+        if (PLVK && valid) {  // PLV is continuous: written even for guard-flagged entries
+          // the odd-K phantom contributed the unit phasor (0, 1) to the PLV sums
+          const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
+          const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
+          const float plv = dead ? 0.f : sqrtf(pr * pr + pim * pim) * invK;
+          const int64_t po = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + j;
+          if (bin_mask & 32u) a.plv_bins[bin_off + po] = plv;
+          if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
+        }
         if (valid && !flagged) {
           const int64_t po = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + j;
           float* bs = band_s + li * kTile + lj;
@@ -274,6 +354,7 @@ __global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
 #pragma unroll
       for (int m = 0; m < 5; ++m)
         if (band_mask & (1u << m)) a.band[m][po] = band_s[(m * kTile + li) * kTile + lj] * inv;
+      if (PLVK && (band_mask & 32u)) a.plv_band[po] = band_s[(5 * kTile + li) * kTile + lj] * inv;
     }
   }
 }
@@ -335,27 +416,37 @@ __global__ void k_lag_fallback(const LagArgs a) {
   }
 }
 
-size_t lag_smem_bytes() {
-  return (size_t)2 * kLagStages * kStageF4 * sizeof(float4) + 5 * kTile * kTile * sizeof(float);
+template <int L, bool PLVK>
+static size_t lag_smem_bytes() {
+  return (size_t)2 * kLagStages * LagShape<L>::F4 * sizeof(float4) + (PLVK ? 6 : 5) * kTile * kTile * sizeof(float);
+}
+
+template <int L, bool PLVK>
+static void launch_lag(const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
+  const size_t smem = lag_smem_bytes<L, PLVK>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_pairs_lag<L, PLVK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  k_pairs_lag<L, PLVK><<<(unsigned)n_tiles, kLagThreads, smem, st>>>(a);
 }
 
 void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
-  static bool configured = false;
-  const size_t smem = lag_smem_bytes();
-  if (!configured) {
-    cudaFuncSetAttribute(k_pairs_lag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
   cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
   {
     PhaseMark ph(p, "lag_prep", st);
-    dim3 grid((a.N64 + 127) / 128, a.Kp, a.nbb);
+    dim3 grid((a.N64 + 127) / 128, a.Kp * a.L, a.nbb);
     k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag,
                                      (float4*)a.PkI, (float4*)a.PkJ);
   }
   {
     PhaseMark ph(p, "pairs_lag", st);
-    k_pairs_lag<<<(unsigned)n_tiles, kLagThreads, smem, st>>>(a);
+    const bool plvk = a.plv_bins || a.plv_band;
+    if (a.L == 1) launch_lag<1, false>(a, n_tiles, st);
+    else if (a.L == 2) plvk ? launch_lag<2, true>(a, n_tiles, st) : launch_lag<2, false>(a, n_tiles, st);
+    else if (a.L == 3) plvk ? launch_lag<3, true>(a, n_tiles, st) : launch_lag<3, false>(a, n_tiles, st);
+    else plvk ? launch_lag<4, true>(a, n_tiles, st) : launch_lag<4, false>(a, n_tiles, st);
   }
   {
     PhaseMark ph(p, "lag_fallback", st);
@@ -375,7 +466,12 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
   unsigned any = 0;
   for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
-  if (!any) return 0;
+  const bool plvk = p.L > 1 && (mask & CS_PLV);
+  if (!any && !plvk) return 0;
+  if (p.L > 4) {
+    cs_set_error("at most 4 tapers are supported, got %d", p.L);
+    return -1;
+  }
   LagArgs a{};
   a.X32 = p.X32;
   a.X64 = p.X64;
@@ -384,7 +480,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.slots = slots; a.K = K;
   a.Kp = (K + 1) / 2;
   {
-    const size_t need = (size_t)2 * nbb * a.Kp * a.N64 * sizeof(float4);
+    const size_t need = (size_t)2 * nbb * a.Kp * p.L * a.N64 * sizeof(float4);
     if (need > p.lag_bytes) {
       if (p.lag_ops) cudaFreeAsync(p.lag_ops, st);
       if (cudaMallocAsync(&p.lag_ops, need, st) != cudaSuccess) {
@@ -396,7 +492,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
       p.lag_bytes = need;
     }
     a.PkI = (const float4*)p.lag_ops;
-    a.PkJ = a.PkI + (size_t)nbb * a.Kp * a.N64;
+    a.PkJ = a.PkI + (size_t)nbb * a.Kp * p.L * a.N64;
   }
   a.bin_lo = bin_lo; a.nbb = nbb;
   a.psd = p.psd; a.mag = p.mag;
@@ -410,6 +506,8 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     a.bins[q] = on ? (float*)out->bins[kLagIdx[q]] : nullptr;
     a.band[q] = on ? (float*)out->band[kLagIdx[q]] : nullptr;
   }
+  a.plv_bins = plvk ? (float*)out->bins[3] : nullptr;
+  a.plv_band = plvk ? (float*)out->band[3] : nullptr;
   a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
   a.scale2 = p.scale * p.scale;
   a.flags = p.flags;
@@ -417,10 +515,6 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.flag_cap = p.flag_cap;
   int64_t n_tiles = 0;
   for (int I = rb; I < re; ++I) n_tiles += a.nt - I;
-  if (p.L != 1) {
-    cs_set_error("multitaper phase-lag kernel not built yet");
-    return -1;
-  }
   run_pairs_lag(p, a, n_tiles, st);
   return 2;
 }
@@ -431,12 +525,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
 int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
   const bool do_x = (mask & (CS_COHY | CS_COH)) != 0;
-  const bool do_u = (mask & CS_PLV) != 0;
+  const bool do_u = (mask & CS_PLV) != 0 && p.L == 1;  // multitaper PLV runs in the lag kernel
   if (!do_x && !do_u) return 0;
-  if (p.L != 1) {
-    cs_set_error("multitaper coherency-family kernel not built yet");
-    return -1;
-  }
   if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, out, p.nscale, st)) return -1;
   return 0;  // launches are counted by the phase marks
 }

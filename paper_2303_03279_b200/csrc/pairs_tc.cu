@@ -454,8 +454,8 @@ __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict_
   const int bl = blockIdx.z;
   if (n >= N || k >= K_pad) return;
   float xr = 0.f, xi = 0.f;
-  if (k < K) {
-    const float2 v = X32[(((int64_t)slots[k] * L) * nb + bin_lo + bl) * N + n];
+  if (k < K) {  // contraction index k = trial * L + taper (multitaper: CSD summed over tapers)
+    const float2 v = X32[(((int64_t)slots[k / L] * L + k % L) * nb + bin_lo + bl) * N + n];
     const float s = nscale[(int64_t)bl * N + n];
     xr = v.x * s;
     xi = v.y * s;
@@ -506,7 +506,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     cs_set_error("cuTensorMapEncodeTiled unavailable");
     return false;
   }
-  const int K_pad = (K * 1 + 15) / 16 * 16;  // UMMA K granularity; the last TMA box is zero-filled
+  const int Kc = K * p.L;                       // contraction length: trials x tapers
+  const int K_pad = (Kc + 15) / 16 * 16;        // UMMA K granularity; the last TMA box is zero-filled
   const size_t need = (size_t)nbb * 8 * p.N * K_pad * sizeof(__half);
   if (need > p.tc_bytes) {
     if (p.tc_ops) cudaFreeAsync(p.tc_ops, st);
@@ -522,7 +523,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   {
     PhaseMark ph(p, "tc_prep", st);
     dim3 grid((K_pad + 31) / 32, (p.N + 7) / 8, nbb);
-    k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, K, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
+    k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, Kc, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
   }
   CUtensorMap mapA, mapB;
   cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 8};
@@ -541,7 +542,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     return false;
   }
   TcArgs a{};
-  a.N = p.N; a.K = K; a.K_pad = K_pad; a.nbb = nbb;
+  a.N = p.N; a.K = Kc; a.K_pad = K_pad; a.nbb = nbb;
   a.i_lo = rb * kTile;
   a.i_hi = re * kTile < p.N ? re * kTile : p.N;
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;

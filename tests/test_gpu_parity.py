@@ -46,8 +46,6 @@ CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg
 @pytest.mark.parametrize("case", CASES)
 def test_metrics_match_reference(case, family):
     g = _load(case)
-    if g["taper"].ndim == 2:
-        pytest.skip("multitaper kernels pending")
     K = g["epochs"].shape[0]
     metrics = [m for m in (LAG if family == "lag" else COHF) if not (m == "USPLI" and K < 2)]
     out, _ = _run(g, metrics)
