@@ -198,15 +198,15 @@ def main():
         run_reference(args, c, rank)
         return
 
-    from paper_2303_03279_b200.plan import DevicePlan, pow2_scale, probe_peaks, row_tile_range
+    from paper_2303_03279_b200.plan import DevicePlan, pow2_scale, probe_peaks
     dist, rank, ws, lr = dist_setup()
     dev = torch.device("cuda", lr)
     metrics = tuple(args.metrics.split(",")) if args.metrics else c.metrics
 
     # ---- node block for K1, pair shard for the pair kernels ----
-    nloc = (c.N + ws - 1) // ws
-    n0, n1 = min(rank * nloc, c.N), min((rank + 1) * nloc, c.N)
-    (rb, re), (p0, p1) = row_tile_range(c.N, ws, rank)
+    from paper_2303_03279_b200.shard import allgather_ring, node_block, shard_plan
+    n0, n1, nloc = node_block(c.N, ws, rank)
+    (rb, re), (p0, p1) = shard_plan(c.N, ws, rank)
     x = synth.generate(c, dev, nodes=slice(n0, n1))
     if x.shape[1] < nloc:  # pad the last block so every rank gathers the same size
         x = torch.cat([x, torch.zeros((c.K, nloc - x.shape[1], c.T), dtype=x.dtype, device=dev)], 1)
@@ -228,10 +228,8 @@ def main():
     def step():
         local.spectra(x, 0)
         if ws > 1:  # the exchange step: all-gather node-block spectra over NVLink
-            dist.all_gather_into_tensor(g32.view(-1), L32.reshape(-1))
-            dist.all_gather_into_tensor(g64.view(-1), L64.reshape(-1))
-            F32.copy_(g32.permute(1, 2, 3, 0, 4).reshape(F32.shape[:3] + (ws * nloc,))[..., :c.N])
-            F64.copy_(g64.permute(1, 2, 3, 0, 4).reshape(F64.shape[:3] + (ws * nloc,))[..., :c.N])
+            allgather_ring(L32, F32, dist, g32)
+            allgather_ring(L64, F64, dist, g64)
         full.pair_metrics(slots, metrics, 0, c.n_bins, outputs=outs, row_tiles=(rb, re), pair_base=p0,
                           pair_count=p1 - p0)
 
@@ -320,10 +318,8 @@ def main():
             xd.copy_(xh, non_blocking=True)
             local.spectra(xd, 0)
             if ws > 1:
-                dist.all_gather_into_tensor(g32.view(-1), L32.reshape(-1))
-                dist.all_gather_into_tensor(g64.view(-1), L64.reshape(-1))
-                F32.copy_(g32.permute(1, 2, 3, 0, 4).reshape(F32.shape[:3] + (ws * nloc,))[..., :c.N])
-                F64.copy_(g64.permute(1, 2, 3, 0, 4).reshape(F64.shape[:3] + (ws * nloc,))[..., :c.N])
+                allgather_ring(L32, F32, dist, g32)
+                allgather_ring(L64, F64, dist, g64)
             o = full.pair_metrics(slots, metrics, 0, c.n_bins, per_bin=False, band=True, row_tiles=(rb, re),
                                   pair_base=p0, pair_count=p1 - p0)
             for m in metrics:
