@@ -432,7 +432,12 @@ static void launch_lag(const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   k_pairs_lag<L, PLVK><<<(unsigned)n_tiles, kLagThreads, smem, st>>>(a);
 }
 
-void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
+bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
+                 const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
+                 int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, cudaStream_t st);
+
+bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
   {
     PhaseMark ph(p, "lag_prep", st);
@@ -443,7 +448,12 @@ void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
   {
     PhaseMark ph(p, "pairs_lag", st);
     const bool plvk = a.plv_bins || a.plv_band;
-    if (a.L == 1) launch_lag<1, false>(a, n_tiles, st);
+    if (a.L == 1) {
+      if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
+                       a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters,
+                       a.flag_cap, n_tiles, st))
+        return false;
+    }
     else if (a.L == 2) plvk ? launch_lag<2, true>(a, n_tiles, st) : launch_lag<2, false>(a, n_tiles, st);
     else if (a.L == 3) plvk ? launch_lag<3, true>(a, n_tiles, st) : launch_lag<3, false>(a, n_tiles, st);
     else plvk ? launch_lag<4, true>(a, n_tiles, st) : launch_lag<4, false>(a, n_tiles, st);
@@ -452,6 +462,7 @@ void run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
     PhaseMark ph(p, "lag_fallback", st);
     k_lag_fallback<<<148 * 4, 256, 0, st>>>(a);
   }
+  return true;
 }
 
 }  // namespace cs
@@ -515,7 +526,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.flag_cap = p.flag_cap;
   int64_t n_tiles = 0;
   for (int I = rb; I < re; ++I) n_tiles += a.nt - I;
-  run_pairs_lag(p, a, n_tiles, st);
+  if (!run_pairs_lag(p, a, n_tiles, st)) return -1;
   return 2;
 }
 

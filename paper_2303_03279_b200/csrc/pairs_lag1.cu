@@ -1,0 +1,284 @@
+// K3 (single taper): phase-lag family + IMAGCOHY on the FP32/ALU pipes, with a
+// TMA producer warp and an mbarrier ring instead of CTA-wide barriers.
+//
+// Reference: spectral.py:216-241 (_fold_csd: Im flush, sign(Im), |Im|, Im sums),
+// metrics.py:49-86 (imagcohy / pli / uspli / wpli / dswpli), metrics.py:115-134
+// and core.py:208-215 (band mean).
+//
+// CTA = 64 x 64 node tile x all bins of the band.  16 compute warps (512
+// threads, 16 x 32, each thread 4 x 2 pairs: i = ty + 16 r, j = tx + 32 c) and 1
+// producer warp.  The packed trial-pair operands (k_lag_prep: float4 (re_a, re_b, im_a,
+// im_b), J side with Im negated) are streamed by 2D TMA boxes of 64 nodes x KC
+// trial pairs into a 4-stage ring; consumers wait on the stage's full barrier and
+// release it with one arrive per warp, so stages never need a CTA-wide sync.
+// Per trial pair and pair of nodes: FMUL2 + FFMA2 (t = Im X_i conj X_j for two
+// trials), FADD2 (sum t), 2 FADD |.| (sum |t|), 2 LEA.HI (#(t < 0)), FMNMX3
+// (min |t|, the exact-sign guard of pairs_lag.cu).
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace cs {
+
+constexpr int k1KC = 16;           // trial pairs per stage
+constexpr int k1Stages = 4;
+constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
+constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
+constexpr int k1NP = k1TR * k1TC;
+constexpr int k1Warps = k1TY * k1TX / 32;  // compute warps
+constexpr int k1Threads = (k1Warps + 1) * 32;
+constexpr int k1StageF4 = k1KC * kTile;   // float4 per side per stage
+constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
+
+struct Lag1Args {
+  int N, N64, K, Kp, bin_lo, nbb;
+  const float* psd;
+  const float* mag;
+  int real0, real1, nt, row_begin;
+  int64_t pair_base, pair_stride;
+  float* bins[5];
+  float* band[5];
+  float g;
+  int4* flags;
+  int* counters;
+  int flag_cap;
+};
+
+__global__ void __launch_bounds__(k1Threads, 1)
+k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
+             const Lag1Args a) {
+  extern __shared__ __align__(128) unsigned char lag1_smem[];
+  float4* XI = (float4*)lag1_smem;                       // [stages][KC][64]
+  float4* XJ = XI + k1Stages * k1StageF4;                // [stages][KC][64]
+  float* band_s = (float*)(XJ + k1Stages * k1StageF4);   // [5][64][64]
+  uint64_t* full = (uint64_t*)(band_s + 5 * kTile * kTile);
+  uint64_t* empty = full + k1Stages;
+
+  int I, J;
+  decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
+  const int iBase = I * kTile, jBase = J * kTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  unsigned bin_mask = 0, band_mask = 0;
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    bin_mask |= (a.bins[m] != nullptr) << m;
+    band_mask |= (a.band[m] != nullptr) << m;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < k1Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], k1Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (band_mask)
+    for (int e = threadIdx.x; e < 5 * kTile * kTile; e += k1Threads) band_s[e] = 0.f;
+  __syncthreads();
+
+  const int n_stage = (a.Kp + k1KC - 1) / k1KC;
+  const int total = n_stage * a.nbb;
+
+  if (warp == k1Warps) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int t = 0; t < total; ++t) {
+        const int s = t % k1Stages;
+        mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
+        const int bl = t / n_stage, st = t % n_stage;
+        const int row = bl * a.Kp + st * k1KC;
+        mbar_expect_tx(&full[s], 2 * k1StageF4 * 16);
+        tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
+        tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ compute warps
+  const int tid = threadIdx.x, tx = tid % k1TX, ty = tid / k1TX;
+  const bool odd = a.K & 1;
+  const float invK = 1.f / (float)a.K;
+  const float uspA = a.K > 1 ? (float)a.K / (float)(a.K - 1) : 0.f;
+  const float uspB = a.K > 1 ? 1.f / (float)(a.K - 1) : 0.f;
+
+  f2 sim[k1NP];
+  float sabs[k1NP], mn[k1NP];
+  int neg[k1NP];
+#pragma unroll
+  for (int p = 0; p < k1NP; ++p) {
+    sim[p] = 0ull;
+    sabs[p] = 0.f;
+    mn[p] = 3.0e38f;
+    neg[p] = 0;
+  }
+
+  for (int t = 0; t < total; ++t) {
+    const int s = t % k1Stages;
+    const int bl = t / n_stage, st = t % n_stage;
+    mbar_wait(&full[s], (t / k1Stages) & 1);
+    const float4* sI = XI + s * k1StageF4;
+    const float4* sJ = XJ + s * k1StageF4;
+    const int nkp = min(k1KC, a.Kp - st * k1KC);
+    auto body = [&](int kp) {
+      float4 xi[k1TR], xj[k1TC];
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) xi[r] = sI[kp * kTile + ty + k1TY * r];
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c) xj[c] = sJ[kp * kTile + tx + k1TX * c];
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) {
+        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+#pragma unroll
+        for (int c = 0; c < k1TC; ++c) {
+          const int p = r * k1TC + c;
+          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+          const f2 tt = ffma2(ii, jr, fmul2(ir, jn));
+          sim[p] = fadd2(sim[p], tt);
+          const float tl = lo_of(tt), th = hi_of(tt);
+          sabs[p] += fabsf(tl);
+          sabs[p] += fabsf(th);
+          neg[p] += (int)(__float_as_uint(tl) >> 31);
+          neg[p] += (int)(__float_as_uint(th) >> 31);
+          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+        }
+      }
+    };
+    if (nkp == k1KC) {
+#pragma unroll 2
+      for (int kp = 0; kp < k1KC; ++kp) body(kp);
+    } else {
+      for (int kp = 0; kp < nkp; ++kp) body(kp);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (st + 1 < n_stage) continue;
+
+    // ---- epilogue for bin bl ----
+    const int b = a.bin_lo + bl;
+    const bool real_bin = (b == a.real0) || (b == a.real1);
+    float Mi[k1TR], Mj[k1TC], Pi[k1TR], Pj[k1TC];
+#pragma unroll
+    for (int r = 0; r < k1TR; ++r) {
+      const int i = iBase + ty + k1TY * r;
+      Mi[r] = i < a.N ? a.mag[(int64_t)bl * a.N + i] : 0.f;
+      Pi[r] = i < a.N ? a.psd[(int64_t)bl * a.N + i] : 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < k1TC; ++c) {
+      const int j = jBase + tx + k1TX * c;
+      Mj[c] = j < a.N ? a.mag[(int64_t)bl * a.N + j] : 0.f;
+      Pj[c] = j < a.N ? a.psd[(int64_t)bl * a.N + j] : 0.f;
+    }
+    const int64_t bin_off = (int64_t)bl * a.pair_stride;
+#pragma unroll
+    for (int r = 0; r < k1TR; ++r) {
+      const int li = ty + k1TY * r, i = iBase + li;
+      const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c) {
+        const int p = r * k1TC + c;
+        const int lj = tx + k1TX * c, j = jBase + lj;
+        const bool valid = (i < j) && (j < a.N);
+        const bool dead = real_bin || Mi[r] == 0.f || Mj[c] == 0.f;
+        const bool flagged = valid && !dead && (mn[p] <= a.g * Mi[r] * Mj[c]);
+        if (flagged) {  // rare: the fp64 fallback writes this (pair, bin)
+          const int slot = atomicAdd(&a.counters[0], 1);
+          if (slot < a.flag_cap)
+            a.flags[slot] = make_int4(i, j, bl, 0);
+          else
+            a.counters[1] = 1;
+        }
+        const float tph = odd ? (Mi[r] * k1Phantom) * (Mj[c] * k1Phantom) : 0.f;
+        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+        const float s_abs = dead ? 0.f : sabs[p] - tph;
+        const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
+        const float pp = Pi[r] * Pj[c];
+        float v[5];
+        v[0] = pp > 0.f ? s_im * rsqrtf(pp) : 0.f;
+        const float pli = fabsf((float)pli_sum) * invK;
+        v[1] = pli;
+        v[2] = pli * pli * uspA - uspB;
+        const float w = s_abs > 0.f ? fminf(__fdividef(fabsf(s_im), s_abs), 1.f) : 0.f;
+        v[3] = w;
+        v[4] = w * w;
+        if (valid && !flagged) {
+          const int64_t po = rowoff + j;
+          float* bs = band_s + li * kTile + lj;
+#pragma unroll
+          for (int m = 0; m < 5; ++m) {
+            if (bin_mask & (1u << m)) a.bins[m][bin_off + po] = v[m];
+            if (band_mask & (1u << m)) bs[m * kTile * kTile] += v[m];
+          }
+        }
+        sim[p] = 0ull;
+        sabs[p] = 0.f;
+        mn[p] = 3.0e38f;
+        neg[p] = 0;
+      }
+    }
+  }
+
+  if (band_mask) {
+    // each thread owns its pairs' band slots: no barrier needed
+    const float inv = 1.f / (float)a.nbb;
+#pragma unroll
+    for (int r = 0; r < k1TR; ++r) {
+      const int li = ty + k1TY * r, i = iBase + li;
+      const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c) {
+        const int lj = tx + k1TX * c, j = jBase + lj;
+        if (!(i < j && j < a.N)) continue;
+#pragma unroll
+        for (int m = 0; m < 5; ++m)
+          if (band_mask & (1u << m)) a.band[m][rowoff + j] = band_s[(m * kTile + li) * kTile + lj] * inv;
+      }
+    }
+  }
+}
+
+bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
+                 const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
+                 int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, cudaStream_t st) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    cs_set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  CUtensorMap mI, mJ;
+  cuuint64_t dims[2] = {(cuuint64_t)N64 * 4, (cuuint64_t)nbb * Kp};
+  cuuint64_t strides[1] = {(cuuint64_t)N64 * 16};
+  cuuint32_t box[2] = {(cuuint32_t)kTile * 4, (cuuint32_t)k1KC};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&mI, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)PkI, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS)
+    r = enc(&mJ, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)PkJ, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    cs_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return false;
+  }
+  Lag1Args a{};
+  a.N = N; a.N64 = N64; a.K = K; a.Kp = Kp; a.bin_lo = bin_lo; a.nbb = nbb;
+  a.psd = psd; a.mag = mag; a.real0 = real0; a.real1 = real1; a.nt = nt; a.row_begin = row_begin;
+  a.pair_base = pair_base; a.pair_stride = pair_stride;
+  for (int m = 0; m < 5; ++m) {
+    a.bins[m] = bins[m];
+    a.band[m] = band[m];
+  }
+  a.g = g; a.flags = flags; a.counters = counters; a.flag_cap = flag_cap;
+  const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 5 * kTile * kTile * 4 + 2 * k1Stages * 8;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_pairs_lag1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  k_pairs_lag1<<<(unsigned)n_tiles, k1Threads, smem, st>>>(mI, mJ, a);
+  return true;
+}
+
+}  // namespace cs
