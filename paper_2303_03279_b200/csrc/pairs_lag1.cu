@@ -19,8 +19,8 @@
 
 namespace cs {
 
-constexpr int k1KC = 16;           // trial pairs per stage
-constexpr int k1Stages = 4;
+constexpr int k1KC = 25;           // max trial pairs per stage (balanced per launch)
+constexpr int k1Stages = 2;
 constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
 constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
 constexpr int k1NP = k1TR * k1TC;
@@ -76,6 +76,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   __syncthreads();
 
   const int n_stage = (a.Kp + k1KC - 1) / k1KC;
+  const int kc = (a.Kp + n_stage - 1) / n_stage;   // balanced stage size (<= k1KC)
   const int total = n_stage * a.nbb;
 
   if (warp == k1Warps) {
@@ -85,7 +86,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const int s = t % k1Stages;
         mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
         const int bl = t / n_stage, st = t % n_stage;
-        const int row = bl * a.Kp + st * k1KC;
+        const int row = bl * a.Kp + st * kc;
         mbar_expect_tx(&full[s], 2 * k1StageF4 * 16);
         tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
         tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
@@ -118,7 +119,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     mbar_wait(&full[s], (t / k1Stages) & 1);
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
-    const int nkp = min(k1KC, a.Kp - st * k1KC);
+    const int nkp = min(kc, a.Kp - st * kc);
     auto body = [&](int kp) {
       float4 xi[k1TR], xj[k1TC];
 #pragma unroll
@@ -143,12 +144,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         }
       }
     };
-    if (nkp == k1KC) {
 #pragma unroll 2
-      for (int kp = 0; kp < k1KC; ++kp) body(kp);
-    } else {
-      for (int kp = 0; kp < nkp; ++kp) body(kp);
-    }
+    for (int kp = 0; kp < nkp; ++kp) body(kp);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (st + 1 < n_stage) continue;

@@ -128,8 +128,10 @@ __device__ __forceinline__ void epi_bar() {  // the epilogue warps only
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const TcArgs a) {
-  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+  // dynamic shared memory starts at the (1024-aligned) base of the CTA's window: no
+  // static __shared__ in this kernel.  Indexing the extern array directly keeps every
+  // epilogue access in the shared state space (LDS/STS, not generic LD/ST).
+  extern __shared__ __align__(1024) unsigned char smem[];
   float2* xbuf = (float2*)(smem + kTcStages * kTcStageBytes);          // [128][65] transpose buffer
   float* colfac = (float*)(xbuf + kTcTile * kTcXStride);               // [64] psd_j * s_j^2
   int64_t* rowoff_s = (int64_t*)(colfac + kTcTileJ);                   // [128] output row offsets
@@ -144,6 +146,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
 
   if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // swizzled TMA/UMMA tiles need 1024-byte alignment
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -437,7 +440,7 @@ __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict_
 // ---------------------------------------------------------------- host side
 size_t tc_smem_bytes() {
   return (size_t)kTcStages * kTcStageBytes + (size_t)kTcTile * kTcXStride * sizeof(float2) + kTcTileJ * 4 +
-         kTcTile * 8 + 1024 + 256;
+         kTcTile * 8 + 256;
 }
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
