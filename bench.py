@@ -177,6 +177,66 @@ def run_reference(args, c, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_window(args, c, dist, rank, ws, lr):
+    """Config 4: online sliding window.  A stream of 1045 trials, window w =
+    trials [5w, 5w + 50): per window K1 runs on the 5 new trials only (cached
+    spectra of the other 45 are reused from the HBM ring) and the pair kernels
+    recompute PLV and WPLI over the window's 50 slots -- the work the
+    reference's rebuild_last(50) performs (metrics.py:450-460,
+    pipeline.py:304-309).  Replicas only at N > 1 (each rank its own stream)."""
+    from paper_2303_03279_b200 import synth
+    from paper_2303_03279_b200.plan import DevicePlan, pow2_scale, probe_peaks
+    dev = torch.device("cuda", lr)
+    W = min(synth.CFG4_WINDOWS, args.warmup + args.steps + 1)
+    n_trials = 5 * (W - 1) + 50
+    x = synth.generate(c, dev, trials=range(n_trials))            # [n_trials, N, T] resident in HBM
+    cap = 64
+    plan = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=cap, device=dev,
+                      scale=pow2_scale(float(x.abs().amax()), min(c.T, c.nfft)))
+    slots = torch.tensor([[(5 * w + k) % cap for k in range(50)] for w in range(W)], dtype=torch.int32, device=dev)
+    outs = plan.alloc_outputs(c.metrics, c.n_bins)
+
+    def window(w):
+        if w == 0:
+            plan.spectra(x[0:50], 0)
+        else:
+            plan.spectra(x[5 * w + 45: 5 * w + 50], (5 * w + 45) % cap)
+        plan.pair_metrics(slots[w], c.metrics, 0, c.n_bins, outputs=outs)
+
+    window(0)
+    for w in range(1, 1 + args.warmup):
+        window(w)
+    torch.cuda.synchronize()
+    plan.set_profiling(True)
+    plan.profile()
+    l0 = plan.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(lr) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for w in range(1 + args.warmup, 1 + args.warmup + args.steps):
+            window(w)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    prof = plan.profile()
+    upd = c.n_pairs * c.n_bins * 50
+    per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
+    fp32_ops, fp64_fma = probe_peaks(lr)
+    line = {"metric": "edge*freq*trial updates/s per online window (config 4, PLV + WPLI)", "value": upd / (ms * 1e-3),
+            "unit": "updates/s", "ms_per_window": ms, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY.md 8(d) cfg4 pink noise + planted 20 Hz)",
+            "config": {"workload": f"cfg{c.cfg}: {c.name}", "N": c.N, "window": 50, "new_trials_per_window": 5,
+                       "bins": [c.lo, c.hi], "metrics": list(c.metrics), "parallelism": f"replicas x{ws}",
+                       "updates_per_window": upd},
+            "breakdown": {k: {"ms_per_launch": round(v, 4), "launches": prof[k][1]} for k, v in per.items()},
+            "gpu_launches": plan.launch_count() - l0, "clocks": clk.summary(),
+            "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,6 +260,9 @@ def main():
 
     from paper_2303_03279_b200.plan import DevicePlan, pow2_scale, probe_peaks
     dist, rank, ws, lr = dist_setup()
+    if c.cfg == 4:
+        run_window(args, c, dist, rank, ws, lr)
+        return
     dev = torch.device("cuda", lr)
     metrics = tuple(args.metrics.split(",")) if args.metrics else c.metrics
 

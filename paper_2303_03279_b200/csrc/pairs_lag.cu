@@ -435,7 +435,7 @@ static void launch_lag(const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, cudaStream_t st);
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, cudaStream_t st);
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
@@ -449,9 +449,16 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
     PhaseMark ph(p, "pairs_lag", st);
     const bool plvk = a.plv_bins || a.plv_band;
     if (a.L == 1) {
+      // small pair spaces (few tiles, many bins): split the bins over CTAs for >= 2 waves
+      int nbc = (int)((2 * 148 + n_tiles - 1) / n_tiles);
+      nbc = nbc < 1 ? 1 : (nbc > a.nbb ? a.nbb : nbc);
+      nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);  // no empty chunks
+      if (nbc > 1)
+        for (int m = 0; m < 5; ++m)
+          if (a.band[m]) cudaMemsetAsync(a.band[m], 0, a.pair_stride * sizeof(float), st);
       if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
                        a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters,
-                       a.flag_cap, n_tiles, st))
+                       a.flag_cap, n_tiles, nbc, st))
         return false;
     }
     else if (a.L == 2) plvk ? launch_lag<2, true>(a, n_tiles, st) : launch_lag<2, false>(a, n_tiles, st);

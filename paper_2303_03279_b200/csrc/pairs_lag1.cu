@@ -31,6 +31,7 @@ constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 
 struct Lag1Args {
   int N, N64, K, Kp, bin_lo, nbb;
+  int bpc, nbc;              // bins per CTA, bin chunks per tile (small pair spaces split bins)
   const float* psd;
   const float* mag;
   int real0, real1, nt, row_begin;
@@ -54,7 +55,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   uint64_t* empty = full + k1Stages;
 
   int I, J;
-  decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
+  const int bchunk = blockIdx.x % a.nbc;
+  decode_tile(blockIdx.x / a.nbc, a.nt, a.row_begin, I, J);
+  const int bl0 = bchunk * a.bpc;                      // first bin (of the call's nbb) of this CTA
+  const int nbl = min(a.bpc, a.nbb - bl0);
   const int iBase = I * kTile, jBase = J * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -77,7 +81,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 
   const int n_stage = (a.Kp + k1KC - 1) / k1KC;
   const int kc = (a.Kp + n_stage - 1) / n_stage;   // balanced stage size (<= k1KC)
-  const int total = n_stage * a.nbb;
+  const int total = n_stage * nbl;
 
   if (warp == k1Warps) {
     // ------------------------------------------------------------ TMA producer
@@ -85,7 +89,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       for (int t = 0; t < total; ++t) {
         const int s = t % k1Stages;
         mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
-        const int bl = t / n_stage, st = t % n_stage;
+        const int bl = bl0 + t / n_stage, st = t % n_stage;
         const int row = bl * a.Kp + st * kc;
         mbar_expect_tx(&full[s], 2 * k1StageF4 * 16);
         tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
@@ -115,7 +119,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 
   for (int t = 0; t < total; ++t) {
     const int s = t % k1Stages;
-    const int bl = t / n_stage, st = t % n_stage;
+    const int bl = bl0 + t / n_stage, st = t % n_stage;
     mbar_wait(&full[s], (t / k1Stages) & 1);
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
@@ -228,7 +232,13 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         if (!(i < j && j < a.N)) continue;
 #pragma unroll
         for (int m = 0; m < 5; ++m)
-          if (band_mask & (1u << m)) a.band[m][rowoff + j] = band_s[(m * kTile + li) * kTile + lj] * inv;
+          if (band_mask & (1u << m)) {
+            const float v = band_s[(m * kTile + li) * kTile + lj] * inv;
+            if (a.nbc > 1)
+              atomicAdd(&a.band[m][rowoff + j], v);  // bins split over CTAs: band zeroed by the host
+            else
+              a.band[m][rowoff + j] = v;
+          }
       }
     }
   }
@@ -237,7 +247,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, cudaStream_t st) {
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -261,6 +271,8 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   }
   Lag1Args a{};
   a.N = N; a.N64 = N64; a.K = K; a.Kp = Kp; a.bin_lo = bin_lo; a.nbb = nbb;
+  a.nbc = nbc;
+  a.bpc = (nbb + nbc - 1) / nbc;
   a.psd = psd; a.mag = mag; a.real0 = real0; a.real1 = real1; a.nt = nt; a.row_begin = row_begin;
   a.pair_base = pair_base; a.pair_stride = pair_stride;
   for (int m = 0; m < 5; ++m) {
@@ -274,7 +286,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     cudaFuncSetAttribute(k_pairs_lag1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  k_pairs_lag1<<<(unsigned)n_tiles, k1Threads, smem, st>>>(mI, mJ, a);
+  k_pairs_lag1<<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
   return true;
 }
 

@@ -53,7 +53,8 @@ struct TcArgs {
   int N, K, K_pad, nbb;
   int i_lo, i_hi;            // row range [i_lo, i_hi) of pairs computed (shard)
   int tile_row0, n_tiles;    // first 128-row tile and number of tiles in the launch
-  const int2* tiles;         // (I, J) per CTA, L2-friendly grouped order
+  const int2* tiles;         // (I, J) per tile, L2-friendly grouped order
+  int bpc, nbc;              // bins per CTA and bin chunks per tile (small pair spaces split bins)
   int nt;                    // 64-node column tiles over N
   const float* psd;          // [nbb][N] plan-scaled sum_k |X|^2
   const float* nscale;       // [nbb][N] per-node-bin power of two used for the fp16 split
@@ -142,7 +143,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int2 tij = a.tiles[blockIdx.x];
+  const int2 tij = a.tiles[blockIdx.x / a.nbc];
+  const int bl0 = (blockIdx.x % a.nbc) * a.bpc;
+  const int bl1 = min(a.nbb, bl0 + a.bpc);
   const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
 
   if (threadIdx.x == 0) {
@@ -175,7 +178,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int bl = 0; bl < a.nbb; ++bl)
+      for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
           const int pass = pass0 + ps;
           for (int c = 0; c < n_chunk; ++c) {
@@ -202,7 +205,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tuse[2] = {0, 0};
-      for (int bl = 0; bl < a.nbb; ++bl)
+      for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
           const int reg = ps;
           mbar_wait(&tempty[reg], (tuse[reg] & 1) ^ 1);
@@ -246,7 +249,8 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     }
     const bool cohy = a.cohy_bins || a.cohy_band;
     uint32_t tuse[2] = {0, 0};
-    for (int bl = 0; bl < a.nbb; ++bl) {
+    for (int bl = bl0; bl < bl1; ++bl) {
+      const bool acc_band = bl != bl0;  // first bin of the chunk initialises the TMEM band sums
       const int64_t bo = (int64_t)bl * a.pair_stride;
       float pi = 0.f;
       if (a.do_x) {
@@ -295,9 +299,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
                 for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u].x = m[u];
               if (a.coh_band) {
                 float b[16];
-                if (bl) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
+                if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + m[u] * inv_nb;
+                for (int u = 0; u < 16; ++u) b[u] = (acc_band ? b[u] : 0.f) + m[u] * inv_nb;
                 tmem_st16(tmem + lane_addr + kTmBand + c0, b);
               }
             }
@@ -306,14 +310,14 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(vr[u], vi[u]);
               if (a.cohy_band) {
                 float br[16], bi[16];
-                if (bl) {
+                if (acc_band) {
                   tmem_ld16(tmem + lane_addr + kTmBand + 128 + c0, br);
                   tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
                 }
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                  br[u] = (bl ? br[u] : 0.f) + vr[u] * inv_nb;
-                  bi[u] = (bl ? bi[u] : 0.f) + vi[u] * inv_nb;
+                  br[u] = (acc_band ? br[u] : 0.f) + vr[u] * inv_nb;
+                  bi[u] = (acc_band ? bi[u] : 0.f) + vi[u] * inv_nb;
                 }
                 tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
                 tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
@@ -327,9 +331,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             }
             if (a.plv_band) {
               float b[16];
-              if (bl) tmem_ld16(tmem + lane_addr + kTmBand + 64 + c0, b);
+              if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 64 + c0, b);
 #pragma unroll
-              for (int u = 0; u < 16; ++u) b[u] = (bl ? b[u] : 0.f) + vr[u] * inv_nb;
+              for (int u = 0; u < 16; ++u) b[u] = (acc_band ? b[u] : 0.f) + vr[u] * inv_nb;
               tmem_st16(tmem + lane_addr + kTmBand + 64 + c0, b);
             }
           }
@@ -387,9 +391,20 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             const int c = lane + 32 * hh, j = jBase + c;
             if (j <= ii || j >= a.N) continue;
             const float2 v = xbuf[row * kTcXStride + c];
-            if (kind == 2) a.cohy_band[ro + j] = v;
-            else if (kind == 0) a.coh_band[ro + j] = v.x;
-            else a.plv_band[ro + j] = v.x;
+            if (a.nbc > 1) {  // bins split over CTAs: the host zeroed the band outputs
+              if (kind == 2) {
+                atomicAdd(&a.cohy_band[ro + j].x, v.x);
+                atomicAdd(&a.cohy_band[ro + j].y, v.y);
+              } else {
+                atomicAdd(kind == 0 ? &a.coh_band[ro + j] : &a.plv_band[ro + j], v.x);
+              }
+            } else if (kind == 2) {
+              a.cohy_band[ro + j] = v;
+            } else if (kind == 0) {
+              a.coh_band[ro + j] = v.x;
+            } else {
+              a.plv_band[ro + j] = v.x;
+            }
           }
         }
         epi_bar();
@@ -516,6 +531,12 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   }
   const int64_t n_tiles = p.tc_ntiles;
   a.tiles = (const int2*)p.tc_tiles;
+  {  // small pair spaces: split bins over CTAs for >= ~2 waves
+    int nbc = n_tiles > 0 ? (int)((2 * 148 + n_tiles - 1) / n_tiles) : 1;
+    nbc = nbc < 1 ? 1 : (nbc > nbb ? nbb : nbc);
+    a.bpc = (nbb + nbc - 1) / nbc;
+    a.nbc = (nbb + a.bpc - 1) / a.bpc;
+  }
   a.psd = p.psd; a.nscale = nscale;
   a.invK = 1.f / (float)K;
   a.pair_base = out->pair_base; a.pair_stride = out->pair_stride;
@@ -534,7 +555,12 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   }
   {
     PhaseMark ph(p, "pairs_tc", st);
-    if (n_tiles > 0) k_pairs_tc<<<(unsigned)n_tiles, kTcThreads, smem, st>>>(mapA, mapB, a);
+    if (a.nbc > 1) {
+      if (a.coh_band) cudaMemsetAsync(a.coh_band, 0, a.pair_stride * sizeof(float), st);
+      if (a.plv_band) cudaMemsetAsync(a.plv_band, 0, a.pair_stride * sizeof(float), st);
+      if (a.cohy_band) cudaMemsetAsync(a.cohy_band, 0, a.pair_stride * sizeof(float2), st);
+    }
+    if (n_tiles > 0) k_pairs_tc<<<(unsigned)(n_tiles * a.nbc), kTcThreads, smem, st>>>(mapA, mapB, a);
   }
   return true;
 }
