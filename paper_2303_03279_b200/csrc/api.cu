@@ -295,8 +295,10 @@ int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_
     cs::PhaseMark ph(*p, "node_stats", st);
     cs::run_node_stats(*p, slots, K, bin_lo, nbb, st);
   }
-  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
+  // the tensor-core family runs first: with COH requested it also produces IMAGCOHY,
+  // whose per-bin values the phase-lag kernel reads back for WPLI
   if (cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
+  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_metrics");
   return CS_OK;
 }

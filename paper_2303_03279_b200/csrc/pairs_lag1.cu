@@ -38,12 +38,14 @@ struct Lag1Args {
   int64_t pair_base, pair_stride;
   float* bins[5];
   float* band[5];
+  const float* ext_imag;     // IMAGCOHY per-bin from the tensor-core kernel (sum Im = IMAG * sqrt(psd psd)), or null
   float g;
   int4* flags;
   int* counters;
   int flag_cap;
 };
 
+template <bool EXT_IM>
 __global__ void __launch_bounds__(k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -124,6 +126,20 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
     const int nkp = min(kc, a.Kp - st * kc);
+    float ximag[k1NP];  // EXT_IM: prefetch this bin's IMAGCOHY before its last stage computes
+    if (EXT_IM && st + 1 == n_stage) {
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) {
+        const int i = iBase + ty + k1TY * r;
+        const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base +
+                               (int64_t)bl * a.pair_stride;
+#pragma unroll
+        for (int c = 0; c < k1TC; ++c) {
+          const int j = jBase + tx + k1TX * c;
+          ximag[r * k1TC + c] = (i < j && j < a.N) ? __ldcs(a.ext_imag + rowoff + j) : 0.f;
+        }
+      }
+    }
     auto body = [&](int kp) {
       float4 xi[k1TR], xj[k1TC];
 #pragma unroll
@@ -138,7 +154,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           const int p = r * k1TC + c;
           const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
           const f2 tt = ffma2(ii, jr, fmul2(ir, jn));
-          sim[p] = fadd2(sim[p], tt);
+          if (!EXT_IM) sim[p] = fadd2(sim[p], tt);  // EXT_IM: sum Im comes from the tensor cores
           const float tl = lo_of(tt), th = hi_of(tt);
           sabs[p] += fabsf(tl);
           sabs[p] += fabsf(th);
@@ -181,7 +197,12 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const int lj = tx + k1TX * c, j = jBase + lj;
         const bool valid = (i < j) && (j < a.N);
         const bool dead = real_bin || Mi[r] == 0.f || Mj[c] == 0.f;
-        const bool flagged = valid && !dead && (mn[p] <= a.g * Mi[r] * Mj[c]);
+        const float pp = Pi[r] * Pj[c];
+        const int64_t po = rowoff + j;
+        // EXT_IM: |sum Im| carries the tensor-core error (~3e-7 sqrt(psd psd)); WPLI
+        // stays within 3e-4 unless sum |Im| < 1e-3 sqrt(psd psd) -> those go to fp64
+        const bool weak = EXT_IM && sabs[p] < 1e-3f * sqrtf(pp);
+        const bool flagged = valid && !dead && (mn[p] <= a.g * Mi[r] * Mj[c] || weak);
         if (flagged) {  // rare: the fp64 fallback writes this (pair, bin)
           const int slot = atomicAdd(&a.counters[0], 1);
           if (slot < a.flag_cap)
@@ -190,10 +211,13 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
             a.counters[1] = 1;
         }
         const float tph = odd ? (Mi[r] * k1Phantom) * (Mj[c] * k1Phantom) : 0.f;
-        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+        float s_im;
+        if (EXT_IM)
+          s_im = (dead || !valid) ? 0.f : ximag[p] * sqrtf(pp);
+        else
+          s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
         const float s_abs = dead ? 0.f : sabs[p] - tph;
         const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
-        const float pp = Pi[r] * Pj[c];
         float v[5];
         v[0] = pp > 0.f ? s_im * rsqrtf(pp) : 0.f;
         const float pli = fabsf((float)pli_sum) * invK;
@@ -203,7 +227,6 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         v[3] = w;
         v[4] = w * w;
         if (valid && !flagged) {
-          const int64_t po = rowoff + j;
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
@@ -247,7 +270,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, cudaStream_t st) {
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, const float* ext_imag,
+                 cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -280,13 +304,18 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     a.band[m] = band[m];
   }
   a.g = g; a.flags = flags; a.counters = counters; a.flag_cap = flag_cap;
+  a.ext_imag = ext_imag;
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 5 * kTile * kTile * 4 + 2 * k1Stages * 8;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_pairs_lag1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_pairs_lag1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_pairs_lag1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  k_pairs_lag1<<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
+  if (ext_imag)
+    k_pairs_lag1<true><<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
+  else
+    k_pairs_lag1<false><<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
   return true;
 }
 

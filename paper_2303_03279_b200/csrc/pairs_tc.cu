@@ -63,6 +63,7 @@ struct TcArgs {
   float* coh_bins;  float* coh_band;
   float2* cohy_bins; float2* cohy_band;
   float* plv_bins;  float* plv_band;
+  float* imag_bins; float* imag_band;   // IMAGCOHY from D_im (the phase-lag kernel then reads it for WPLI)
   int do_x, do_u;
 };
 
@@ -296,7 +297,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               for (int u = 0; u < 16; ++u) m[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]);
               if (!cohy)
 #pragma unroll
-                for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u].x = m[u];
+                for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(m[u], vi[u]);
               if (a.coh_band) {
                 float b[16];
                 if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
@@ -304,6 +305,13 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
                 for (int u = 0; u < 16; ++u) b[u] = (acc_band ? b[u] : 0.f) + m[u] * inv_nb;
                 tmem_st16(tmem + lane_addr + kTmBand + c0, b);
               }
+            }
+            if (a.imag_band && !a.cohy_band) {  // IMAGCOHY band mean in the COHY-im columns
+              float bi[16];
+              if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+#pragma unroll
+              for (int u = 0; u < 16; ++u) bi[u] = (acc_band ? bi[u] : 0.f) + vi[u] * inv_nb;
+              tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
             }
             if (cohy) {
 #pragma unroll
@@ -358,6 +366,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             if (pass == 0) {
               if (cohy && a.cohy_bins) a.cohy_bins[bo + ro + j] = v;
               if (a.coh_bins) a.coh_bins[bo + ro + j] = cohy ? sqrtf(v.x * v.x + v.y * v.y) : v.x;
+              if (a.imag_bins) a.imag_bins[bo + ro + j] = v.y;
             } else if (a.plv_bins) {
               a.plv_bins[bo + ro + j] = v.x;
             }
@@ -367,15 +376,17 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       }
     }
     // band means: TMEM -> transpose buffer -> coalesced stores
-    if (a.coh_band || a.plv_band || a.cohy_band) {
+    if (a.coh_band || a.plv_band || a.cohy_band || a.imag_band) {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      for (int kind = 0; kind < 3; ++kind) {
-        if ((kind == 0 && !a.coh_band) || (kind == 1 && !a.plv_band) || (kind == 2 && !a.cohy_band)) continue;
+      for (int kind = 0; kind < 4; ++kind) {
+        if ((kind == 0 && !a.coh_band) || (kind == 1 && !a.plv_band) || (kind == 2 && !a.cohy_band) ||
+            (kind == 3 && (!a.imag_band || a.cohy_band)))
+          continue;
 #pragma unroll
         for (int c1 = 0; c1 < 32; c1 += 16) {
           const int c0 = cb + c1;
           float b0[16], b1[16];
-          tmem_ld16(tmem + lane_addr + kTmBand + (kind == 2 ? 128 : kind * 64) + c0, b0);
+          tmem_ld16(tmem + lane_addr + kTmBand + (kind >= 2 ? (kind == 3 ? 192 : 128) : kind * 64) + c0, b0);
           if (kind == 2) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, b1);
 #pragma unroll
           for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(b0[u], kind == 2 ? b1[u] : 0.f);
@@ -391,19 +402,22 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             const int c = lane + 32 * hh, j = jBase + c;
             if (j <= ii || j >= a.N) continue;
             const float2 v = xbuf[row * kTcXStride + c];
+            float* dst1 = kind == 0 ? a.coh_band : (kind == 1 ? a.plv_band : a.imag_band);
             if (a.nbc > 1) {  // bins split over CTAs: the host zeroed the band outputs
               if (kind == 2) {
                 atomicAdd(&a.cohy_band[ro + j].x, v.x);
                 atomicAdd(&a.cohy_band[ro + j].y, v.y);
               } else {
-                atomicAdd(kind == 0 ? &a.coh_band[ro + j] : &a.plv_band[ro + j], v.x);
+                atomicAdd(&dst1[ro + j], v.x);
               }
             } else if (kind == 2) {
               a.cohy_band[ro + j] = v;
-            } else if (kind == 0) {
-              a.coh_band[ro + j] = v.x;
             } else {
-              a.plv_band[ro + j] = v.x;
+              dst1[ro + j] = v.x;
+            }
+            if (kind == 2 && a.imag_band) {  // IMAGCOHY band = Im of the COHY band mean
+              if (a.nbc > 1) atomicAdd(&a.imag_band[ro + j], v.y);
+              else a.imag_band[ro + j] = v.y;
             }
           }
         }
@@ -459,7 +473,7 @@ size_t tc_smem_bytes() {
 }
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
-                  const cs_outputs* out, const float* nscale, cudaStream_t st) {
+                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -546,6 +560,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.coh_band = do_x ? (float*)out->band[1] : nullptr;
   a.plv_bins = do_u ? (float*)out->bins[3] : nullptr;
   a.plv_band = do_u ? (float*)out->band[3] : nullptr;
+  a.imag_bins = do_imag ? (float*)out->bins[2] : nullptr;
+  a.imag_band = do_imag ? (float*)out->band[2] : nullptr;
   a.do_x = do_x; a.do_u = do_u;
   const size_t smem = tc_smem_bytes();
   static bool configured = false;
@@ -559,6 +575,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
       if (a.coh_band) cudaMemsetAsync(a.coh_band, 0, a.pair_stride * sizeof(float), st);
       if (a.plv_band) cudaMemsetAsync(a.plv_band, 0, a.pair_stride * sizeof(float), st);
       if (a.cohy_band) cudaMemsetAsync(a.cohy_band, 0, a.pair_stride * sizeof(float2), st);
+      if (a.imag_band) cudaMemsetAsync(a.imag_band, 0, a.pair_stride * sizeof(float), st);
     }
     if (n_tiles > 0) k_pairs_tc<<<(unsigned)(n_tiles * a.nbc), kTcThreads, smem, st>>>(mapA, mapB, a);
   }
