@@ -1,6 +1,7 @@
 // C ABI of csconn (include/csconn.h): plan lifetime, argument validation with
 // the reference's error classes (core.py:17-22), kernel orchestration.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -207,6 +208,15 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
       }
       ws[(size_t)l * p->nb + b] = make_double2((double)sr, (double)si);
     }
+  // FFT path: power-of-two nfft and a band for which ~5 M log2 M flops beat 4 T_eff nb
+  {
+    const bool pow2 = nfft >= 8 && (nfft & (nfft - 1)) == 0;
+    const int M = nfft / 2;
+    int lg = 0;
+    while ((1 << lg) < M) ++lg;
+    const char* force = getenv("CSCONN_SPECTRA");
+    p->use_fft = pow2 && (force ? force[0] == 'f' : (5.0 * M * lg + 16.0 * M < 4.0 * p->T_eff * p->nb));
+  }
   const int64_t P = (int64_t)N * (N - 1) / 2;
   int64_t cap = P * p->nb / 64;
   if (cap < (1 << 16)) cap = 1 << 16;
@@ -230,6 +240,32 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   }
   cudaMemcpy(p->tww, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
   cudaMemcpy(p->wsum, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (p->use_fft) {
+    const int M = nfft / 2;
+    std::vector<double2> ft(M / 2 > 0 ? M / 2 : 1), pt(M + 1);
+    for (int j = 0; j < M / 2; ++j) {
+      double c, s;
+      twiddle(j, M, &c, &s);
+      ft[j] = make_double2(c, s);
+    }
+    for (int k = 0; k <= M; ++k) {
+      double c, s;
+      twiddle(k, nfft, &c, &s);
+      pt[k] = make_double2(c, s);
+    }
+    bool ok2 = cudaMalloc(&p->fft_tw, ft.size() * sizeof(double2)) == cudaSuccess &&
+               cudaMalloc(&p->post_tw, pt.size() * sizeof(double2)) == cudaSuccess;
+    if (tapers) ok2 = ok2 && cudaMalloc(&p->taper, (size_t)L * p->T_eff * sizeof(double)) == cudaSuccess;
+    if (!ok2) {
+      cudaGetLastError();
+      cs_set_error("device allocation failed (FFT tables)");
+      cs_plan_destroy(p);
+      return CS_ENOMEM;
+    }
+    cudaMemcpy(p->fft_tw, ft.data(), ft.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(p->post_tw, pt.data(), pt.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    if (tapers) cudaMemcpy(p->taper, tapers, (size_t)L * p->T_eff * sizeof(double), cudaMemcpyHostToDevice);
+  }
   cudaMemset(p->X64, 0, ring * sizeof(double2));
   cudaMemset(p->X32, 0, ring * sizeof(float2));
   cudaMemset(p->counters, 0, 4 * sizeof(int));
@@ -244,7 +280,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
 int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   DeviceGuard g(p->device);
-  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
+  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
   if (p->tc_ops) cudaFree(p->tc_ops);
   if (p->tc_tiles) cudaFree(p->tc_tiles);
   if (p->lag_ops) cudaFree(p->lag_ops);

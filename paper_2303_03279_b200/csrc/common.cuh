@@ -22,6 +22,10 @@ struct Plan {
   int dc_local = -1, nyq_local = -1;  // plan-local indices of exactly-real bins
   double2* tww = nullptr;        // [L][nb][T_eff]   taper x twiddle
   double2* wsum = nullptr;       // [L][nb]          sum_t tww (mean correction)
+  double* taper = nullptr;       // [L][T_eff] tapers (null: rectangular)        -- FFT path
+  double2* fft_tw = nullptr;     // [nfft/4] e^{-2 pi i j / (nfft/2)}             -- FFT path
+  double2* post_tw = nullptr;    // [nfft/2 + 1] e^{-2 pi i k / nfft}            -- FFT path
+  bool use_fft = false;          // power-of-two nfft and a band wide enough to prefer the FFT
   double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
   float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra
   float* psd = nullptr;          // [nb][N] per-call node statistics

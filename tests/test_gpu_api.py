@@ -292,3 +292,23 @@ def test_reference_threshold_fixture(metric):
     want = g["band_" + metric]
     assert np.abs(net.weights - want).max() <= 1e-4
     assert np.abs(net.weights / np.abs(net.weights).max() - want / np.abs(want).max()).max() <= 1e-4
+
+
+@pytest.mark.parametrize("nfft,T,lo,hi,taper", [(64, 64, 0, 32, None), (128, 100, 3, 60, "hann"),
+                                                (512, 500, 0, 256, "hann"), (1024, 1000, 8, 13, "hann"),
+                                                (256, 300, 5, 20, ("dpss", 2.0, 3))])
+def test_fft_and_dft_spectra_agree(monkeypatch, nfft, T, lo, hi, taper):
+    """Both K1 variants (direct DFT and real FFT) against the oracle's rfft spectra."""
+    from paper_2303_03279_b200.plan import DevicePlan, make_taper
+    rng = np.random.default_rng(nfft + T)
+    x = rng.standard_normal((3, 5, T)) + 7.0
+    tap = make_taper(taper, min(T, nfft))
+    want = np.stack([np.stack([O.trial_spectra(e, nfft, None if tap is None else tp)[:, lo:hi + 1]
+                               for tp in ([None] if tap is None else tap)]) for e in x])  # [K, L, C, nb]
+    for mode in ("fft", "dft"):
+        monkeypatch.setenv("CSCONN_SPECTRA", mode)
+        plan = DevicePlan(5, T, nfft, lo, hi, taper=taper, slot_capacity=3, device="cuda")
+        plan.spectra(torch.tensor(x, device="cuda"), 0)
+        got = plan.ring()[0].cpu().numpy()                 # [S, L, nb, N]
+        got = np.transpose(got, (0, 1, 3, 2))               # [K, L, C, nb]
+        np.testing.assert_allclose(got, want, atol=1e-9 * np.abs(want).max(), err_msg=mode)
