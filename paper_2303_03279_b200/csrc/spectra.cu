@@ -388,66 +388,72 @@ k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stri
               const double2* __restrict__ post_tw, int slot0, int slot_cap, double2* __restrict__ X64,
               float2* __restrict__ X32, float scale, int dc_local, int nyq_local) {
   extern __shared__ double2 fft_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = blockIdx.x * kFftWarps + warp;
-  const int k = blockIdx.y / L, l = blockIdx.y % L;
   const int M = nfft >> 1;
-  double2* z = fft_smem + warp * M;
+  double2* stw = fft_smem;                                  // [M/2] twiddles, shared by the CTA
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < (M >> 1); j += blockDim.x) stw[j] = tw[j];
+  __syncthreads();
+  const int n = blockIdx.x * kFftWarps + warp;
+  const int k = blockIdx.y;
+  double2* z = fft_smem + (M >> 1) + warp * M;
   if (n >= N) return;  // warp-uniform
   const Tin* xr = x + (int64_t)k * trial_stride + (int64_t)n * node_stride;
-  const double* w = taper ? taper + (int64_t)l * T_eff : nullptr;
 
-  // mean of the real samples, shifted by the first sample (fp64)
+  // mean of the real samples, shifted by the first sample (fp64); samples stay in L1 for the taper loop
   const double c = (double)xr[0];
   double s = 0.0;
   for (int t = lane; t < T_eff; t += 32) s += (double)xr[t] - c;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const double mean = s / (double)T_eff;
+  const double mu = c + s / (double)T_eff;
+  const int slot = (slot0 + k) % slot_cap;
 
-  // z_q = v_2q + i v_2q+1 (v = (x - mu) * taper, zero padded), stored at bitrev(q)
-  for (int q = lane; q < M; q += 32) {
-    const int t0 = 2 * q, t1 = 2 * q + 1;
-    double a = 0.0, b = 0.0;
-    if (t0 < T_eff) a = ((double)xr[t0] - c - mean) * (w ? w[t0] : 1.0);
-    if (t1 < T_eff) b = ((double)xr[t1] - c - mean) * (w ? w[t1] : 1.0);
-    z[__brev(q) >> (32 - log2M)] = make_double2(a, b);
-  }
-  __syncwarp();
-  // iterative radix-2 DIT
-  for (int sgn = 0; sgn < log2M; ++sgn) {
-    const int half = 1 << sgn;
-    const int tstride = M >> (sgn + 1);  // twiddle index stride into tw[j] = e^{-2 pi i j / M}
-    for (int bq = lane; bq < (M >> 1); bq += 32) {
-      const int pos = bq & (half - 1);
-      const int i0 = ((bq >> sgn) << (sgn + 1)) + pos;
-      const int i1 = i0 + half;
-      const double2 wv = tw[pos * tstride];
-      const double2 u = z[i0], v0 = z[i1];
-      const double2 v = make_double2(v0.x * wv.x - v0.y * wv.y, v0.x * wv.y + v0.y * wv.x);
-      z[i0] = make_double2(u.x + v.x, u.y + v.y);
-      z[i1] = make_double2(u.x - v.x, u.y - v.y);
+  for (int l = 0; l < L; ++l) {  // all tapers of this signal in one warp: samples read once from HBM
+    const double* w = taper ? taper + (int64_t)l * T_eff : nullptr;
+    // z_q = v_2q + i v_2q+1 (v = (x - mu) * taper, zero padded), stored at bitrev(q)
+    for (int q = lane; q < M; q += 32) {
+      const int t0 = 2 * q, t1 = 2 * q + 1;
+      double a = 0.0, b = 0.0;
+      if (t0 < T_eff) a = ((double)xr[t0] - mu) * (w ? w[t0] : 1.0);
+      if (t1 < T_eff) b = ((double)xr[t1] - mu) * (w ? w[t1] : 1.0);
+      z[__brev(q) >> (32 - log2M)] = make_double2(a, b);
     }
     __syncwarp();
-  }
-  // real-FFT split for the plan bins
-  const int slot = (slot0 + k) % slot_cap;
-  for (int b = lane; b < nb; b += 32) {
-    const int kk = lo + b;
-    const double2 zk = z[kk == M ? 0 : kk];
-    const double2 zm = z[(M - kk) & (M - 1)];  // Z_{M-k}, with Z_M = Z_0
-    const double er = 0.5 * (zk.x + zm.x), ei = 0.5 * (zk.y - zm.y);   // E_k = (Z_k + conj Z_{M-k}) / 2
-    const double dr = 0.5 * (zk.x - zm.x), di = 0.5 * (zk.y + zm.y);   // D = (Z_k - conj Z_{M-k}) / 2
-    const double2 wk = post_tw[kk];                                    // e^{-2 pi i k / nfft}
-    // O_k = -i D ;  X_k = E_k + W^k O_k
-    const double orr = di, oi = -dr;
-    double re = er + (wk.x * orr - wk.y * oi);
-    double im = ei + (wk.x * oi + wk.y * orr);
-    if (b == dc_local) re = im = 0.0;
-    if (b == nyq_local) im = 0.0;
-    const int64_t o = (((int64_t)slot * L + l) * (int64_t)(nb) + b) * N + n;
-    X64[o] = make_double2(re, im);
-    X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+    // iterative radix-2 DIT; twiddles from shared memory
+    for (int sgn = 0; sgn < log2M; ++sgn) {
+      const int half = 1 << sgn;
+      const int tstride = M >> (sgn + 1);
+#pragma unroll 4
+      for (int bq = lane; bq < (M >> 1); bq += 32) {
+        const int pos = bq & (half - 1);
+        const int i0 = ((bq >> sgn) << (sgn + 1)) + pos;
+        const int i1 = i0 + half;
+        const double2 wv = stw[pos * tstride];
+        const double2 u = z[i0], v0 = z[i1];
+        const double2 v = make_double2(fma(v0.x, wv.x, -v0.y * wv.y), fma(v0.x, wv.y, v0.y * wv.x));
+        z[i0] = make_double2(u.x + v.x, u.y + v.y);
+        z[i1] = make_double2(u.x - v.x, u.y - v.y);
+      }
+      __syncwarp();
+    }
+    // real-FFT split for the plan bins
+    for (int b = lane; b < nb; b += 32) {
+      const int kk = lo + b;
+      const double2 zk = z[kk == M ? 0 : kk];
+      const double2 zm = z[(M - kk) & (M - 1)];  // Z_{M-k}, with Z_M = Z_0
+      const double er = 0.5 * (zk.x + zm.x), ei = 0.5 * (zk.y - zm.y);   // E_k = (Z_k + conj Z_{M-k}) / 2
+      const double dr = 0.5 * (zk.x - zm.x), di = 0.5 * (zk.y + zm.y);   // D = (Z_k - conj Z_{M-k}) / 2
+      const double2 wk = post_tw[kk];                                    // e^{-2 pi i k / nfft}
+      const double orr = di, oi = -dr;                                   // O_k = -i D
+      double re = er + (wk.x * orr - wk.y * oi);
+      double im = ei + (wk.x * oi + wk.y * orr);
+      if (b == dc_local) re = im = 0.0;
+      if (b == nyq_local) im = 0.0;
+      const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * N + n;
+      X64[o] = make_double2(re, im);
+      X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+    }
+    __syncwarp();
   }
 }
 
@@ -456,8 +462,8 @@ bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_
   const int M = p.nfft / 2;
   int log2M = 0;
   while ((1 << log2M) < M) ++log2M;
-  const size_t smem = (size_t)kFftWarps * M * sizeof(double2);
-  dim3 grid((p.N + kFftWarps - 1) / kFftWarps, kc * p.L);
+  const size_t smem = (size_t)(kFftWarps * M + M / 2) * sizeof(double2);
+  dim3 grid((p.N + kFftWarps - 1) / kFftWarps, kc);
   if (dtype == CS_F64) {
     static bool cfg = false;
     if (!cfg) { cudaFuncSetAttribute(k_spectra_fft<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
