@@ -87,282 +87,6 @@ __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict
   PkJ[o] = make_float4(va.x, wb.x, -va.y, wb.y);
 }
 
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-// CTA tile 64 x 64 nodes; thread micro-tile kTR rows x kTC cols (rows i = ty + 16 r,
-// cols j = tx + 32 c) so a warp shares one i row (broadcast loads) and writes 32
-// consecutive pairs of that row (coalesced 128 B stores).
-constexpr int kTR = 4, kTC = 2;
-constexpr int kTY = kTile / kTR, kTX = kTile / kTC;  // 16 x 32 = 512 threads
-constexpr int kLagThreads = kTY * kTX;
-constexpr int kNP = kTR * kTC;
-template <int L>
-struct LagShape {
-  static constexpr int KC = L == 1 ? kKC : kKC / L;  // trial pairs per stage
-  static constexpr int F4 = KC * L * kTile;           // float4 per side per stage
-};
-
-template <int L, bool PLVK>
-__global__ void __launch_bounds__(kLagThreads, 1) k_pairs_lag(const LagArgs a) {
-  constexpr int KC = LagShape<L>::KC;
-  constexpr int kStageF4 = LagShape<L>::F4;
-  constexpr int NM = PLVK ? 6 : 5;                     // band metrics kept in smem
-  extern __shared__ float4 smem4[];
-  float4* XI = smem4;                                  // [stages][KC][L][64]
-  float4* XJ = smem4 + kLagStages * kStageF4;          // [stages][KC][L][64]
-  float* band_s = (float*)(smem4 + 2 * kLagStages * kStageF4);  // [NM][64][64]
-
-  int I, J;
-  decode_tile(blockIdx.x, a.nt, a.row_begin, I, J);
-  const int tid = threadIdx.x, tx = tid % kTX, ty = tid / kTX;
-  const int iBase = I * kTile, jBase = J * kTile;
-
-  unsigned bin_mask = 0, band_mask = 0;
-#pragma unroll
-  for (int m = 0; m < 5; ++m) {
-    bin_mask |= (a.bins[m] != nullptr) << m;
-    band_mask |= (a.band[m] != nullptr) << m;
-  }
-  if (PLVK) {
-    bin_mask |= (a.plv_bins != nullptr) << 5;
-    band_mask |= (a.plv_band != nullptr) << 5;
-  }
-  if (band_mask)
-    for (int e = tid; e < NM * kTile * kTile; e += kLagThreads) band_s[e] = 0.f;
-
-  const int n_stage = (a.Kp + KC - 1) / KC;     // stages per bin
-  const int total = n_stage * a.nbb;            // flat (bin, stage) sequence
-  const bool odd = a.K & 1;
-  const float invK = 1.f / (float)a.K;
-  const float uspA = a.K > 1 ? (float)a.K / (float)(a.K - 1) : 0.f;
-  const float uspB = a.K > 1 ? 1.f / (float)(a.K - 1) : 0.f;
-
-  // cp.async staging of flat step t into buffer t % stages (2 float4 per side per thread)
-  auto issue = [&](int t) {
-    if (t < total) {
-      const int bl = t / n_stage, st = t % n_stage;
-      const int kp0 = st * KC;
-      float4* dI = XI + (t % kLagStages) * kStageF4;
-      float4* dJ = XJ + (t % kLagStages) * kStageF4;
-      for (int e = tid; e < kStageF4; e += kLagThreads) {
-        const int row = e >> 6, node = e & 63;          // row = kp * L + l
-        const int kp = row / L, l = row % L;
-        const int kpg = min(kp0 + kp, a.Kp - 1);  // clamp: rows past Kp are never read
-        const int64_t ob = (((int64_t)bl * a.Kp + kpg) * L + l) * a.N64;
-        cpa16(dI + e, a.PkI + ob + iBase + node);
-        cpa16(dJ + e, a.PkJ + ob + jBase + node);
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
-  f2 sim[kNP];
-  float sabs[kNP], mn[kNP];
-  int neg[kNP];
-  f2 pvr[PLVK ? kNP : 1], pvi[PLVK ? kNP : 1];
-  auto reset_acc = [&]() {
-#pragma unroll
-    for (int p = 0; p < kNP; ++p) {
-      sim[p] = 0ull;
-      sabs[p] = 0.f;
-      mn[p] = 3.0e38f;
-      neg[p] = 0;
-      if (PLVK) {
-        pvr[p] = 0ull;
-        pvi[p] = 0ull;
-      }
-    }
-  };
-  auto compute_kp = [&](const float4* sI, const float4* sJ, int kp) {
-    if (L == 1) {
-      float4 xi[kTR], xj[kTC];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r) xi[r] = sI[kp * kTile + ty + kTY * r];
-#pragma unroll
-      for (int c = 0; c < kTC; ++c) xj[c] = sJ[kp * kTile + tx + kTX * c];
-#pragma unroll
-      for (int r = 0; r < kTR; ++r) {
-        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
-#pragma unroll
-        for (int c = 0; c < kTC; ++c) {
-          const int p = r * kTC + c;
-          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-          const f2 t = ffma2(ii, jr, fmul2(ir, jn));   // Im(X_i conj X_j) for trials a, b
-          sim[p] = fadd2(sim[p], t);
-          const float tl = lo_of(t), th = hi_of(t);
-          sabs[p] += fabsf(tl);
-          sabs[p] += fabsf(th);
-          neg[p] += (int)(__float_as_uint(tl) >> 31);
-          neg[p] += (int)(__float_as_uint(th) >> 31);
-          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
-        }
-      }
-    } else {
-      // taper sum inside each trial: t = sum_l Im(X_il conj X_jl) (spectral.py:272-283
-      // precedent: the nonlinear terms act on the taper-mean CSD; 1/L cancels)
-      f2 t[kNP], re1[PLVK ? kNP : 1], re2[PLVK ? kNP : 1];
-#pragma unroll
-      for (int p = 0; p < kNP; ++p) {
-        t[p] = 0ull;
-        if (PLVK) re1[p] = re2[p] = 0ull;
-      }
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        float4 xi[kTR], xj[kTC];
-#pragma unroll
-        for (int r = 0; r < kTR; ++r) xi[r] = sI[(kp * L + l) * kTile + ty + kTY * r];
-#pragma unroll
-        for (int c = 0; c < kTC; ++c) xj[c] = sJ[(kp * L + l) * kTile + tx + kTX * c];
-#pragma unroll
-        for (int r = 0; r < kTR; ++r) {
-          const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
-#pragma unroll
-          for (int c = 0; c < kTC; ++c) {
-            const int p = r * kTC + c;
-            const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-            t[p] = ffma2(ii, jr, ffma2(ir, jn, t[p]));
-            if (PLVK) {  // Re = sum ir jr + ii ji = re1 - re2 with re2 = sum ii (-ji)
-              re1[p] = ffma2(ir, jr, re1[p]);
-              re2[p] = ffma2(ii, jn, re2[p]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int p = 0; p < kNP; ++p) {
-        sim[p] = fadd2(sim[p], t[p]);
-        const float tl = lo_of(t[p]), th = hi_of(t[p]);
-        sabs[p] += fabsf(tl);
-        sabs[p] += fabsf(th);
-        neg[p] += (int)(__float_as_uint(tl) >> 31);
-        neg[p] += (int)(__float_as_uint(th) >> 31);
-        mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
-        if (PLVK) {
-          f2 re;
-          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(re) : "l"(re1[p]), "l"(re2[p]));
-          const f2 m2 = ffma2(t[p], t[p], fmul2(re, re));
-          const float ml = lo_of(m2), mh = hi_of(m2);
-          const f2 rs = pk(ml > 0.f ? rsqrtf(ml) : 0.f, mh > 0.f ? rsqrtf(mh) : 0.f);
-          pvr[p] = ffma2(re, rs, pvr[p]);
-          pvi[p] = ffma2(t[p], rs, pvi[p]);
-        }
-      }
-    }
-  };
-
-#pragma unroll
-  for (int t = 0; t < kLagStages - 1; ++t) issue(t);
-  reset_acc();
-
-  for (int t = 0; t < total; ++t) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kLagStages - 2));
-    __syncthreads();                       // stage t visible; stage t-1 fully consumed
-    issue(t + kLagStages - 1);
-    const int bl = t / n_stage, st = t % n_stage;
-    const float4* sI = XI + (t % kLagStages) * kStageF4;
-    const float4* sJ = XJ + (t % kLagStages) * kStageF4;
-    const int nkp = min(KC, a.Kp - st * KC);
-    if (nkp == KC) {
-#pragma unroll 4
-      for (int kp = 0; kp < KC; ++kp) compute_kp(sI, sJ, kp);
-    } else {
-      for (int kp = 0; kp < nkp; ++kp) compute_kp(sI, sJ, kp);
-    }
-    if (st + 1 < n_stage) continue;
-
-    // ---- epilogue: finalize bin bl (fast-math intrinsics; fp32 outputs) ----
-    const int b = a.bin_lo + bl;
-    const bool real_bin = (b == a.real0) || (b == a.real1);
-    float Mi[kTR], Mj[kTC], Pi[kTR], Pj[kTC];
-#pragma unroll
-    for (int r = 0; r < kTR; ++r) {
-      const int i = iBase + ty + kTY * r;
-      Mi[r] = i < a.N ? a.mag[(int64_t)bl * a.N + i] : 0.f;
-      Pi[r] = i < a.N ? a.psd[(int64_t)bl * a.N + i] : 0.f;
-    }
-#pragma unroll
-    for (int c = 0; c < kTC; ++c) {
-      const int j = jBase + tx + kTX * c;
-      Mj[c] = j < a.N ? a.mag[(int64_t)bl * a.N + j] : 0.f;
-      Pj[c] = j < a.N ? a.psd[(int64_t)bl * a.N + j] : 0.f;
-    }
-    const int64_t bin_off = (int64_t)bl * a.pair_stride;
-    float* obin[5];
-#pragma unroll
-    for (int m = 0; m < 5; ++m) obin[m] = (bin_mask & (1u << m)) ? a.bins[m] + bin_off : nullptr;
-    const float g = a.g;
-#pragma unroll
-    for (int r = 0; r < kTR; ++r)
-#pragma unroll
-      for (int c = 0; c < kTC; ++c) {
-        const int p = r * kTC + c;
-        const int li = ty + kTY * r, lj = tx + kTX * c;
-        const int i = iBase + li, j = jBase + lj;
-        const bool valid = (i < j) && (j < a.N);
-        const bool dead = real_bin || Mi[r] == 0.f || Mj[c] == 0.f;
-        const bool flagged = valid && !dead && (mn[p] <= g * Mi[r] * Mj[c]);
-        if (flagged) {  // rare: the fp64 fallback writes this (pair, bin)
-          const int slot = atomicAdd(&a.counters[0], 1);
-          if (slot < a.flag_cap)
-            a.flags[slot] = make_int4(i, j, bl, 0);
-          else
-            a.counters[1] = 1;
-        }
-        const float tph = odd ? (Mi[r] * kPhantom) * (Mj[c] * kPhantom) : 0.f;
-        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
-        const float s_abs = dead ? 0.f : sabs[p] - tph;
-        const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
-        const float pp = Pi[r] * Pj[c];
-        float v[5];
-        v[0] = pp > 0.f ? s_im * rsqrtf(pp) : 0.f;                   // IMAGCOHY
-        const float pli = fabsf((float)pli_sum) * invK;              // PLI
-        v[1] = pli;
-        v[2] = pli * pli * uspA - uspB;                              // USPLI
-        const float w = s_abs > 0.f ? __fdividef(fabsf(s_im), s_abs) : 0.f;  // WPLI, 0/0 -> 0
-        v[3] = fminf(w, 1.f);
-        v[4] = v[3] * v[3];                                          // DSWPLI
-        if (PLVK && valid) {  // PLV is continuous: written even for guard-flagged entries
-          // the odd-K phantom contributed the unit phasor (0, 1) to the PLV sums
-          const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
-          const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
-          const float plv = dead ? 0.f : sqrtf(pr * pr + pim * pim) * invK;
-          const int64_t po = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + j;
-          if (bin_mask & 32u) a.plv_bins[bin_off + po] = plv;
-          if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
-        }
-        if (valid && !flagged) {
-          const int64_t po = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + j;
-          float* bs = band_s + li * kTile + lj;
-#pragma unroll
-          for (int m = 0; m < 5; ++m) {
-            if (bin_mask & (1u << m)) obin[m][po] = v[m];
-            if (band_mask & (1u << m)) bs[m * kTile * kTile] += v[m];
-          }
-        }
-      }
-    reset_acc();
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-
-  if (band_mask) {
-    __syncthreads();
-    const float inv = 1.f / (float)a.nbb;
-    for (int e = tid; e < kTile * kTile; e += kLagThreads) {
-      const int li = e >> 6, lj = e & 63;
-      const int i = iBase + li, j = jBase + lj;
-      if (!(i < j && j < a.N)) continue;
-      const int64_t po = pair_of(i, j, a.N) - a.pair_base;
-#pragma unroll
-      for (int m = 0; m < 5; ++m)
-        if (band_mask & (1u << m)) a.band[m][po] = band_s[(m * kTile + li) * kTile + lj] * inv;
-      if (PLVK && (band_mask & 32u)) a.plv_band[po] = band_s[(5 * kTile + li) * kTile + lj] * inv;
-    }
-  }
-}
-
 // fp64 recomputation of flagged (pair, bin) entries: one warp per entry, lanes
 // over trials; reference arithmetic of spectral.py:204-241 in complex128.
 __global__ void k_lag_fallback(const LagArgs a) {
@@ -426,27 +150,11 @@ __global__ void k_lag_fallback(const LagArgs a) {
   }
 }
 
-template <int L, bool PLVK>
-static size_t lag_smem_bytes() {
-  return (size_t)2 * kLagStages * LagShape<L>::F4 * sizeof(float4) + (PLVK ? 6 : 5) * kTile * kTile * sizeof(float);
-}
-
-template <int L, bool PLVK>
-static void launch_lag(const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
-  const size_t smem = lag_smem_bytes<L, PLVK>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_pairs_lag<L, PLVK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  k_pairs_lag<L, PLVK><<<(unsigned)n_tiles, kLagThreads, smem, st>>>(a);
-}
-
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, const float* ext_imag,
-                 cudaStream_t st);
+                 int L, float* plv_bins, float* plv_band, cudaStream_t st);
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
@@ -458,23 +166,19 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
   }
   {
     PhaseMark ph(p, "pairs_lag", st);
-    const bool plvk = a.plv_bins || a.plv_band;
-    if (a.L == 1) {
-      // small pair spaces (few tiles, many bins): split the bins over CTAs for >= 2 waves
-      int nbc = (int)((2 * 148 + n_tiles - 1) / n_tiles);
-      nbc = nbc < 1 ? 1 : (nbc > a.nbb ? a.nbb : nbc);
-      nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);  // no empty chunks
-      if (nbc > 1)
-        for (int m = 0; m < 5; ++m)
-          if (a.band[m]) cudaMemsetAsync(a.band[m], 0, a.pair_stride * sizeof(float), st);
-      if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
-                       a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters,
-                       a.flag_cap, n_tiles, nbc, a.ext_imag, st))
-        return false;
+    // small pair spaces (few tiles, many bins): split the bins over CTAs for >= 2 waves
+    int nbc = (int)((2 * 148 + n_tiles - 1) / n_tiles);
+    nbc = nbc < 1 ? 1 : (nbc > a.nbb ? a.nbb : nbc);
+    nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);  // no empty chunks
+    if (nbc > 1) {
+      for (int m = 0; m < 5; ++m)
+        if (a.band[m]) cudaMemsetAsync(a.band[m], 0, a.pair_stride * sizeof(float), st);
+      if (a.plv_band) cudaMemsetAsync(a.plv_band, 0, a.pair_stride * sizeof(float), st);
     }
-    else if (a.L == 2) plvk ? launch_lag<2, true>(a, n_tiles, st) : launch_lag<2, false>(a, n_tiles, st);
-    else if (a.L == 3) plvk ? launch_lag<3, true>(a, n_tiles, st) : launch_lag<3, false>(a, n_tiles, st);
-    else plvk ? launch_lag<4, true>(a, n_tiles, st) : launch_lag<4, false>(a, n_tiles, st);
+    if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
+                     a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters, a.flag_cap,
+                     n_tiles, nbc, a.ext_imag, a.L, a.plv_bins, a.plv_band, st))
+      return false;
   }
   {
     PhaseMark ph(p, "lag_fallback", st);

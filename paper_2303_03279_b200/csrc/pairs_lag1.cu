@@ -5,9 +5,9 @@
 // metrics.py:49-86 (imagcohy / pli / uspli / wpli / dswpli), metrics.py:115-134
 // and core.py:208-215 (band mean).
 //
-// CTA = 64 x 64 node tile x all bins of the band.  16 compute warps (512
-// threads, 16 x 32, each thread 4 x 2 pairs: i = ty + 16 r, j = tx + 32 c) and 1
-// producer warp.  The packed trial-pair operands (k_lag_prep: float4 (re_a, re_b, im_a,
+// CTA = 64 x 64 node tile x all bins of the band.  16 warps (512 threads,
+// 16 x 32, each thread 4 x 2 pairs: i = ty + 16 r, j = tx + 32 c); lane 0 of warp
+// 0 issues the TMA loads.  The packed trial-pair operands (k_lag_prep: float4 (re_a, re_b, im_a,
 // im_b), J side with Im negated) are streamed by 2D TMA boxes of 64 nodes x KC
 // trial pairs into a 4-stage ring; consumers wait on the stage's full barrier and
 // release it with one arrive per warp, so stages never need a CTA-wide sync.
@@ -19,14 +19,15 @@
 
 namespace cs {
 
-constexpr int k1KC = 25;           // max trial pairs per stage (balanced per launch)
+constexpr int k1Rows = 25;         // max operand rows (trial pair x taper) per stage
 constexpr int k1Stages = 2;
 constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
 constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
 constexpr int k1NP = k1TR * k1TC;
 constexpr int k1Warps = k1TY * k1TX / 32;  // compute warps
-constexpr int k1Threads = (k1Warps + 1) * 32;
-constexpr int k1StageF4 = k1KC * kTile;   // float4 per side per stage
+constexpr int k1Threads = k1Warps * 32;        // multitaper: lane 0 of warp 0 also issues the TMA loads
+constexpr int k1ThreadsP = k1Threads + 32;     // single taper: plus a dedicated TMA producer warp
+constexpr int k1StageF4 = k1Rows * kTile;  // float4 per side per stage
 constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 
 struct Lag1Args {
@@ -38,6 +39,8 @@ struct Lag1Args {
   int64_t pair_base, pair_stride;
   float* bins[5];
   float* band[5];
+  float* plv_bins;           // multitaper: PLV of the taper-mean CSD (PLVK instantiation)
+  float* plv_band;
   const float* ext_imag;     // IMAGCOHY per-bin from the tensor-core kernel (sum Im = IMAG * sqrt(psd psd)), or null
   float g;
   int4* flags;
@@ -45,15 +48,21 @@ struct Lag1Args {
   int flag_cap;
 };
 
-template <bool EXT_IM>
-__global__ void __launch_bounds__(k1Threads, 1)
+// L == 1 uses a dedicated producer warp (17 warps: the per-SMSP register file
+// then allows 96 registers, enough for the single-taper loop); L > 1 needs 128
+// registers, so 16 warps with the TMA issued from warp 0 (measured: the dedicated
+// warp is 2.7 % faster for L == 1 on cfg5).
+template <int L, bool PLVK, bool EXT_IM>
+__global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
+  constexpr int KCL = k1Rows / L;  // max trial pairs per stage
+  constexpr int NM = PLVK ? 6 : 5;
   extern __shared__ __align__(128) unsigned char lag1_smem[];
   float4* XI = (float4*)lag1_smem;                       // [stages][KC][64]
   float4* XJ = XI + k1Stages * k1StageF4;                // [stages][KC][64]
-  float* band_s = (float*)(XJ + k1Stages * k1StageF4);   // [5][64][64]
-  uint64_t* full = (uint64_t*)(band_s + 5 * kTile * kTile);
+  float* band_s = (float*)(XJ + k1Stages * k1StageF4);   // [NM][64][64]
+  uint64_t* full = (uint64_t*)(band_s + 6 * kTile * kTile);
   uint64_t* empty = full + k1Stages;
 
   int I, J;
@@ -70,6 +79,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     bin_mask |= (a.bins[m] != nullptr) << m;
     band_mask |= (a.band[m] != nullptr) << m;
   }
+  if (PLVK) {
+    bin_mask |= (a.plv_bins != nullptr) << 5;
+    band_mask |= (a.plv_band != nullptr) << 5;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < k1Stages; ++s) {
       mbar_init(&full[s], 1);
@@ -78,27 +91,44 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (band_mask)
-    for (int e = threadIdx.x; e < 5 * kTile * kTile; e += k1Threads) band_s[e] = 0.f;
+    for (int e = threadIdx.x; e < NM * kTile * kTile; e += blockDim.x) band_s[e] = 0.f;
   __syncthreads();
 
-  const int n_stage = (a.Kp + k1KC - 1) / k1KC;
-  const int kc = (a.Kp + n_stage - 1) / n_stage;   // balanced stage size (<= k1KC)
+  const int n_stage = (a.Kp + KCL - 1) / KCL;
+  const int kc = (a.Kp + n_stage - 1) / n_stage;   // balanced stage size (<= KCL trial pairs)
   const int total = n_stage * nbl;
 
-  if (warp == k1Warps) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      for (int t = 0; t < total; ++t) {
-        const int s = t % k1Stages;
-        mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
-        const int bl = bl0 + t / n_stage, st = t % n_stage;
-        const int row = bl * a.Kp + st * kc;
-        mbar_expect_tx(&full[s], 2 * k1StageF4 * 16);
-        tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
-        tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
-      }
+  // TMA issue (warp 0, lane 0): stage t into slot t % stages once every warp has
+  // released that slot's previous use.  16 warps = 4 per SMSP keep 128 registers
+  // per thread available (a 17th producer warp would cap them at 96).
+  constexpr bool kDedicated = L == 1;
+  auto issue = [&](int t) {
+    if (!kDedicated && warp == 0 && lane == 0 && t < total) {
+      const int s = t % k1Stages;
+      mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
+      const int bl = bl0 + t / n_stage, st = t % n_stage;
+      const int row = (bl * a.Kp + st * kc) * L;
+      mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16);  // exactly the two TMA boxes
+      tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
+      tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
     }
-    return;
+  };
+  if (kDedicated) {
+    if (warp == k1Warps) {  // producer warp: the whole stage sequence
+      if (lane == 0)
+        for (int t = 0; t < total; ++t) {
+          const int s = t % k1Stages;
+          mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
+          const int bl = bl0 + t / n_stage, st = t % n_stage;
+          const int row = (bl * a.Kp + st * kc) * L;
+          mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16);
+          tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
+          tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
+        }
+      return;
+    }
+  } else {
+    for (int t = 0; t < k1Stages - 1; ++t) issue(t);
   }
 
   // ------------------------------------------------------------ compute warps
@@ -111,15 +141,18 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   f2 sim[k1NP];
   float sabs[k1NP], mn[k1NP];
   int neg[k1NP];
+  f2 pvr[PLVK ? k1NP : 1], pvi[PLVK ? k1NP : 1];
 #pragma unroll
   for (int p = 0; p < k1NP; ++p) {
     sim[p] = 0ull;
     sabs[p] = 0.f;
     mn[p] = 3.0e38f;
     neg[p] = 0;
+    if (PLVK) pvr[p] = pvi[p] = 0ull;
   }
 
   for (int t = 0; t < total; ++t) {
+    issue(t + k1Stages - 1);
     const int s = t % k1Stages;
     const int bl = bl0 + t / n_stage, st = t % n_stage;
     mbar_wait(&full[s], (t / k1Stages) & 1);
@@ -140,27 +173,68 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         }
       }
     }
+    auto stats = [&](int p, f2 tt) {
+      if (!EXT_IM) sim[p] = fadd2(sim[p], tt);  // EXT_IM: sum Im comes from the tensor cores
+      const float tl = lo_of(tt), th = hi_of(tt);
+      sabs[p] += fabsf(tl);
+      sabs[p] += fabsf(th);
+      neg[p] += (int)(__float_as_uint(tl) >> 31);
+      neg[p] += (int)(__float_as_uint(th) >> 31);
+      mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+    };
     auto body = [&](int kp) {
-      float4 xi[k1TR], xj[k1TC];
+      if (L == 1) {
+        float4 xi[k1TR], xj[k1TC];
 #pragma unroll
-      for (int r = 0; r < k1TR; ++r) xi[r] = sI[kp * kTile + ty + k1TY * r];
+        for (int r = 0; r < k1TR; ++r) xi[r] = sI[kp * kTile + ty + k1TY * r];
 #pragma unroll
-      for (int c = 0; c < k1TC; ++c) xj[c] = sJ[kp * kTile + tx + k1TX * c];
+        for (int c = 0; c < k1TC; ++c) xj[c] = sJ[kp * kTile + tx + k1TX * c];
 #pragma unroll
-      for (int r = 0; r < k1TR; ++r) {
-        const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
+        for (int r = 0; r < k1TR; ++r) {
+          const f2 ir = pk(xi[r].x, xi[r].y), ii = pk(xi[r].z, xi[r].w);
 #pragma unroll
-        for (int c = 0; c < k1TC; ++c) {
-          const int p = r * k1TC + c;
-          const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-          const f2 tt = ffma2(ii, jr, fmul2(ir, jn));
-          if (!EXT_IM) sim[p] = fadd2(sim[p], tt);  // EXT_IM: sum Im comes from the tensor cores
-          const float tl = lo_of(tt), th = hi_of(tt);
-          sabs[p] += fabsf(tl);
-          sabs[p] += fabsf(th);
-          neg[p] += (int)(__float_as_uint(tl) >> 31);
-          neg[p] += (int)(__float_as_uint(th) >> 31);
-          mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
+          for (int c = 0; c < k1TC; ++c) {
+            const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
+            stats(r * k1TC + c, ffma2(ii, jr, fmul2(ir, jn)));  // Im(X_i conj X_j), trials a, b
+          }
+        }
+      } else {
+        // multitaper: t = sum_l Im(X_il conj X_jl) (the 1/L of the taper mean cancels)
+        float4 xj[L][k1TC];
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+#pragma unroll
+          for (int c = 0; c < k1TC; ++c) xj[l][c] = sJ[(kp * L + l) * kTile + tx + k1TX * c];
+#pragma unroll
+        for (int r = 0; r < k1TR; ++r) {
+          float4 xi[L];
+#pragma unroll
+          for (int l = 0; l < L; ++l) xi[l] = sI[(kp * L + l) * kTile + ty + k1TY * r];
+#pragma unroll
+          for (int c = 0; c < k1TC; ++c) {
+            const int p = r * k1TC + c;
+            f2 tt = 0ull, re1 = 0ull, re2 = 0ull;
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+              const f2 ir = pk(xi[l].x, xi[l].y), ii = pk(xi[l].z, xi[l].w);
+              const f2 jr = pk(xj[l][c].x, xj[l][c].y), jn = pk(xj[l][c].z, xj[l][c].w);
+              tt = ffma2(ii, jr, ffma2(ir, jn, tt));
+              if (PLVK) {  // Re = sum ir jr + ii ji = re1 - re2 with re2 = sum ii (-ji)
+                re1 = ffma2(ir, jr, re1);
+                re2 = ffma2(ii, jn, re2);
+              }
+            }
+            stats(p, tt);
+            if (PLVK) {  // unit phasor of the trial's taper-mean CSD
+              f2 re;
+              asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(re) : "l"(re1), "l"(re2));
+              const f2 m2 = ffma2(tt, tt, fmul2(re, re));
+              const float ml = lo_of(m2), mh = hi_of(m2);
+              const f2 rs = pk(ml > 0.f ? rsqrtf(ml) : 0.f, mh > 0.f ? rsqrtf(mh) : 0.f);
+              pvr[p] = ffma2(re, rs, pvr[p]);
+              pvi[p] = ffma2(tt, rs, pvi[p]);
+            }
+          }
         }
       }
     };
@@ -226,6 +300,15 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const float w = s_abs > 0.f ? fminf(__fdividef(fabsf(s_im), s_abs), 1.f) : 0.f;
         v[3] = w;
         v[4] = w * w;
+        if (PLVK && valid) {  // PLV is continuous: written even for guard-flagged entries
+          // the odd-K phantom contributed the unit phasor (0, 1) to the PLV sums
+          const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
+          const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
+          const float plv = dead ? 0.f : sqrtf(pr * pr + pim * pim) * invK;
+          if (bin_mask & 32u) a.plv_bins[bin_off + po] = plv;
+          if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
+          pvr[p] = pvi[p] = 0ull;
+        }
         if (valid && !flagged) {
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
@@ -254,13 +337,14 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const int lj = tx + k1TX * c, j = jBase + lj;
         if (!(i < j && j < a.N)) continue;
 #pragma unroll
-        for (int m = 0; m < 5; ++m)
+        for (int m = 0; m < NM; ++m)
           if (band_mask & (1u << m)) {
+            float* dst = m < 5 ? a.band[m] : a.plv_band;
             const float v = band_s[(m * kTile + li) * kTile + lj] * inv;
             if (a.nbc > 1)
-              atomicAdd(&a.band[m][rowoff + j], v);  // bins split over CTAs: band zeroed by the host
+              atomicAdd(&dst[rowoff + j], v);  // bins split over CTAs: band zeroed by the host
             else
-              a.band[m][rowoff + j] = v;
+              dst[rowoff + j] = v;
           }
       }
     }
@@ -271,16 +355,16 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, const float* ext_imag,
-                 cudaStream_t st) {
+                 int L, float* plv_bins, float* plv_band, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
     return false;
   }
   CUtensorMap mI, mJ;
-  cuuint64_t dims[2] = {(cuuint64_t)N64 * 4, (cuuint64_t)nbb * Kp};
+  cuuint64_t dims[2] = {(cuuint64_t)N64 * 4, (cuuint64_t)nbb * Kp * L};
   cuuint64_t strides[1] = {(cuuint64_t)N64 * 16};
-  cuuint32_t box[2] = {(cuuint32_t)kTile * 4, (cuuint32_t)k1KC};
+  cuuint32_t box[2] = {(cuuint32_t)kTile * 4, (cuuint32_t)((k1Rows / L) * L)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mI, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)PkI, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -305,17 +389,34 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   }
   a.g = g; a.flags = flags; a.counters = counters; a.flag_cap = flag_cap;
   a.ext_imag = ext_imag;
-  const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 5 * kTile * kTile * 4 + 2 * k1Stages * 8;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_pairs_lag1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_pairs_lag1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+  a.plv_bins = plv_bins;
+  a.plv_band = plv_band;
+  const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
+  const unsigned grid = (unsigned)(n_tiles * nbc);
+  const bool plvk = plv_bins || plv_band;
+#define CS_LAG1(LL, PV, EX)                                                                              \
+  do {                                                                                                   \
+    static bool cfg = false;                                                                             \
+    if (!cfg) {                                                                                          \
+      cudaFuncSetAttribute(k_pairs_lag1<LL, PV, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cfg = true;                                                                                        \
+    }                                                                                                    \
+    k_pairs_lag1<LL, PV, EX><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
+  } while (0)
+  if (L == 1) {
+    if (ext_imag) CS_LAG1(1, false, true);
+    else CS_LAG1(1, false, false);
+  } else if (L == 2) {
+    if (plvk) CS_LAG1(2, true, false);
+    else CS_LAG1(2, false, false);
+  } else if (L == 3) {
+    if (plvk) CS_LAG1(3, true, false);
+    else CS_LAG1(3, false, false);
+  } else {
+    if (plvk) CS_LAG1(4, true, false);
+    else CS_LAG1(4, false, false);
   }
-  if (ext_imag)
-    k_pairs_lag1<true><<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
-  else
-    k_pairs_lag1<false><<<(unsigned)(n_tiles * nbc), k1Threads, smem, st>>>(mI, mJ, a);
+#undef CS_LAG1
   return true;
 }
 
