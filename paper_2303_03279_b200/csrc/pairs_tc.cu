@@ -49,6 +49,12 @@ constexpr int kTcEpiWarps = 8;
 // [256,512) band sums: COH, PLV, COHY re, COHY im (64 each)
 constexpr int kTmBand = 256;
 
+#ifdef CS_TC_ABLATION
+#define TC_ABL(bit) (a.dbg & (bit))
+#else
+#define TC_ABL(bit) 0
+#endif
+
 struct TcArgs {
   int N, K, K_pad, nbb;
   int i_lo, i_hi;            // row range [i_lo, i_hi) of pairs computed (shard)
@@ -65,6 +71,8 @@ struct TcArgs {
   float* plv_bins;  float* plv_band;
   float* imag_bins; float* imag_band;   // IMAGCOHY from D_im (the phase-lag kernel then reads it for WPLI)
   int do_x, do_u;
+  int dbg;   // ablation bits (builds with -DCS_TC_ABLATION only): 1 per-bin stores, 2 TMEM-phase
+             // math, 4 band phase, 8 MMAs, 16 TMA loads are skipped (timing experiments)
 };
 
 // 16 consecutive fp32 columns of this thread's TMEM lane
@@ -78,6 +86,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+// two 16-column loads under one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float* v, uint32_t tb, float* w) {
+  uint32_t r[16], s[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]), "=r"(s[7]),
+        "=r"(s[8]), "=r"(s[9]), "=r"(s[10]), "=r"(s[11]), "=r"(s[12]), "=r"(s[13]), "=r"(s[14]), "=r"(s[15])
+      : "r"(tb));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    v[q] = __uint_as_float(r[q]);
+    w[q] = __uint_as_float(s[q]);
+  }
 }
 
 // K-major operand tile [128 rows x 32 fp16] written by TMA with SWIZZLE_64B:
@@ -144,10 +172,10 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int2 tij = a.tiles[blockIdx.x / a.nbc];
-  const int bl0 = (blockIdx.x % a.nbc) * a.bpc;
-  const int bl1 = min(a.nbb, bl0 + a.bpc);
-  const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
+  // persistent CTAs: work unit u = (tile u / nbc, bin chunk u % nbc), strided by the grid;
+  // the smem ring and TMEM phases carry over between units, so the next unit's loads
+  // and MMAs overlap this unit's epilogue
+  const int n_units = a.n_tiles * a.nbc;
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // swizzled TMA/UMMA tiles need 1024-byte alignment
@@ -179,12 +207,21 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int2 tij = a.tiles[u / a.nbc];
+        const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
+        const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
       for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
           const int pass = pass0 + ps;
           for (int c = 0; c < n_chunk; ++c) {
             mbar_wait(&empty[stage], phase ^ 1);
             unsigned char* st = smem + stage * kTcStageBytes;
+            if (TC_ABL(16)) {
+              mbar_arrive(&full[stage]);
+              if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+              continue;
+            }
             mbar_expect_tx(&full[stage], kTcStageBytes);
             for (int pl = 0; pl < 4; ++pl) {
               const int z = (bl * 2 + pass) * 4 + pl;
@@ -194,42 +231,51 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
         }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      // (A plane, B plane) for D_re then D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l;
-      // the last three D_im products are -(Re_i Im_j) via the A-negate bit
-      const int prod_a[12] = {0, 0, 1, 2, 2, 3, 2, 2, 3, 0, 0, 1};
-      const int prod_b[12] = {0, 1, 0, 2, 3, 2, 0, 1, 0, 2, 3, 2};
-      const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t tuse[2] = {0, 0};
+    // the whole warp runs the (uniform) loop so descriptors stay in uniform registers;
+    // one elected lane issues each tcgen05.mma / commit
+    // (A plane, B plane) for D_re then D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l;
+    // the last three D_im products are -(Re_i Im_j) via the A-negate bit
+    constexpr int prod_a[12] = {0, 0, 1, 2, 2, 3, 2, 2, 3, 0, 0, 1};
+    constexpr int prod_b[12] = {0, 1, 0, 2, 3, 2, 0, 1, 0, 2, 3, 2};
+    constexpr uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t tuse = 0;  // bit r: phase of TMEM region r
+    const uint64_t desc0 = umma_desc_sw64(smem_u32(smem));
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
       for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
           const int reg = ps;
-          mbar_wait(&tempty[reg], (tuse[reg] & 1) ^ 1);
-          ++tuse[reg];
+          mbar_wait(&tempty[reg], ((tuse >> reg) & 1) ^ 1);
+          tuse ^= 1u << reg;
           tc_fence_after();
           const uint32_t d_re = tmem + reg * 128, d_im = d_re + 64;
           for (int c = 0; c < n_chunk; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t base = smem_u32(smem + stage * kTcStageBytes);
-            const int n_steps = min(kTcChunk / 16, (a.K_pad - c * kTcChunk) / 16);
-            for (int s = 0; s < n_steps; ++s)
+            const uint64_t sd = desc0 + (uint64_t)((stage * kTcStageBytes) >> 4);
+            const int n_steps = TC_ABL(8) ? 0 : min(kTcChunk / 16, (a.K_pad - c * kTcChunk) / 16);
 #pragma unroll
-              for (int q = 0; q < 12; ++q) {
-                const uint64_t ad = umma_desc_sw64(base + prod_a[q] * kTcPlaneA + s * 32);
-                const uint64_t bd = umma_desc_sw64(base + 4 * kTcPlaneA + prod_b[q] * kTcPlaneB + s * 32);
-                const bool first = (c == 0 && s == 0 && (q == 0 || q == 6));
-                tc_mma(q < 6 ? d_re : d_im, ad, bd, (q >= 9) ? id_neg : id_pos, first ? 0u : 1u);
+            for (int s = 0; s < kTcChunk / 16; ++s) {
+              if (s < n_steps) {
+#pragma unroll
+                for (int q = 0; q < 12; ++q) {
+                  const uint64_t ad = sd + (uint64_t)((prod_a[q] * kTcPlaneA + s * 32) >> 4);
+                  const uint64_t bd = sd + (uint64_t)((4 * kTcPlaneA + prod_b[q] * kTcPlaneB + s * 32) >> 4);
+                  const bool first = (c == 0 && s == 0 && (q == 0 || q == 6));
+                  tc_mma_elect(q < 6 ? d_re : d_im, ad, bd, (q >= 9) ? id_neg : id_pos, first ? 0u : 1u);
+                }
               }
-            tc_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+            }
+            tc_commit_elect(&empty[stage]);  // frees the smem stage when these MMAs finish
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
-          tc_commit(&tfull[reg]);      // accumulators of (bin, pass) complete
+          tc_commit_elect(&tfull[reg]);      // accumulators of (bin, pass) complete
         }
     }
   } else if (warp >= 4) {
@@ -237,23 +283,31 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     // warp e = warp - 4: TMEM lane quadrant q = warp % 4 (hardware rule), column half h
     const int e = warp - 4, q = warp & 3, h = e >> 2;
     const int r = q * 32 + lane;             // tile row owned in the TMEM phase
-    const int i = iBase + r;
     const int cb = h * 32;                   // first tile column owned in the TMEM phase
     const float inv_nb = 1.f / (float)a.nbb;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const int et = e * 32 + lane;            // 0..255 within the epilogue group
+    const uint32_t xb = smem_u32(xbuf), cfb = smem_u32(colfac), rob = smem_u32(rowoff_s);
+    const uint32_t xrow = xb + (uint32_t)(r * kTcXStride) * 8u;  // this thread's transpose row
+    const bool cohy = a.cohy_bins || a.cohy_band;
+    uint32_t tuse = 0;  // bit r: phase of TMEM region r
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int2 tij = a.tiles[u / a.nbc];
+    const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
+    const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
+    const int i = iBase + r;
+    const int chi = a.N - jBase;             // valid tile columns: c < chi (and c > i - jBase)
+    // (the previous unit's last epi_bar ordered its rowoff_s reads before these writes)
     if (et < kTcTile) {
       const int ii = iBase + et;
       const bool ok = ii >= a.i_lo && ii < a.i_hi && ii < a.N;
       // pair (ii, j) -> rowoff + j; row 0 legitimately has offset -1, so INT64_MIN marks skipped rows
       rowoff_s[et] = ok ? (int64_t)ii * (a.N - 1) - (int64_t)ii * (ii - 1) / 2 - ii - 1 - a.pair_base : INT64_MIN;
     }
-    const bool cohy = a.cohy_bins || a.cohy_band;
-    uint32_t tuse[2] = {0, 0};
     for (int bl = bl0; bl < bl1; ++bl) {
       const bool acc_band = bl != bl0;  // first bin of the chunk initialises the TMEM band sums
       const int64_t bo = (int64_t)bl * a.pair_stride;
-      float pi = 0.f;
+      float rsi = 0.f;                  // 1/sqrt(psd_i s_i^2), 0 for a dead node
       if (a.do_x) {
         if (et < kTcTileJ) {
           const int j = jBase + et;
@@ -262,47 +316,51 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             const float sj = a.nscale[(int64_t)bl * a.N + j];
             f = a.psd[(int64_t)bl * a.N + j] * sj * sj;
           }
-          colfac[et] = f;
+          colfac[et] = f > 0.f ? rsqrtf(f) : 0.f;
         }
         if (i < a.N) {
           const float si = a.nscale[(int64_t)bl * a.N + i];
-          pi = a.psd[(int64_t)bl * a.N + i] * si * si;
+          const float pi = a.psd[(int64_t)bl * a.N + i] * si * si;
+          rsi = pi > 0.f ? rsqrtf(pi) : 0.f;
         }
       }
       epi_bar();
       for (int ps = 0; ps < npass; ++ps) {
         const int pass = pass0 + ps;
         const int reg = ps;
-        mbar_wait(&tfull[reg], tuse[reg] & 1);
-        ++tuse[reg];
+        mbar_wait(&tfull[reg], (tuse >> reg) & 1);
+        tuse ^= 1u << reg;
         tc_fence_after();
         const uint32_t t_acc = tmem + lane_addr + reg * 128;
 #pragma unroll
         for (int c1 = 0; c1 < 32; c1 += 16) {
           const int c0 = cb + c1;
           float vr[16], vi[16];
-          tmem_ld16(t_acc + c0, vr);
-          tmem_ld16(t_acc + 64 + c0, vi);
+          tmem_ld16x2(t_acc + c0, vr, t_acc + 64 + c0, vi);
+          if (TC_ABL(2)) { sts_f2(xrow + c0 * 8u, vr[3], vi[5]); continue; }
           if (pass == 0) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-              const float pp = pi * colfac[c0 + u];
-              const float rs = pp > 0.f ? rsqrtf(pp) : 0.f;
-              vr[u] *= rs;
-              vi[u] *= rs;
+            for (int u4 = 0; u4 < 16; u4 += 4) {
+              const float4 cf = lds_f4(cfb + (uint32_t)(c0 + u4) * 4u);
+              const float rs[4] = {rsi * cf.x, rsi * cf.y, rsi * cf.z, rsi * cf.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                vr[u4 + u] *= rs[u];
+                vi[u4 + u] *= rs[u];
+              }
             }
             if (a.coh_band || !cohy) {
               float m[16];
 #pragma unroll
-              for (int u = 0; u < 16; ++u) m[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]);
+              for (int u = 0; u < 16; ++u) m[u] = sqrt_approx(vr[u] * vr[u] + vi[u] * vi[u]);
               if (!cohy)
 #pragma unroll
-                for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(m[u], vi[u]);
+                for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, m[u], vi[u]);
               if (a.coh_band) {
                 float b[16];
                 if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) b[u] = (acc_band ? b[u] : 0.f) + m[u] * inv_nb;
+                for (int u = 0; u < 16; ++u) b[u] = acc_band ? fmaf(m[u], inv_nb, b[u]) : m[u] * inv_nb;
                 tmem_st16(tmem + lane_addr + kTmBand + c0, b);
               }
             }
@@ -310,22 +368,19 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               float bi[16];
               if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
 #pragma unroll
-              for (int u = 0; u < 16; ++u) bi[u] = (acc_band ? bi[u] : 0.f) + vi[u] * inv_nb;
+              for (int u = 0; u < 16; ++u) bi[u] = acc_band ? fmaf(vi[u], inv_nb, bi[u]) : vi[u] * inv_nb;
               tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
             }
             if (cohy) {
 #pragma unroll
-              for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(vr[u], vi[u]);
+              for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, vr[u], vi[u]);
               if (a.cohy_band) {
                 float br[16], bi[16];
-                if (acc_band) {
-                  tmem_ld16(tmem + lane_addr + kTmBand + 128 + c0, br);
-                  tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
-                }
+                if (acc_band) tmem_ld16x2(tmem + lane_addr + kTmBand + 128 + c0, br, tmem + lane_addr + kTmBand + 192 + c0, bi);
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                  br[u] = (acc_band ? br[u] : 0.f) + vr[u] * inv_nb;
-                  bi[u] = (acc_band ? bi[u] : 0.f) + vi[u] * inv_nb;
+                  br[u] = acc_band ? fmaf(vr[u], inv_nb, br[u]) : vr[u] * inv_nb;
+                  bi[u] = acc_band ? fmaf(vi[u], inv_nb, bi[u]) : vi[u] * inv_nb;
                 }
                 tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
                 tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
@@ -334,14 +389,14 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
           } else {
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-              vr[u] = sqrtf(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
-              xbuf[r * kTcXStride + c0 + u].x = vr[u];
+              vr[u] = sqrt_approx(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
+              sts_f32(xrow + (uint32_t)(c0 + u) * 8u, vr[u]);
             }
             if (a.plv_band) {
               float b[16];
               if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 64 + c0, b);
 #pragma unroll
-              for (int u = 0; u < 16; ++u) b[u] = (acc_band ? b[u] : 0.f) + vr[u] * inv_nb;
+              for (int u = 0; u < 16; ++u) b[u] = acc_band ? fmaf(vr[u], inv_nb, b[u]) : vr[u] * inv_nb;
               tmem_st16(tmem + lane_addr + kTmBand + 64 + c0, b);
             }
           }
@@ -352,23 +407,46 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[reg]);
         epi_bar();
-        // per-bin outputs: warp e stores rows [16 e, 16 e + 16), 64 contiguous pairs each
-        for (int rr = 0; rr < 16; ++rr) {
-          const int row = e * 16 + rr;
-          const int64_t ro = rowoff_s[row];
-          if (ro == INT64_MIN) continue;
-          const int ii = iBase + row;
+        // per-bin outputs: warp e stores rows [16 e, 16 e + 16), 64 contiguous pairs each;
+        // four rows per group, all shared loads of a group issued before its stores
+        if (!TC_ABL(1)) {
+          float* const px = pass == 0 ? a.coh_bins : a.plv_bins;   // .x: COH (or |COHY|) / PLV
+          float* const py = pass == 0 ? a.imag_bins : nullptr;     // .y: IMAGCOHY
+          float2* const pc = (pass == 0 && cohy) ? a.cohy_bins : nullptr;
+          const bool magx = pass == 0 && cohy;                     // buffer holds COHY: COH = |.|
+          for (int g = 0; g < 16; g += 4) {
+            long long ro[4];
+            float2 v0[4], v1[4];
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int c = lane + 32 * hh, j = jBase + c;
-            if (j <= ii || j >= a.N) continue;
-            const float2 v = xbuf[row * kTcXStride + c];
-            if (pass == 0) {
-              if (cohy && a.cohy_bins) a.cohy_bins[bo + ro + j] = v;
-              if (a.coh_bins) a.coh_bins[bo + ro + j] = cohy ? sqrtf(v.x * v.x + v.y * v.y) : v.x;
-              if (a.imag_bins) a.imag_bins[bo + ro + j] = v.y;
-            } else if (a.plv_bins) {
-              a.plv_bins[bo + ro + j] = v.x;
+            for (int t = 0; t < 4; ++t) {
+              const int row = e * 16 + g + t;
+              ro[t] = lds_s64(rob + (uint32_t)row * 8u);
+              const uint32_t xa = xb + (uint32_t)(row * kTcXStride + lane) * 8u;
+              v0[t] = lds_f2(xa);
+              v1[t] = lds_f2(xa + 256u);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int row = e * 16 + g + t;
+              const int clo = iBase + row + 1 - jBase;
+              const bool live = ro[t] != INT64_MIN;
+              const bool ok0 = live && lane >= clo && lane < chi;
+              const bool ok1 = live && lane + 32 >= clo && lane + 32 < chi;
+              const int64_t off = bo + ro[t] + jBase + lane;
+              if (px) {
+                const float x0 = magx ? sqrt_approx(v0[t].x * v0[t].x + v0[t].y * v0[t].y) : v0[t].x;
+                const float x1 = magx ? sqrt_approx(v1[t].x * v1[t].x + v1[t].y * v1[t].y) : v1[t].x;
+                if (ok0) px[off] = x0;
+                if (ok1) px[off + 32] = x1;
+              }
+              if (py) {
+                if (ok0) py[off] = v0[t].y;
+                if (ok1) py[off + 32] = v1[t].y;
+              }
+              if (pc) {
+                if (ok0) pc[off] = v0[t];
+                if (ok1) pc[off + 32] = v1[t];
+              }
             }
           }
         }
@@ -376,7 +454,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       }
     }
     // band means: TMEM -> transpose buffer -> coalesced stores
-    if (a.coh_band || a.plv_band || a.cohy_band || a.imag_band) {
+    if (!TC_ABL(4) && (a.coh_band || a.plv_band || a.cohy_band || a.imag_band)) {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       for (int kind = 0; kind < 4; ++kind) {
         if ((kind == 0 && !a.coh_band) || (kind == 1 && !a.plv_band) || (kind == 2 && !a.cohy_band) ||
@@ -386,44 +464,47 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         for (int c1 = 0; c1 < 32; c1 += 16) {
           const int c0 = cb + c1;
           float b0[16], b1[16];
-          tmem_ld16(tmem + lane_addr + kTmBand + (kind >= 2 ? (kind == 3 ? 192 : 128) : kind * 64) + c0, b0);
-          if (kind == 2) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, b1);
+          const uint32_t col = kTmBand + (kind >= 2 ? (kind == 3 ? 192 : 128) : kind * 64) + c0;
+          if (kind == 2) tmem_ld16x2(tmem + lane_addr + col, b0, tmem + lane_addr + kTmBand + 192 + c0, b1);
+          else tmem_ld16(tmem + lane_addr + col, b0);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) xbuf[r * kTcXStride + c0 + u] = make_float2(b0[u], kind == 2 ? b1[u] : 0.f);
+          for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, b0[u], kind == 2 ? b1[u] : 0.f);
         }
         epi_bar();
+        float* dst1 = kind == 0 ? a.coh_band : (kind == 1 ? a.plv_band : a.imag_band);
         for (int rr = 0; rr < 16; ++rr) {
           const int row = e * 16 + rr;
-          const int64_t ro = rowoff_s[row];
+          const long long ro = lds_s64(rob + (uint32_t)row * 8u);
           if (ro == INT64_MIN) continue;
-          const int ii = iBase + row;
+          const int clo = iBase + row + 1 - jBase;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const int c = lane + 32 * hh, j = jBase + c;
-            if (j <= ii || j >= a.N) continue;
-            const float2 v = xbuf[row * kTcXStride + c];
-            float* dst1 = kind == 0 ? a.coh_band : (kind == 1 ? a.plv_band : a.imag_band);
+            const int c = lane + 32 * hh;
+            if (c < clo || c >= chi) continue;
+            const float2 v = lds_f2(xb + (uint32_t)(row * kTcXStride + c) * 8u);
+            const int64_t o = ro + jBase + c;
             if (a.nbc > 1) {  // bins split over CTAs: the host zeroed the band outputs
               if (kind == 2) {
-                atomicAdd(&a.cohy_band[ro + j].x, v.x);
-                atomicAdd(&a.cohy_band[ro + j].y, v.y);
+                atomicAdd(&a.cohy_band[o].x, v.x);
+                atomicAdd(&a.cohy_band[o].y, v.y);
               } else {
-                atomicAdd(&dst1[ro + j], v.x);
+                atomicAdd(&dst1[o], v.x);
               }
             } else if (kind == 2) {
-              a.cohy_band[ro + j] = v;
+              a.cohy_band[o] = v;
             } else {
-              dst1[ro + j] = v.x;
+              dst1[o] = v.x;
             }
             if (kind == 2 && a.imag_band) {  // IMAGCOHY band = Im of the COHY band mean
-              if (a.nbc > 1) atomicAdd(&a.imag_band[ro + j], v.y);
-              else a.imag_band[ro + j] = v.y;
+              if (a.nbc > 1) atomicAdd(&a.imag_band[o], v.y);
+              else a.imag_band[o] = v.y;
             }
           }
         }
         epi_bar();
       }
     }
+    }  // units
   }
 
   tc_fence_before();
@@ -544,6 +625,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     p.tc_tiles_key = key;
   }
   const int64_t n_tiles = p.tc_ntiles;
+  a.n_tiles = (int)n_tiles;
   a.tiles = (const int2*)p.tc_tiles;
   {  // small pair spaces: split bins over CTAs for >= ~2 waves
     int nbc = n_tiles > 0 ? (int)((2 * 148 + n_tiles - 1) / n_tiles) : 1;
@@ -563,6 +645,9 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.imag_bins = do_imag ? (float*)out->bins[2] : nullptr;
   a.imag_band = do_imag ? (float*)out->band[2] : nullptr;
   a.do_x = do_x; a.do_u = do_u;
+#ifdef CS_TC_ABLATION
+  { const char* d = getenv("CSCONN_TC_DBG"); a.dbg = d ? atoi(d) : 0; }
+#endif
   const size_t smem = tc_smem_bytes();
   static bool configured = false;
   if (!configured) {
@@ -577,7 +662,13 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
       if (a.cohy_band) cudaMemsetAsync(a.cohy_band, 0, a.pair_stride * sizeof(float2), st);
       if (a.imag_band) cudaMemsetAsync(a.imag_band, 0, a.pair_stride * sizeof(float), st);
     }
-    if (n_tiles > 0) k_pairs_tc<<<(unsigned)(n_tiles * a.nbc), kTcThreads, smem, st>>>(mapA, mapB, a);
+    if (n_tiles > 0) {  // persistent: one CTA per SM (210 KB smem), units strided over the grid
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+      const int64_t units = n_tiles * a.nbc;
+      const int64_t grid = units < nsm ? units : nsm;
+      k_pairs_tc<<<(unsigned)grid, kTcThreads, smem, st>>>(mapA, mapB, a);
+    }
   }
   return true;
 }
