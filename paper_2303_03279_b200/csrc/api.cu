@@ -282,7 +282,8 @@ int cs_plan_destroy(cs_plan* p) {
   DeviceGuard g(p->device);
   cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
   if (p->tc_ops) cudaFree(p->tc_ops);
-  if (p->tc_tiles) cudaFree(p->tc_tiles);
+  for (auto& e : p->tc_tiles)
+    if (e.ptr) cudaFree(e.ptr);
   if (p->lag_ops) cudaFree(p->lag_ops);
   cudaFree(p->flags); cudaFree(p->counters);
   if (p->prof) {

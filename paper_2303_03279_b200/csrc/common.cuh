@@ -35,9 +35,14 @@ struct Plan {
   size_t tc_bytes = 0;
   void* lag_ops = nullptr;       // packed trial-pair operands of the phase-lag kernel
   size_t lag_bytes = 0;
-  void* tc_tiles = nullptr;      // tensor-core tile order (int2 list) for the cached row range
-  int64_t tc_ntiles = 0;
-  uint64_t tc_tiles_key = 0;
+  struct TileList {              // tensor-core tile order (int2 list) of one row range
+    uint64_t key = 0;
+    void* ptr = nullptr;
+    int64_t n = 0;
+  };
+  static constexpr int kTileCache = 16;  // row-chunked callers cycle through a few ranges
+  TileList tc_tiles[kTileCache];
+  int tc_tiles_next = 0;
   int4* flags = nullptr;         // fp64-fallback work list (i, j, local bin, -)
   int* counters = nullptr;       // [0] flag count, [1] overflow
   int flag_cap = 0;

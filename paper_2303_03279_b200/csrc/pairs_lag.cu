@@ -44,8 +44,6 @@ struct LagArgs {
   int64_t pair_base, pair_stride;
   float* bins[5];    // IMAGCOHY, PLI, USPLI, WPLI, DSWPLI : [nbb][pair_stride]
   float* band[5];
-  const float* ext_imag;  // IMAGCOHY per-bin written by the tensor-core kernel (single taper), or null
-  float* ext_imag_band;   // and its band mean
   float* plv_bins;   // multitaper only: PLV of the taper-mean CSD (not separable -> CUDA cores)
   float* plv_band;
   float g;           // guard factor
@@ -136,12 +134,6 @@ __global__ void k_lag_fallback(const LagArgs a) {
       v[4] = (float)(wpli * wpli);
       const int64_t po = pair_of(i, j, a.N) - a.pair_base;
       const float inv = 1.f / (float)a.nbb;
-      if (a.ext_imag) {  // IMAGCOHY came from the tensor-core kernel: replace it by the fp64 value
-        float* ib = (float*)a.ext_imag + (int64_t)bl * a.pair_stride + po;
-        const float old = *ib;
-        *ib = v[0];
-        if (a.ext_imag_band) atomicAdd(&a.ext_imag_band[po], (v[0] - old) * inv);
-      }
       for (int m = 0; m < 5; ++m) {
         if (a.bins[m]) a.bins[m][(int64_t)bl * a.pair_stride + po] = v[m];
         if (a.band[m]) atomicAdd(&a.band[m][po], v[m] * inv);
@@ -153,7 +145,7 @@ __global__ void k_lag_fallback(const LagArgs a) {
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, const float* ext_imag,
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, cudaStream_t st);
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
@@ -177,7 +169,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
     }
     if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
                      a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters, a.flag_cap,
-                     n_tiles, nbc, a.ext_imag, a.L, a.plv_bins, a.plv_band, st))
+                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, st))
       return false;
   }
   {
@@ -194,21 +186,6 @@ namespace cs {
 // metric-bit -> lag-kernel output slot
 static const unsigned kLagBits[5] = {CS_IMAGCOHY, CS_PLI, CS_USPLI, CS_WPLI, CS_DSWPLI};
 
-// Single taper with COH/COHY requested and IMAGCOHY per-bin output present: the
-// tensor-core pass that produces COH also yields D_im = sum Im exactly as IMAGCOHY
-// needs it, so IMAGCOHY moves there and the phase-lag kernel drops its sum-Im
-// accumulation (one FADD2 of eight FMA-pipe cycles per two trials) and reads it back.
-// Measured on cfg5 (B200, all 7 metrics): the phase-lag kernel drops from 8.95 to
-// 8.31 ms, but the tensor-core kernel then carries the IMAGCOHY stores (3.15 -> 3.66
-// ms) and the fallback patches them (0.28 -> 0.62 ms): 14.55 vs 14.31 ms per step.
-// Kept as an option (CSCONN_EXT_IMAG=1), off by default.
-bool lag_ext_imag(const Plan& p, unsigned mask, const cs_outputs* out) {
-  static const bool enabled = [] {
-    const char* e = getenv("CSCONN_EXT_IMAG");
-    return e && e[0] == '1';
-  }();
-  return enabled && p.L == 1 && (mask & CS_IMAGCOHY) && (mask & (CS_COH | CS_COHY)) && out->bins[2] != nullptr;
-}
 static const int kLagIdx[5] = {2, 4, 5, 6, 7};
 
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
@@ -255,12 +232,6 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     a.bins[q] = on ? (float*)out->bins[kLagIdx[q]] : nullptr;
     a.band[q] = on ? (float*)out->band[kLagIdx[q]] : nullptr;
   }
-  if (lag_ext_imag(p, mask, out)) {  // IMAGCOHY (and sum Im) come from the tensor-core kernel
-    a.ext_imag = (const float*)out->bins[2];
-    a.ext_imag_band = (float*)out->band[2];
-    a.bins[0] = nullptr;
-    a.band[0] = nullptr;
-  }
   a.plv_bins = plvk ? (float*)out->bins[3] : nullptr;
   a.plv_band = plvk ? (float*)out->band[3] : nullptr;
   a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
@@ -282,7 +253,7 @@ int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   const bool do_x = (mask & (CS_COHY | CS_COH)) != 0;
   const bool do_u = (mask & CS_PLV) != 0 && p.L == 1;  // multitaper PLV runs in the lag kernel
   if (!do_x && !do_u) return 0;
-  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, lag_ext_imag(p, mask, out), out, p.nscale, st))
+  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, false, out, p.nscale, st))
     return -1;
   return 0;  // launches are counted by the phase marks
 }

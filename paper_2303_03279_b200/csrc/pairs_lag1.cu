@@ -41,7 +41,6 @@ struct Lag1Args {
   float* band[5];
   float* plv_bins;           // multitaper: PLV of the taper-mean CSD (PLVK instantiation)
   float* plv_band;
-  const float* ext_imag;     // IMAGCOHY per-bin from the tensor-core kernel (sum Im = IMAG * sqrt(psd psd)), or null
   float g;
   int4* flags;
   int* counters;
@@ -52,7 +51,7 @@ struct Lag1Args {
 // then allows 96 registers, enough for the single-taper loop); L > 1 needs 128
 // registers, so 16 warps with the TMA issued from warp 0 (measured: the dedicated
 // warp is 2.7 % faster for L == 1 on cfg5).
-template <int L, bool PLVK, bool EXT_IM>
+template <int L, bool PLVK>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -151,30 +150,20 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     if (PLVK) pvr[p] = pvi[p] = 0ull;
   }
 
+  int bl = bl0, st = -1;  // bin and stage-in-bin of step t, advanced incrementally (no divisions)
   for (int t = 0; t < total; ++t) {
     issue(t + k1Stages - 1);
+    if (++st == n_stage) {
+      st = 0;
+      ++bl;
+    }
     const int s = t % k1Stages;
-    const int bl = bl0 + t / n_stage, st = t % n_stage;
     mbar_wait(&full[s], (t / k1Stages) & 1);
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
     const int nkp = min(kc, a.Kp - st * kc);
-    float ximag[k1NP];  // EXT_IM: prefetch this bin's IMAGCOHY before its last stage computes
-    if (EXT_IM && st + 1 == n_stage) {
-#pragma unroll
-      for (int r = 0; r < k1TR; ++r) {
-        const int i = iBase + ty + k1TY * r;
-        const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base +
-                               (int64_t)bl * a.pair_stride;
-#pragma unroll
-        for (int c = 0; c < k1TC; ++c) {
-          const int j = jBase + tx + k1TX * c;
-          ximag[r * k1TC + c] = (i < j && j < a.N) ? __ldcs(a.ext_imag + rowoff + j) : 0.f;
-        }
-      }
-    }
     auto stats = [&](int p, f2 tt) {
-      if (!EXT_IM) sim[p] = fadd2(sim[p], tt);  // EXT_IM: sum Im comes from the tensor cores
+      sim[p] = fadd2(sim[p], tt);
       const float tl = lo_of(tt), th = hi_of(tt);
       sabs[p] += fabsf(tl);
       sabs[p] += fabsf(th);
@@ -245,38 +234,43 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     if (st + 1 < n_stage) continue;
 
     // ---- epilogue for bin bl ----
+    // per-node factors first (6 nodes per thread), then ~30 instructions per pair
     const int b = a.bin_lo + bl;
     const bool real_bin = (b == a.real0) || (b == a.real1);
-    float Mi[k1TR], Mj[k1TC], Pi[k1TR], Pj[k1TC];
+    float Mi[k1TR], gMi[k1TR], rPi[k1TR], phI[k1TR];
+    float Mj[k1TC], rPj[k1TC], phJ[k1TC];
 #pragma unroll
     for (int r = 0; r < k1TR; ++r) {
       const int i = iBase + ty + k1TY * r;
-      Mi[r] = i < a.N ? a.mag[(int64_t)bl * a.N + i] : 0.f;
-      Pi[r] = i < a.N ? a.psd[(int64_t)bl * a.N + i] : 0.f;
+      const float m = (i < a.N && !real_bin) ? a.mag[(int64_t)bl * a.N + i] : 0.f;
+      const float pw = i < a.N ? a.psd[(int64_t)bl * a.N + i] : 0.f;
+      Mi[r] = m;
+      gMi[r] = a.g * m;
+      rPi[r] = pw > 0.f ? rsqrt_approx(pw) : 0.f;
+      phI[r] = odd ? m * k1Phantom : 0.f;
     }
 #pragma unroll
     for (int c = 0; c < k1TC; ++c) {
       const int j = jBase + tx + k1TX * c;
-      Mj[c] = j < a.N ? a.mag[(int64_t)bl * a.N + j] : 0.f;
-      Pj[c] = j < a.N ? a.psd[(int64_t)bl * a.N + j] : 0.f;
+      const float m = (j < a.N && !real_bin) ? a.mag[(int64_t)bl * a.N + j] : 0.f;
+      const float pw = j < a.N ? a.psd[(int64_t)bl * a.N + j] : 0.f;
+      Mj[c] = m;
+      rPj[c] = pw > 0.f ? rsqrt_approx(pw) : 0.f;
+      phJ[c] = m * k1Phantom;
     }
     const int64_t bin_off = (int64_t)bl * a.pair_stride;
 #pragma unroll
     for (int r = 0; r < k1TR; ++r) {
       const int li = ty + k1TY * r, i = iBase + li;
-      const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+      const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + bin_off;
 #pragma unroll
       for (int c = 0; c < k1TC; ++c) {
         const int p = r * k1TC + c;
         const int lj = tx + k1TX * c, j = jBase + lj;
         const bool valid = (i < j) && (j < a.N);
-        const bool dead = real_bin || Mi[r] == 0.f || Mj[c] == 0.f;
-        const float pp = Pi[r] * Pj[c];
-        const int64_t po = rowoff + j;
-        // EXT_IM: |sum Im| carries the tensor-core error (~3e-7 sqrt(psd psd)); WPLI
-        // stays within 3e-4 unless sum |Im| < 1e-3 sqrt(psd psd) -> those go to fp64
-        const bool weak = EXT_IM && sabs[p] < 1e-3f * sqrtf(pp);
-        const bool flagged = valid && !dead && (mn[p] <= a.g * Mi[r] * Mj[c] || weak);
+        // dead: a node with a zero spectrum in this bin (or DC / Nyquist): all Im are 0
+        const bool dead = Mi[r] * Mj[c] == 0.f;
+        const bool flagged = valid && !dead && mn[p] <= gMi[r] * Mj[c];
         if (flagged) {  // rare: the fp64 fallback writes this (pair, bin)
           const int slot = atomicAdd(&a.counters[0], 1);
           if (slot < a.flag_cap)
@@ -284,28 +278,24 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           else
             a.counters[1] = 1;
         }
-        const float tph = odd ? (Mi[r] * k1Phantom) * (Mj[c] * k1Phantom) : 0.f;
-        float s_im;
-        if (EXT_IM)
-          s_im = (dead || !valid) ? 0.f : ximag[p] * sqrtf(pp);
-        else
-          s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+        const float tph = phI[r] * phJ[c];  // odd-K phantom trial (0 when K is even)
+        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
         const float s_abs = dead ? 0.f : sabs[p] - tph;
         const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
         float v[5];
-        v[0] = pp > 0.f ? s_im * rsqrtf(pp) : 0.f;
+        v[0] = s_im * rPi[r] * rPj[c];
         const float pli = fabsf((float)pli_sum) * invK;
         v[1] = pli;
         v[2] = pli * pli * uspA - uspB;
-        const float w = s_abs > 0.f ? fminf(__fdividef(fabsf(s_im), s_abs), 1.f) : 0.f;
+        const float w = s_abs > 0.f ? fminf(fabsf(s_im) * rcp_approx(s_abs), 1.f) : 0.f;
         v[3] = w;
         v[4] = w * w;
         if (PLVK && valid) {  // PLV is continuous: written even for guard-flagged entries
           // the odd-K phantom contributed the unit phasor (0, 1) to the PLV sums
           const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
           const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
-          const float plv = dead ? 0.f : sqrtf(pr * pr + pim * pim) * invK;
-          if (bin_mask & 32u) a.plv_bins[bin_off + po] = plv;
+          const float plv = dead ? 0.f : sqrt_approx(pr * pr + pim * pim) * invK;
+          if (bin_mask & 32u) a.plv_bins[rowoff + j] = plv;
           if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
           pvr[p] = pvi[p] = 0ull;
         }
@@ -313,7 +303,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
-            if (bin_mask & (1u << m)) a.bins[m][bin_off + po] = v[m];
+            if (bin_mask & (1u << m)) a.bins[m][rowoff + j] = v[m];
             if (band_mask & (1u << m)) bs[m * kTile * kTile] += v[m];
           }
         }
@@ -354,7 +344,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc, const float* ext_imag,
+                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
@@ -388,33 +378,31 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     a.band[m] = band[m];
   }
   a.g = g; a.flags = flags; a.counters = counters; a.flag_cap = flag_cap;
-  a.ext_imag = ext_imag;
   a.plv_bins = plv_bins;
   a.plv_band = plv_band;
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
   const unsigned grid = (unsigned)(n_tiles * nbc);
   const bool plvk = plv_bins || plv_band;
-#define CS_LAG1(LL, PV, EX)                                                                              \
+#define CS_LAG1(LL, PV)                                                                              \
   do {                                                                                                   \
     static bool cfg = false;                                                                             \
     if (!cfg) {                                                                                          \
-      cudaFuncSetAttribute(k_pairs_lag1<LL, PV, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cudaFuncSetAttribute(k_pairs_lag1<LL, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       cfg = true;                                                                                        \
     }                                                                                                    \
-    k_pairs_lag1<LL, PV, EX><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
+    k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
   } while (0)
   if (L == 1) {
-    if (ext_imag) CS_LAG1(1, false, true);
-    else CS_LAG1(1, false, false);
+    CS_LAG1(1, false);
   } else if (L == 2) {
-    if (plvk) CS_LAG1(2, true, false);
-    else CS_LAG1(2, false, false);
+    if (plvk) CS_LAG1(2, true);
+    else CS_LAG1(2, false);
   } else if (L == 3) {
-    if (plvk) CS_LAG1(3, true, false);
-    else CS_LAG1(3, false, false);
+    if (plvk) CS_LAG1(3, true);
+    else CS_LAG1(3, false);
   } else {
-    if (plvk) CS_LAG1(4, true, false);
-    else CS_LAG1(4, false, false);
+    if (plvk) CS_LAG1(4, true);
+    else CS_LAG1(4, false);
   }
 #undef CS_LAG1
   return true;

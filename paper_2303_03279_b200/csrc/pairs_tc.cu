@@ -605,28 +605,36 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   // grouped tile order: bands of 8 row tiles swept column by column, so the CTAs
   // resident at once touch ~8 x 128 + 18 x 64 nodes of operands (L2 resident)
   const uint64_t key = ((uint64_t)a.tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)a.nt;
-  if (key != p.tc_tiles_key || !p.tc_tiles) {
+  Plan::TileList* tle = nullptr;
+  for (auto& e : p.tc_tiles)
+    if (e.key == key && e.ptr) tle = &e;
+  if (!tle) {  // build once per row range (a blocking upload: first call for that range only)
     std::vector<int2> tl;
     constexpr int GR = 8;
     for (int b0 = a.tile_row0; b0 < tile_row1; b0 += GR)
       for (int J = 0; J < a.nt; ++J)
         for (int I = b0; I < b0 + GR && I < tile_row1; ++I)
           if (J >= 2 * I) tl.push_back(make_int2(I, J));
-    if (p.tc_tiles) cudaFree(p.tc_tiles);
-    p.tc_tiles = nullptr;
-    p.tc_ntiles = (int64_t)tl.size();
-    if (!tl.empty()) {
-      if (cudaMalloc(&p.tc_tiles, tl.size() * sizeof(int2)) != cudaSuccess) {
-        cs_set_error("device allocation failed (tile list)");
-        return false;
-      }
-      cudaMemcpy(p.tc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    tle = &p.tc_tiles[p.tc_tiles_next];
+    p.tc_tiles_next = (p.tc_tiles_next + 1) % Plan::kTileCache;
+    if (tle->ptr) {
+      cudaStreamSynchronize(st);  // the evicted list may still be read by queued work
+      cudaFree(tle->ptr);
     }
-    p.tc_tiles_key = key;
+    tle->ptr = nullptr;
+    tle->key = key;
+    tle->n = (int64_t)tl.size();
+    const size_t bytes = (tl.empty() ? 1 : tl.size()) * sizeof(int2);
+    if (cudaMalloc(&tle->ptr, bytes) != cudaSuccess) {
+      tle->ptr = nullptr;
+      cs_set_error("device allocation failed (tile list)");
+      return false;
+    }
+    if (!tl.empty()) cudaMemcpy(tle->ptr, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice);
   }
-  const int64_t n_tiles = p.tc_ntiles;
+  const int64_t n_tiles = tle->n;
   a.n_tiles = (int)n_tiles;
-  a.tiles = (const int2*)p.tc_tiles;
+  a.tiles = (const int2*)tle->ptr;
   {  // small pair spaces: split bins over CTAs for >= ~2 waves
     int nbc = n_tiles > 0 ? (int)((2 * 148 + n_tiles - 1) / n_tiles) : 1;
     nbc = nbc < 1 ? 1 : (nbc > nbb ? nbb : nbc);

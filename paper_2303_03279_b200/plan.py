@@ -258,3 +258,90 @@ def compute_connectivity(x: torch.Tensor, nfft: int, lo: int, hi: int, metrics=S
     slots = torch.arange(K, dtype=torch.int32, device=x.device)
     out = plan.pair_metrics(slots, metrics, 0, plan.n_bins, per_bin=per_bin, band=band, stream=stream)
     return out, plan
+
+
+class HostPipeline:
+    """Host-in / host-out batch path with the copies overlapped (the e2e call).
+
+    ``run(xh)`` takes pinned host samples [K, N, T] and returns the band means of
+    ``metrics`` as pinned host arrays [P] (pair order of ``np.triu_indices(N, 1)``),
+    the layout of ``ConnectivityNetwork.weights`` (reference core.py:132-152).
+    Inside one call the upload is split into trial chunks so K1 starts on the
+    first chunk while the rest is in flight, and the pair kernels run over row-tile
+    chunks so each chunk's download overlaps the next chunk's kernels.  ``submit``
+    enqueues without waiting: the upload of call s+1 then overlaps the pair
+    kernels and download of call s (three streams, event-ordered; the spectrum
+    ring and outputs are reused, so every ordering hazard is an event wait).
+    """
+
+    def __init__(self, n_nodes: int, n_samples: int, nfft: int, lo: int, hi: int, n_trials: int,
+                 metrics=SEVEN, taper=None, scale: float = 1.0, device=None, dtype=torch.float32,
+                 in_chunks: int = 10, row_chunks: int = 8):
+        self.plan = DevicePlan(n_nodes, n_samples, nfft, lo, hi, taper=taper, slot_capacity=n_trials,
+                               device=device, scale=scale)
+        dev = self.plan.device
+        self.K = int(n_trials)
+        self.metrics = tuple(m.upper() for m in metrics)
+        self.xd = torch.empty((self.K, n_nodes, n_samples), dtype=dtype, device=dev)
+        self.slots = torch.arange(self.K, dtype=torch.int32, device=dev)
+        P = self.plan.n_pairs
+        self.out = {m: torch.empty((P,), dtype=torch.complex64 if m == "COHY" else torch.float32, device=dev)
+                    for m in self.metrics}
+        bounds = np.linspace(0, self.K, min(in_chunks, self.K) + 1).round().astype(int)
+        self.k_chunks = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        self.r_chunks = []
+        n_r = max(1, min(row_chunks, (n_nodes + 63) // 64))
+        for r in range(n_r):
+            rt, pr = row_tile_range(n_nodes, n_r, r)
+            if pr[1] > pr[0]:
+                self.r_chunks.append((rt, pr))
+        with torch.cuda.device(dev):
+            self.s_in, self.s_comp, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+            self.ev_in = [torch.cuda.Event() for _ in self.k_chunks]
+            self.ev_k1 = torch.cuda.Event()
+            self.ev_rows = [torch.cuda.Event() for _ in self.r_chunks]
+            self.ev_out = torch.cuda.Event()
+        self._armed = False  # ev_k1 / ev_out recorded at least once
+
+    def alloc_host(self):
+        return {m: torch.empty(t.shape, dtype=t.dtype).pin_memory() for m, t in self.out.items()}
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.xd.numel() * self.xd.element_size()
+
+    def submit(self, xh: torch.Tensor, host_out: dict) -> torch.cuda.Event:
+        """Enqueue one call; returns the event that completes its download."""
+        if tuple(xh.shape) != tuple(self.xd.shape) or xh.dtype != self.xd.dtype:
+            raise ParameterError(f"expected host samples {tuple(self.xd.shape)} {self.xd.dtype}")
+        p = self.plan
+        if self._armed:
+            self.s_in.wait_event(self.ev_k1)      # the previous call's K1 has consumed xd
+        for (k0, k1), ev in zip(self.k_chunks, self.ev_in):
+            with torch.cuda.stream(self.s_in):
+                self.xd[k0:k1].copy_(xh[k0:k1], non_blocking=True)
+            ev.record(self.s_in)
+        for (k0, k1), ev in zip(self.k_chunks, self.ev_in):
+            self.s_comp.wait_event(ev)
+            p.spectra(self.xd[k0:k1], k0, stream=self.s_comp)
+        self.ev_k1.record(self.s_comp)
+        if self._armed:
+            self.s_comp.wait_event(self.ev_out)   # the previous call's download has read the outputs
+        for ((rb, re), (p0, p1)), ev in zip(self.r_chunks, self.ev_rows):
+            view = {m: {"bins": None, "band": t[p0:p1]} for m, t in self.out.items()}
+            p.pair_metrics(self.slots, self.metrics, 0, p.n_bins, outputs=view, per_bin=False, band=True,
+                           row_tiles=(rb, re), pair_base=p0, pair_count=p1 - p0, stream=self.s_comp)
+            ev.record(self.s_comp)
+        for ((rb, re), (p0, p1)), ev in zip(self.r_chunks, self.ev_rows):
+            self.s_out.wait_event(ev)
+            with torch.cuda.stream(self.s_out):
+                for m, t in self.out.items():
+                    host_out[m][p0:p1].copy_(t[p0:p1], non_blocking=True)
+        self.ev_out.record(self.s_out)
+        self._armed = True
+        return self.ev_out
+
+    def run(self, xh: torch.Tensor, host_out: dict | None = None) -> dict:
+        host_out = host_out if host_out is not None else self.alloc_host()
+        self.submit(xh, host_out).synchronize()
+        return host_out
