@@ -264,6 +264,28 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
     }
     cudaMemcpy(p->fft_tw, ft.data(), ft.size() * sizeof(double2), cudaMemcpyHostToDevice);
     cudaMemcpy(p->post_tw, pt.data(), pt.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    if ((M == 256 || M == 512) && !(getenv("CSCONN_FFT") && getenv("CSCONN_FFT")[0] == 'r')) {
+      const int A = M / 32;  // four-step tables: W_M^{b k_a} [k_a][b], then W_32^j
+      std::vector<double2> t4((size_t)A * 32 + 32);
+      for (int ka = 0; ka < A; ++ka)
+        for (int b = 0; b < 32; ++b) {
+          double c, s;
+          twiddle((long)b * ka, M, &c, &s);
+          t4[(size_t)ka * 32 + b] = make_double2(c, s);
+        }
+      for (int j = 0; j < 32; ++j) {
+        double c, s;
+        twiddle(j, 32, &c, &s);
+        t4[(size_t)A * 32 + j] = make_double2(c, s);
+      }
+      if (cudaMalloc(&p->fft4_tw, t4.size() * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        cs_set_error("device allocation failed (FFT tables)");
+        cs_plan_destroy(p);
+        return CS_ENOMEM;
+      }
+      cudaMemcpy(p->fft4_tw, t4.data(), t4.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    }
     if (tapers) cudaMemcpy(p->taper, tapers, (size_t)L * p->T_eff * sizeof(double), cudaMemcpyHostToDevice);
   }
   cudaMemset(p->X64, 0, ring * sizeof(double2));
@@ -280,7 +302,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
 int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   DeviceGuard g(p->device);
-  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
+  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->fft4_tw); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
   if (p->tc_ops) cudaFree(p->tc_ops);
   for (auto& e : p->tc_tiles)
     if (e.ptr) cudaFree(e.ptr);

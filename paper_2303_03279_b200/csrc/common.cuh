@@ -25,6 +25,7 @@ struct Plan {
   double* taper = nullptr;       // [L][T_eff] tapers (null: rectangular)        -- FFT path
   double2* fft_tw = nullptr;     // [nfft/4] e^{-2 pi i j / (nfft/2)}             -- FFT path
   double2* post_tw = nullptr;    // [nfft/2 + 1] e^{-2 pi i k / nfft}            -- FFT path
+  double2* fft4_tw = nullptr;    // [A][32] W_M^{b k_a}, then [32] W_32^j       -- four-step FFT (M = 32 A)
   bool use_fft = false;          // power-of-two nfft and a band wide enough to prefer the FFT
   double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
   float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra

@@ -26,6 +26,11 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
+template <typename T>
+__device__ __forceinline__ void cp_async4_any(T* smem, const T* gmem) {  // one element
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(sizeof(T)));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
@@ -457,9 +462,244 @@ k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Four-step register FFT for M = nfft/2 = 32 A complex points (A = 8, 16), one
+// warp per (node, trial), all tapers.  The real signal is packed as
+// z_q = v_2q + i v_2q+1 (M-point complex FFT + real split).  With q = 32 a + b:
+//   Z[k_a + A k_b] = sum_b W_32^{b k_b} W_M^{b k_a} sum_a z[32 a + b] W_A^{a k_a}
+// step 1: lane b runs the A-point DFT over a in registers; step 2: twiddle
+// W_M^{b k_a} (table [k_a][b], conflict-free); step 3: one shared-memory
+// transpose gives lane (k_a, h) the b = h + R m, m < A (R = 32/A), an A-point
+// register DFT over m, twiddle W_32^{h k'} and an R-point DFT across the R lanes
+// by shuffles.  Shared memory is touched twice per element (no per-stage
+// exchanges), butterflies stay in registers: FP64-pipe bound.
+constexpr int kFft4Warps = 4;
+
+__constant__ double2 c_w16[16] = {
+    {1.0, 0.0},
+    {0.92387953251128675613, -0.38268343236508977173},
+    {0.70710678118654752440, -0.70710678118654752440},
+    {0.38268343236508977173, -0.92387953251128675613},
+    {0.0, -1.0},
+    {-0.38268343236508977173, -0.92387953251128675613},
+    {-0.70710678118654752440, -0.70710678118654752440},
+    {-0.92387953251128675613, -0.38268343236508977173},
+    {-1.0, 0.0},
+    {-0.92387953251128675613, 0.38268343236508977173},
+    {-0.70710678118654752440, 0.70710678118654752440},
+    {-0.38268343236508977173, 0.92387953251128675613},
+    {0.0, 1.0},
+    {0.38268343236508977173, 0.92387953251128675613},
+    {0.70710678118654752440, 0.70710678118654752440},
+    {0.92387953251128675613, 0.38268343236508977173}};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
+  return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+}
+__host__ __device__ constexpr int brev_c(int i, int lg) {
+  int r = 0;
+  for (int k = 0; k < lg; ++k) r |= ((i >> k) & 1) << (lg - 1 - k);
+  return r;
+}
+// in-register A-point DFT (natural order in and out), radix-2 DIT
+template <int A>
+__device__ __forceinline__ void dft_reg(double2 (&v)[A]) {
+  constexpr int LG = A == 16 ? 4 : (A == 8 ? 3 : (A == 4 ? 2 : 1));
+  double2 t[A];
+#pragma unroll
+  for (int i = 0; i < A; ++i) t[i] = v[brev_c(i, LG)];
+#pragma unroll
+  for (int s = 1; s < A; s <<= 1)
+#pragma unroll
+    for (int k = 0; k < A; k += 2 * s)
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const int wi = j * (16 / (2 * s));  // W_{2s}^j = W_16^{16 j / 2s}
+        double2 b = t[k + j + s];
+        if (wi == 4) b = make_double2(b.y, -b.x);
+        else if (wi != 0) b = cmul(b, c_w16[wi]);
+        const double2 a = t[k + j];
+        t[k + j] = make_double2(a.x + b.x, a.y + b.y);
+        t[k + j + s] = make_double2(a.x - b.x, a.y - b.y);
+      }
+#pragma unroll
+  for (int i = 0; i < A; ++i) v[i] = t[i];
+}
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+template <typename Tin, int A>
+__global__ void __launch_bounds__(kFft4Warps * 32, 4)
+k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N, int T_eff, int lo,
+               int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw4,
+               const double2* __restrict__ post_tw, const double2* __restrict__ wsum, int slot0, int slot_cap,
+               double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local, int nyq_local,
+               int n_trials, int vec16) {
+  constexpr int R = 32 / A, M = 32 * A, S = 32 + R, PAD = 8 / R;
+  constexpr int BUF = (A * S > M + PAD * R) ? A * S : M + PAD * R;
+  extern __shared__ double2 f4_smem[];
+  double2* tabM = f4_smem;        // [A][32]  W_M^{b k_a}
+  double2* w32 = tabM + A * 32;   // [32]     W_32^j
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < A * 32 + 32; j += blockDim.x) f4_smem[j] = tw4[j];
+  __syncthreads();
+  double2* buf = w32 + 32 + kFft4Warps * BUF * 0 + warp * BUF;
+  // per-warp sample staging (cp.async): the next signal streams in while this one transforms
+  Tin* stage = (Tin*)(w32 + 32 + kFft4Warps * BUF) + warp * (32 * A * 2);
+  const int ka2 = lane / R, h = lane % R;
+  const int j_out = R == 4 ? (((h & 1) << 1) | (h >> 1)) : h;  // R-point DIF output order
+  const int64_t n_sig = (int64_t)N * n_trials;
+  const int64_t gw = (int64_t)blockIdx.x * kFft4Warps + warp, nw = (int64_t)gridDim.x * kFft4Warps;
+  constexpr int V = 16 / sizeof(Tin);  // elements per 16-byte copy
+  auto prefetch = [&](int64_t sig) {
+    if (sig < n_sig) {
+      const int n = (int)(sig % N), k = (int)(sig / N);
+      const Tin* xr = x + (int64_t)k * trial_stride + (int64_t)n * node_stride;
+      if (vec16) {
+        for (int e = lane * V; e < T_eff; e += 32 * V) cp_async16(stage + e, xr + e, 16);
+      } else {
+        for (int e = lane; e < T_eff; e += 32) cp_async4_any(stage + e, xr + e);
+      }
+    }
+    cp_async_commit();
+  };
+  prefetch(gw);
+  for (int64_t sig = gw; sig < n_sig; sig += nw) {
+    const int n = (int)(sig % N), k = (int)(sig / N);
+    const int slot = (slot0 + k) % slot_cap;
+    cp_async_wait0();
+    __syncwarp();
+    // d_t = x_t - c (c = first sample, exact for fp32 input); the mean is removed after
+    // the transform by linearity: X_b = FFT(d w)_b - mean(d) W_b, W_b = sum_t w_t e_bt
+    // (plan table wsum)
+    const double c = (double)stage[0];
+    double mean_d = 0.0;
+    for (int l = 0; l < L; ++l) {
+      const double* w = taper ? taper + (int64_t)l * T_eff : nullptr;
+      double2 v[A];
+      double sum = 0.0;
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const int t0 = 2 * (32 * a + lane);
+        const double d0 = t0 < T_eff ? (double)stage[t0] - c : 0.0;
+        const double d1 = t0 + 1 < T_eff ? (double)stage[t0 + 1] - c : 0.0;
+        sum += d0 + d1;
+        v[a] = w ? make_double2(d0 * (t0 < T_eff ? w[t0] : 0.0), d1 * (t0 + 1 < T_eff ? w[t0 + 1] : 0.0))
+                 : make_double2(d0, d1);
+      }
+      if (l == L - 1) {  // samples are in registers: stream the next signal in
+        __syncwarp();
+        prefetch(sig + nw);
+      }
+      if (l == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        mean_d = sum / (double)T_eff;
+      }
+      dft_reg<A>(v);                       // over a -> k_a
+#pragma unroll
+      for (int ka = 1; ka < A; ++ka) v[ka] = cmul(v[ka], tabM[ka * 32 + lane]);
+#pragma unroll
+      for (int ka = 0; ka < A; ++ka) buf[ka * S + lane] = v[ka];
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < A; ++m) v[m] = buf[ka2 * S + h + R * m];
+      __syncwarp();
+      dft_reg<A>(v);                       // over m -> k'
+#pragma unroll
+      for (int kp = 1; kp < A; ++kp) v[kp] = cmul(v[kp], w32[(h * kp) & 31]);
+      if (R == 2) {
+#pragma unroll
+        for (int kp = 0; kp < A; ++kp) {
+          const double2 o = shfl_xor2(v[kp], 1);
+          v[kp] = h == 0 ? make_double2(v[kp].x + o.x, v[kp].y + o.y) : make_double2(o.x - v[kp].x, o.y - v[kp].y);
+        }
+      } else {  // R == 4: two radix-2 DIF stages across lanes h ^ 2, h ^ 1
+#pragma unroll
+        for (int kp = 0; kp < A; ++kp) {
+          const double2 o = shfl_xor2(v[kp], 2);
+          if (h < 2) {
+            v[kp] = make_double2(v[kp].x + o.x, v[kp].y + o.y);
+          } else {
+            const double2 d = make_double2(o.x - v[kp].x, o.y - v[kp].y);
+            v[kp] = h == 3 ? make_double2(d.y, -d.x) : d;
+          }
+        }
+#pragma unroll
+        for (int kp = 0; kp < A; ++kp) {
+          const double2 o = shfl_xor2(v[kp], 1);
+          v[kp] = (h & 1) == 0 ? make_double2(v[kp].x + o.x, v[kp].y + o.y)
+                               : make_double2(o.x - v[kp].x, o.y - v[kp].y);
+        }
+      }
+      // Z[k], k = k_a + A k' + A^2 j, stored at k + PAD j (conflict-free)
+#pragma unroll
+      for (int kp = 0; kp < A; ++kp) buf[ka2 + A * kp + (A * A + PAD) * j_out] = v[kp];
+      __syncwarp();
+      for (int b = lane; b < nb; b += 32) {
+        const int kk = lo + b;
+        const int k1 = kk == M ? 0 : kk, k2 = (M - kk) & (M - 1);
+        const double2 zk = buf[k1 + PAD * (k1 / (A * A))];
+        const double2 zm = buf[k2 + PAD * (k2 / (A * A))];
+        const double er = 0.5 * (zk.x + zm.x), ei = 0.5 * (zk.y - zm.y);
+        const double dr = 0.5 * (zk.x - zm.x), di = 0.5 * (zk.y + zm.y);
+        const double2 wk = post_tw[kk];
+        const double orr = di, oi = -dr;
+        const double2 ws = wsum[l * nb + b];
+        double re = er + (wk.x * orr - wk.y * oi) - mean_d * ws.x;
+        double im = ei + (wk.x * oi + wk.y * orr) - mean_d * ws.y;
+        if (b == dc_local) re = im = 0.0;
+        if (b == nyq_local) im = 0.0;
+        const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * N + n;
+        X64[o] = make_double2(re, im);
+        X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+      }
+      __syncwarp();
+    }
+  }
+  cp_async_wait0();
+}
+
+template <typename Tin, int A>
+void launch_fft4(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0, int kc, cudaStream_t st) {
+  constexpr int R = 32 / A, M = 32 * A, S = 32 + R, PAD = 8 / R;
+  constexpr int BUF = (A * S > M + PAD * R) ? A * S : M + PAD * R;
+  const size_t smem = (size_t)(A * 32 + 32 + kFft4Warps * BUF) * sizeof(double2) +
+                      (size_t)kFft4Warps * 64 * A * sizeof(Tin);
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    cudaFuncSetAttribute(k_spectra_fft4<Tin, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_spectra_fft4<Tin, A>, kFft4Warps * 32, smem);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+  const int64_t sigs = (int64_t)p.N * kc;
+  int64_t grid = (int64_t)nsm * ctas_per_sm;
+  const int64_t need = (sigs + kFft4Warps - 1) / kFft4Warps;
+  if (grid > need) grid = need;
+  // 16-byte staging copies when every row start and the row length allow it
+  const int vec16 = ((uintptr_t)x % 16 == 0) && ((ts * (int64_t)sizeof(Tin)) % 16 == 0) &&
+                    ((ns * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.T_eff * (int)sizeof(Tin)) % 16 == 0);
+  k_spectra_fft4<Tin, A><<<(unsigned)grid, kFft4Warps * 32, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff,
+      p.lo, p.nb, p.L, p.taper, p.fft4_tw, p.post_tw, p.wsum, slot0, p.slot_cap, p.X64, p.X32, p.scale,
+      p.dc_local, p.nyq_local, kc, vec16);
+}
+
 bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0, int kc,
                      cudaStream_t st) {
   const int M = p.nfft / 2;
+  if (p.fft4_tw && (M == 256 || M == 512)) {  // four-step register FFT
+    if (dtype == CS_F64) {
+      if (M == 256) launch_fft4<double, 8>(p, x, ts, ns, slot0, kc, st);
+      else launch_fft4<double, 16>(p, x, ts, ns, slot0, kc, st);
+    } else {
+      if (M == 256) launch_fft4<float, 8>(p, x, ts, ns, slot0, kc, st);
+      else launch_fft4<float, 16>(p, x, ts, ns, slot0, kc, st);
+    }
+    return true;
+  }
   int log2M = 0;
   while ((1 << log2M) < M) ++log2M;
   const size_t smem = (size_t)(kFftWarps * M + M / 2) * sizeof(double2);
