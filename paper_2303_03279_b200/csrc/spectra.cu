@@ -39,20 +39,30 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 // exact in fp64 for fp32 input) the demeaned, tapered DFT is
 //   X_b = sum_t (d_t - mean(d)) w_t e_bt = Y_b - mean(d) W_b,  Y_b = sum_t d_t tww_bt,
 // W_b = sum_t tww_bt (host, long double), so the mean never needs a second read.
-template <typename Tin, int NBT>
+// NS signals per thread share every broadcast twiddle load (NS = 2 for <= 8 bins:
+// 24 DFMA per 6 LDS.128 instead of 12).
+template <typename Tin, int NBT, int NS>
+struct SpecShape {
+  static constexpr int ROWS = kSpecNodes * NS;                       // nodes per CTA
+  static constexpr int TC = (NS == 1 ? kSpecRowBytes : kSpecRowBytes / 2) / (int)sizeof(Tin);  // samples per chunk
+  static constexpr int RS = TC + 16 / (int)sizeof(Tin);             // padded row stride (conflict-free LDS.128)
+  static constexpr size_t SMEM = 2 * (size_t)ROWS * RS * sizeof(Tin) + 2 * (size_t)NBT * TC * sizeof(double2);
+};
+
+template <typename Tin, int NBT, int NS>
 __global__ void __launch_bounds__(kSpecNodes)
 k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N,
           int T_eff, int nb, int L, const double2* __restrict__ tww, const double2* __restrict__ wsum,
           int slot0, int slot_cap, double2* __restrict__ X64, float2* __restrict__ X32, float scale,
           int dc_local, int nyq_local, int vec16) {
-  constexpr int TC = kSpecRowBytes / sizeof(Tin);            // samples per chunk
-  constexpr int RS = TC + 16 / sizeof(Tin);                   // padded row stride (conflict-free LDS.128)
+  using Sh = SpecShape<Tin, NBT, NS>;
+  constexpr int ROWS = Sh::ROWS, TC = Sh::TC, RS = Sh::RS;
   extern __shared__ __align__(16) unsigned char spec_smem[];
-  Tin* sx = (Tin*)spec_smem;                                  // [2][128][RS]
-  double2* stw = (double2*)(spec_smem + 2 * kSpecNodes * RS * sizeof(Tin));  // [2][NBT][TC]
+  Tin* sx = (Tin*)spec_smem;                                  // [2][ROWS][RS]
+  double2* stw = (double2*)(spec_smem + 2 * ROWS * RS * sizeof(Tin));  // [2][NBT][TC]
 
   const int tid = threadIdx.x;
-  const int n0 = blockIdx.x * kSpecNodes;
+  const int n0 = blockIdx.x * ROWS;
   const int b0 = blockIdx.y * NBT;
   const int k = blockIdx.z / L;
   const int l = blockIdx.z % L;
@@ -63,12 +73,12 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
 
   auto issue = [&](int ch, int buf) {
     const int t0 = ch * TC;
-    Tin* dst = sx + buf * kSpecNodes * RS;
+    Tin* dst = sx + buf * ROWS * RS;
     if (vec16) {
-      constexpr int PER_ROW = kSpecRowBytes / 16;   // 16-byte pieces per row
-      constexpr int EPP = 16 / sizeof(Tin);         // elements per piece
+      constexpr int EPP = 16 / sizeof(Tin);         // elements per 16-byte piece
+      constexpr int PER_ROW = TC / EPP;             // pieces per row
 #pragma unroll 4
-      for (int q = 0; q < PER_ROW; ++q) {
+      for (int q = 0; q < PER_ROW * NS; ++q) {
         const int e = tid + kSpecNodes * q;
         const int row = e / PER_ROW, piece = e % PER_ROW;
         const int n = n0 + row, t = t0 + piece * EPP;
@@ -78,7 +88,7 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
         cp_async16(dst + row * RS + piece * EPP, src, bytes);
       }
     } else {
-      for (int q = 0; q < TC; ++q) {
+      for (int q = 0; q < TC * NS; ++q) {
         const int e = tid + kSpecNodes * q;
         const int row = e / TC, col = e % TC;
         const int n = n0 + row, t = t0 + col;
@@ -101,10 +111,14 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
     cp_async_commit();
   };
 
-  double are[NBT], aim[NBT];
+  double are[NS][NBT], aim[NS][NBT];
 #pragma unroll
-  for (int j = 0; j < NBT; ++j) are[j] = aim[j] = 0.0;
-  double c = 0.0, sum = 0.0;
+  for (int q = 0; q < NS; ++q)
+#pragma unroll
+    for (int j = 0; j < NBT; ++j) are[q][j] = aim[q][j] = 0.0;
+  double c[NS], sum[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) c[q] = sum[q] = 0.0;
 
   issue(0, 0);
   for (int ch = 0; ch < n_chunk; ++ch) {
@@ -116,79 +130,99 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
       cp_async_wait0();
     }
     __syncthreads();
-    const Tin* row = sx + buf * kSpecNodes * RS + tid * RS;
+    const Tin* rows = sx + buf * ROWS * RS;
     const double2* tw = stw + buf * NBT * TC;
-    if (ch == 0) c = (double)row[0];
-    const int tn = min(TC, T_eff - ch * TC);
-    double csum = 0.0;
-    if (tn == TC) {
-#pragma unroll 2
-      for (int t = 0; t < TC; t += 16 / (int)sizeof(Tin)) {
-        Tin v[16 / sizeof(Tin)];
-        *(float4*)v = *(const float4*)(row + t);
+    if (ch == 0) {
 #pragma unroll
-        for (int u = 0; u < (int)(16 / sizeof(Tin)); ++u) {
-          const double d = (double)v[u] - c;
-          csum += d;
+      for (int q = 0; q < NS; ++q) c[q] = (double)rows[(tid + kSpecNodes * q) * RS];
+    }
+    const int tn = min(TC, T_eff - ch * TC);
+    if (tn == TC) {
+      constexpr int VE = 16 / sizeof(Tin);
+#pragma unroll 2
+      for (int t = 0; t < TC; t += VE) {
+        Tin v[NS][VE];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) *(float4*)v[q] = *(const float4*)(rows + (tid + kSpecNodes * q) * RS + t);
+#pragma unroll
+        for (int u = 0; u < VE; ++u) {
+          double d[NS];
+#pragma unroll
+          for (int q = 0; q < NS; ++q) {
+            d[q] = (double)v[q][u] - c[q];
+            sum[q] += d[q];
+          }
 #pragma unroll
           for (int j = 0; j < NBT; ++j) {
             const double2 w = tw[j * TC + t + u];
-            are[j] = fma(d, w.x, are[j]);
-            aim[j] = fma(d, w.y, aim[j]);
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+              are[q][j] = fma(d[q], w.x, are[q][j]);
+              aim[q][j] = fma(d[q], w.y, aim[q][j]);
+            }
           }
         }
       }
     } else {
       for (int t = 0; t < tn; ++t) {
-        const double d = (double)row[t] - c;
-        csum += d;
+        double d[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          d[q] = (double)rows[(tid + kSpecNodes * q) * RS + t] - c[q];
+          sum[q] += d[q];
+        }
 #pragma unroll
         for (int j = 0; j < NBT; ++j) {
           const double2 w = tw[j * TC + t];
-          are[j] = fma(d, w.x, are[j]);
-          aim[j] = fma(d, w.y, aim[j]);
+#pragma unroll
+          for (int q = 0; q < NS; ++q) {
+            are[q][j] = fma(d[q], w.x, are[q][j]);
+            aim[q][j] = fma(d[q], w.y, aim[q][j]);
+          }
         }
       }
     }
-    sum += csum;
     __syncthreads();
   }
 
-  const int n = n0 + tid;
-  if (n >= N) return;
-  const double mean = sum / (double)T_eff;
   const int slot = (slot0 + k) % slot_cap;
 #pragma unroll
-  for (int j = 0; j < NBT; ++j) {
-    if (j >= nbt) break;
-    const int b = b0 + j;
-    const double2 W = wsum[(int64_t)l * nb + b];
-    double re = fma(-mean, W.x, are[j]), im = fma(-mean, W.y, aim[j]);
-    if (b == dc_local) re = im = 0.0;       // spectral.py:96: DC is exactly zero
-    if (b == nyq_local) im = 0.0;           // Nyquist of a real signal is real
-    const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
-    X64[o] = make_double2(re, im);
-    X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+  for (int q = 0; q < NS; ++q) {
+    const int n = n0 + tid + kSpecNodes * q;
+    if (n >= N) continue;
+    const double mean = sum[q] / (double)T_eff;
+#pragma unroll
+    for (int j = 0; j < NBT; ++j) {
+      if (j >= nbt) break;
+      const int b = b0 + j;
+      const double2 W = wsum[(int64_t)l * nb + b];
+      double re = fma(-mean, W.x, are[q][j]), im = fma(-mean, W.y, aim[q][j]);
+      if (b == dc_local) re = im = 0.0;       // spectral.py:96: DC is exactly zero
+      if (b == nyq_local) im = 0.0;           // Nyquist of a real signal is real
+      const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
+      X64[o] = make_double2(re, im);
+      X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
+    }
   }
 }
 
 template <typename Tin, int NBT>
 static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0,
                            int kc, cudaStream_t st) {
-  constexpr int TC = kSpecRowBytes / sizeof(Tin);
-  constexpr int RS = TC + 16 / sizeof(Tin);
-  const size_t smem = 2 * kSpecNodes * RS * sizeof(Tin) + 2 * NBT * TC * sizeof(double2);
+  constexpr int NS = NBT <= 8 ? 2 : 1;
+  using Sh = SpecShape<Tin, NBT, NS>;
+  const size_t smem = Sh::SMEM;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_spectra<Tin, NBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_spectra<Tin, NBT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   const int vec16 = ((uintptr_t)x % 16 == 0) && ((ns * (int64_t)sizeof(Tin)) % 16 == 0) &&
                     ((ts * (int64_t)sizeof(Tin)) % 16 == 0);
-  dim3 grid((p.N + kSpecNodes - 1) / kSpecNodes, (p.nb + NBT - 1) / NBT, kc * p.L);
-  k_spectra<Tin, NBT><<<grid, kSpecNodes, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
-                                                       p.L, p.tww, p.wsum, slot0, p.slot_cap, p.X64,
-                                                       p.X32, p.scale, p.dc_local, p.nyq_local, vec16);
+  dim3 grid((p.N + Sh::ROWS - 1) / Sh::ROWS, (p.nb + NBT - 1) / NBT, kc * p.L);
+  k_spectra<Tin, NBT, NS><<<grid, kSpecNodes, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
+                                                           p.L, p.tww, p.wsum, slot0, p.slot_cap, p.X64,
+                                                           p.X32, p.scale, p.dc_local, p.nyq_local, vec16);
 }
 
 template <typename Tin>
