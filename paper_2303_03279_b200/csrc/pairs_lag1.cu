@@ -217,9 +217,11 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
             if (PLVK) {  // unit phasor of the trial's taper-mean CSD
               f2 re;
               asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(re) : "l"(re1), "l"(re2));
+              // |CSD|^2 clamped to FLT_MIN: a zero CSD (dead node) then adds 0 * 2^63 = 0,
+              // and the MUFU needs no denormal fix-up (scaled spectra are O(1))
               const f2 m2 = ffma2(tt, tt, fmul2(re, re));
-              const float ml = lo_of(m2), mh = hi_of(m2);
-              const f2 rs = pk(ml > 0.f ? rsqrtf(ml) : 0.f, mh > 0.f ? rsqrtf(mh) : 0.f);
+              const float ml = fmaxf(lo_of(m2), 1.17549435e-38f), mh = fmaxf(hi_of(m2), 1.17549435e-38f);
+              const f2 rs = pk(rsqrt_approx(ml), rsqrt_approx(mh));
               pvr[p] = ffma2(re, rs, pvr[p]);
               pvi[p] = ffma2(tt, rs, pvi[p]);
             }
