@@ -47,6 +47,18 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def _ncu_traffic(cfg: int, kernel, ws: int):
+    """dram bytes per launch of ``kernel`` at config ``cfg`` from the committed ncu capture
+    (profiles/ncu_traffic.json, written from an `ncu --set full` run of this bench)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if kernel is None or ws != 1 or not p.exists():
+        return None
+    for e in json.loads(p.read_text()).get("entries", []):
+        if e.get("config") == cfg and kernel.startswith(e.get("kernel", "?")):
+            return e
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -154,7 +166,7 @@ def run_reference(args, c, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_sub = args.cpu_nodes
+    n_sub = args.cpu_nodes if args.cpu_nodes else 512  # ~1.8 s per step: the whole run stays within minutes
     samples = []
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(c, n_sub, threads)
@@ -245,10 +257,12 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--metrics", default=None, help="comma list (default: the config's metrics)")
-    ap.add_argument("--cpu-nodes", type=int, default=768, help="node subset for the CPU baseline")
+    ap.add_argument("--cpu-nodes", type=int, default=None,
+                    help="node subset for the CPU baseline (default 768; 512 per step for --impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--no-per-metric", action="store_true", help="skip the one-metric-at-a-time runs")
     args = ap.parse_args()
 
     from paper_2303_03279_b200 import synth
@@ -353,7 +367,64 @@ def main():
         roof = {"kernel": "k_spectra", "bound": "fp64", "achieved": flop_dfma / (k1_ms * 1e-3) / 1e12,
                 "peak": fp64_fma / 1e12, "unit": "T DFMA/s", "frac": flop_dfma / (k1_ms * 1e-3) / fp64_fma,
                 "traffic": None, "hbm_frac": bytes_ / (k1_ms * 1e-3) / (peaks["hbm_gbs"] * 1e9)}
+    # dram traffic per launch of the dominant kernel from the committed ncu --set full capture
+    tr = _ncu_traffic(c.cfg, roof["kernel"] if roof else None, ws)
+    if roof is not None:
+        roof["traffic"] = tr["bytes_per_launch"] if tr else None
+        if tr:
+            roof["traffic_source"] = tr["source"]
+    # K2 (tensor cores): SURVEY 8(d) roofline = max(3 x flops / bf16 sustained, output bytes / HBM)
+    roof_k2 = None
+    tc_ms = per.get("pairs_tc", 0.0)
+    if tc_ms > 0:
+        L = 1 if not isinstance(c.taper, tuple) else c.taper[2]
+        P_loc = p1 - p0
+        flops = 8.0 * c.K * L * P_loc * c.n_bins + (8.0 * c.K * P_loc * c.n_bins if ("PLV" in metrics and L == 1) else 0.0)
+        n_out = sum(m in metrics for m in ("COH", "IMAGCOHY", "PLV", "COHY"))
+        out_bytes = 4.0 * n_out * P_loc * (c.n_bins + 1)
+        t_tc = 3.0 * flops / (peaks["bf16_tflops_sustained"] * 1e12)
+        t_hbm = out_bytes / (peaks["hbm_gbs"] * 1e9)
+        bound = "tensor" if t_tc >= t_hbm else "hbm"
+        roof_k2 = {"kernel": "k_pairs_tc", "bound": bound,
+                   "achieved": (3.0 * flops / (tc_ms * 1e-3) / 1e12) if bound == "tensor" else out_bytes / (tc_ms * 1e-3) / 1e9,
+                   "peak": peaks["bf16_tflops_sustained"] if bound == "tensor" else peaks["hbm_gbs"],
+                   "unit": "TFLOP/s (bf16x3-equivalent)" if bound == "tensor" else "GB/s",
+                   "frac": max(t_tc, t_hbm) / (tc_ms * 1e-3),
+                   "raw_tflops": flops / (tc_ms * 1e-3) / 1e12, "ms": tc_ms,
+                   "note": "fp16 hi/lo split = 3 products per real product; frac = roofline time / measured time"}
     breakdown = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in prof.items()}
+
+    # ---- per metric: each metric alone with K1 + only the kernel it needs ----
+    per_metric = None
+    if not args.no_per_metric and len(metrics) > 1:
+        full.set_profiling(False)
+        if local is not full:
+            local.set_profiling(False)
+        per_metric = {}
+        n_pm = max(3, min(args.steps, 10))
+        for m in metrics:
+            om = full.alloc_outputs((m,), c.n_bins, per_bin=True, band=True, pair_count=p1 - p0)
+
+            def step_m():
+                local.spectra(x, 0)
+                if ws > 1:
+                    allgather_ring(L32, F32, dist, g32)
+                    allgather_ring(L64, F64, dist, g64)
+                full.pair_metrics(slots, (m,), 0, c.n_bins, outputs=om, row_tiles=(rb, re), pair_base=p0,
+                                  pair_count=p1 - p0)
+            for _ in range(2):
+                step_m()
+            barrier()
+            e0.record()
+            for _ in range(n_pm):
+                step_m()
+            e1.record()
+            barrier()
+            tm = torch.tensor([e0.elapsed_time(e1) / n_pm], device=dev)
+            if dist is not None:
+                dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            per_metric[m] = {"updates_per_s": c.updates / (float(tm) * 1e-3), "ms_per_step": float(tm)}
+            del om
 
     line = {
         "metric": f"edge*freq*trial updates/s (config {c.cfg}, {len(metrics)} metrics fused)",
@@ -365,7 +436,7 @@ def main():
                    "outputs": "per-bin [nb,P] + band-mean [P] per metric", "parallelism": f"pair-row-tiles x{ws}",
                    "l2": "inputs 4.1 GB > 126 MB L2 (no flush needed)" if c.cfg == 5 else "inputs > L2" ,
                    "updates_per_step": c.updates},
-        "roofline": roof, "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
+        "roofline": roof, "roofline_k2": roof_k2, "per_metric": per_metric, "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
         "gpu_launches": launches, "clocks": clk.summary(),
         "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma, "hbm_gbs": peaks["hbm_gbs"],
                   "hbm_source": peak_kind},
@@ -433,9 +504,10 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        r = cpu_baseline(c, args.cpu_nodes, os.cpu_count() or 1)
+        n_cpu = args.cpu_nodes or 768
+        r = cpu_baseline(c, n_cpu, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": r["updates"] / r["s"], "unit": "updates/s", "cores": 1, "kind": "port",
-                                "sample": f"node subset N'={args.cpu_nodes} of cfg{c.cfg}, all K={c.K}, {c.n_bins} bins, "
+                                "sample": f"node subset N'={n_cpu} of cfg{c.cfg}, all K={c.K}, {c.n_bins} bins, "
                                           f"{len(c.metrics)} finalizers; fold single-threaded as in the reference "
                                           f"(FFT pool of {os.cpu_count()} threads)",
                                 "breakdown_s": {k: r[k] for k in ("fft_s", "fold_s", "finalize_s")}}

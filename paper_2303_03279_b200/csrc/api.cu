@@ -354,10 +354,14 @@ int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_
     cs::PhaseMark ph(*p, "node_stats", st);
     cs::run_node_stats(*p, slots, K, bin_lo, nbb, st);
   }
-  // the tensor-core family runs first: with COH requested it also produces IMAGCOHY,
-  // whose per-bin values the phase-lag kernel reads back for WPLI
-  if (cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
-  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, out, st) < 0) return CS_EPARAM;
+  // only the requested metrics' buffers are ever written
+  cs_outputs o = *out;
+  for (int m = 0; m < CS_NUM_METRICS; ++m)
+    if (!(mask & (1u << m))) o.bins[m] = o.band[m] = nullptr;
+  // tensor-core family (COHY, COH, PLV; IMAGCOHY when no sign-based metric is asked),
+  // then the phase-lag family
+  if (cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st) < 0) return CS_EPARAM;
+  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st) < 0) return CS_EPARAM;
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_metrics");
   return CS_OK;
 }

@@ -188,8 +188,19 @@ static const unsigned kLagBits[5] = {CS_IMAGCOHY, CS_PLI, CS_USPLI, CS_WPLI, CS_
 
 static const int kLagIdx[5] = {2, 4, 5, 6, 7};
 
+// IMAGCOHY without any sign-based metric: D_im of the tensor-core pass already is
+// sum Im(X_i conj X_j) (fp16 hi/lo products, ~1e-6 relative), so the phase-lag
+// kernel is not launched for it.  With PLI/USPLI/WPLI/DSWPLI requested the
+// phase-lag kernel accumulates sum Im anyway and IMAGCOHY stays there.
+// (Not with COHY requested: the near-zero IMAGCOHY entries are zeroed in the
+// tensor-core epilogue for the fp64 fallback, which would corrupt COHY's Im.)
+static bool imag_on_tensor_cores(unsigned mask) {
+  return (mask & CS_IMAGCOHY) && !(mask & (CS_PLI | CS_USPLI | CS_WPLI | CS_DSWPLI | CS_COHY));
+}
+
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
+  if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
   unsigned any = 0;
   for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
   const bool plvk = p.L > 1 && (mask & CS_PLV);
@@ -250,11 +261,30 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
 
 int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
-  const bool do_x = (mask & (CS_COHY | CS_COH)) != 0;
+  const bool do_imag = imag_on_tensor_cores(mask);
+  const bool do_x = (mask & (CS_COHY | CS_COH)) != 0 || do_imag;
   const bool do_u = (mask & CS_PLV) != 0 && p.L == 1;  // multitaper PLV runs in the lag kernel
   if (!do_x && !do_u) return 0;
-  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, false, out, p.nscale, st))
+  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, do_imag, out, p.nscale, st))
     return -1;
+  if (do_imag && (out->bins[2] || out->band[2])) {  // fp64 values for the near-zero IMAGCOHY entries
+    LagArgs a{};
+    a.X64 = p.X64;
+    a.N = p.N; a.nb = p.nb; a.L = p.L;
+    a.slots = slots; a.K = K;
+    a.bin_lo = bin_lo; a.nbb = nbb;
+    a.psd = p.psd;
+    a.pair_base = out->pair_base;
+    a.pair_stride = out->pair_stride;
+    a.bins[0] = (float*)out->bins[2];
+    a.band[0] = (float*)out->band[2];
+    a.scale2 = p.scale * p.scale;
+    a.flags = p.flags;
+    a.counters = p.counters;
+    a.flag_cap = p.flag_cap;
+    PhaseMark ph(p, "lag_fallback", st);
+    k_lag_fallback<<<148 * 4, 256, 0, st>>>(a);
+  }
   return 0;  // launches are counted by the phase marks
 }
 

@@ -71,6 +71,13 @@ struct TcArgs {
   float* plv_bins;  float* plv_band;
   float* imag_bins; float* imag_band;   // IMAGCOHY from D_im (the phase-lag kernel then reads it for WPLI)
   int do_x, do_u;
+  // IMAGCOHY produced here (no sign-based metric asked): entries with |IMAG| < imag_tau
+  // (above the tensor-core error bound) go to the fp64 fallback list, so values that
+  // are exactly 0 in the reference (zero-lag copies) come out exact, not ~1e-9
+  int4* flags;
+  int* counters;
+  int flag_cap;
+  float imag_tau;
   int dbg;   // ablation bits (builds with -DCS_TC_ABLATION only): 1 per-bin stores, 2 TMEM-phase
              // math, 4 band phase, 8 MMAs, 16 TMA loads are skipped (timing experiments)
 };
@@ -347,6 +354,21 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               for (int u = 0; u < 4; ++u) {
                 vr[u4 + u] *= rs[u];
                 vi[u4 + u] *= rs[u];
+              }
+              if (a.flags) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int j = jBase + c0 + u4 + u;
+                  if (rs[u] > 0.f && i < j && j < a.N && i >= a.i_lo && i < a.i_hi &&
+                      fabsf(vi[u4 + u]) < a.imag_tau) {
+                    const int slot = atomicAdd(&a.counters[0], 1);
+                    if (slot < a.flag_cap)
+                      a.flags[slot] = make_int4(i, j, bl, 0);
+                    else
+                      a.counters[1] = 1;
+                    vi[u4 + u] = 0.f;  // out of the band sum; the fallback adds the fp64 value
+                  }
+                }
               }
             }
             if (a.coh_band || !cohy) {
@@ -653,6 +675,13 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.imag_bins = do_imag ? (float*)out->bins[2] : nullptr;
   a.imag_band = do_imag ? (float*)out->band[2] : nullptr;
   a.do_x = do_x; a.do_u = do_u;
+  if (do_imag && (a.imag_bins || a.imag_band)) {
+    a.flags = p.flags;
+    a.counters = p.counters;
+    a.flag_cap = p.flag_cap;
+    a.imag_tau = 1e-5f + 6e-8f * (float)Kc;  // > fp16-split + fp32-accumulation error of D_im / norm
+    cudaMemsetAsync(p.counters, 0, 2 * sizeof(int), st);
+  }
 #ifdef CS_TC_ABLATION
   { const char* d = getenv("CSCONN_TC_DBG"); a.dbg = d ? atoi(d) : 0; }
 #endif

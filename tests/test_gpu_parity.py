@@ -42,12 +42,17 @@ CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg
          "dpss_small", "zerolag_dead", "zerolag_dead_hann", "sim2024_thresh"]
 
 
-@pytest.mark.parametrize("family", ["lag", "coherency"])
+# "imag_tc": IMAGCOHY without a sign-based metric is produced by the tensor-core kernel
+FAMILIES = {"lag": LAG, "coherency": COHF, "imag_tc": ("IMAGCOHY",), "coh_imag_tc": ("COH", "IMAGCOHY", "PLV"),
+            "cohy_imag": ("COHY", "IMAGCOHY")}
+
+
+@pytest.mark.parametrize("family", list(FAMILIES))
 @pytest.mark.parametrize("case", CASES)
 def test_metrics_match_reference(case, family):
     g = _load(case)
     K = g["epochs"].shape[0]
-    metrics = [m for m in (LAG if family == "lag" else COHF) if not (m == "USPLI" and K < 2)]
+    metrics = [m for m in FAMILIES[family] if not (m == "USPLI" and K < 2)]
     out, _ = _run(g, metrics)
     import oracle as O
     taper = g["taper"] if g["taper"].size else None
