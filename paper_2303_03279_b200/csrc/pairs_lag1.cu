@@ -297,7 +297,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
           const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
           const float plv = dead ? 0.f : sqrt_approx(pr * pr + pim * pim) * invK;
-          if (bin_mask & 32u) a.plv_bins[rowoff + j] = plv;
+          if (bin_mask & 32u) __stcs(&a.plv_bins[rowoff + j], plv);  // streaming: keep the operands in L2
           if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
           pvr[p] = pvi[p] = 0ull;
         }
@@ -305,7 +305,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
-            if (bin_mask & (1u << m)) a.bins[m][rowoff + j] = v[m];
+            if (bin_mask & (1u << m)) __stcs(&a.bins[m][rowoff + j], v[m]);
             if (band_mask & (1u << m)) bs[m * kTile * kTile] += v[m];
           }
         }
@@ -336,7 +336,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
             if (a.nbc > 1)
               atomicAdd(&dst[rowoff + j], v);  // bins split over CTAs: band zeroed by the host
             else
-              dst[rowoff + j] = v;
+              __stcs(&dst[rowoff + j], v);
           }
       }
     }

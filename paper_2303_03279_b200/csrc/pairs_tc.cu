@@ -458,16 +458,16 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               if (px) {
                 const float x0 = magx ? sqrt_approx(v0[t].x * v0[t].x + v0[t].y * v0[t].y) : v0[t].x;
                 const float x1 = magx ? sqrt_approx(v1[t].x * v1[t].x + v1[t].y * v1[t].y) : v1[t].x;
-                if (ok0) px[off] = x0;
-                if (ok1) px[off + 32] = x1;
+                if (ok0) __stcs(px + off, x0);  // streaming stores: keep the operands in L2
+                if (ok1) __stcs(px + off + 32, x1);
               }
               if (py) {
-                if (ok0) py[off] = v0[t].y;
-                if (ok1) py[off + 32] = v1[t].y;
+                if (ok0) __stcs(py + off, v0[t].y);
+                if (ok1) __stcs(py + off + 32, v1[t].y);
               }
               if (pc) {
-                if (ok0) pc[off] = v0[t];
-                if (ok1) pc[off + 32] = v1[t];
+                if (ok0) __stcs(pc + off, v0[t]);
+                if (ok1) __stcs(pc + off + 32, v1[t]);
               }
             }
           }
