@@ -117,7 +117,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       if (lane == 0)
         for (int t = 0; t < total; ++t) {
           const int s = t % k1Stages;
-          mbar_wait(&empty[s], ((t / k1Stages) & 1) ^ 1);
+          mbar_wait_backoff(&empty[s], ((t / k1Stages) & 1) ^ 1);
           const int bl = bl0 + t / n_stage, st = t % n_stage;
           const int row = (bl * a.Kp + st * kc) * L;
           mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16);
