@@ -63,6 +63,15 @@ extern "C" {
 #define CS_DSWPLI (1u << 7)
 #define CS_NUM_METRICS 8
 
+/* cs_plan_create flags */
+#define CS_PLAN_WELCH (1u << 0) /* welch mode (spectral.py:100-111, 264-283): a trial of
+                                   n_samples >= 2 nfft is cut into n_samples / nfft
+                                   non-overlapping nfft segments, each demeaned and
+                                   transformed; its CSD / PSD is the mean over segments
+                                   before the nonlinear terms.  The segments occupy the
+                                   plan's taper axis (n_tapers must be 1, tapers NULL).
+                                   Shorter trials fall back to fixed mode. */
+
 typedef struct cs_plan cs_plan;
 
 /* Output descriptor for cs_pair_metrics.  bins[m]: [nbb][pair_stride] fp32
@@ -96,7 +105,8 @@ typedef struct cs_sums {
  * reference's rectangular window (n_tapers must then be 1).  slot_capacity:
  * number of trial slots in the spectrum ring.  spectrum_scale: power of two
  * applied to the fp32 copy of the spectra (0 -> 1.0); every metric is
- * invariant to it.
+ * invariant to it.  flags: CS_PLAN_WELCH or 0 (reference: SpectrumSet(...) +
+ * accumulate_epoch(mode) of spectral.py:125-141, 264-286).
  */
 int cs_plan_create(cs_plan** plan, int device, int n_nodes, int n_samples, int nfft,
                    int lo_bin, int hi_bin, int n_tapers, const double* tapers,
@@ -132,6 +142,12 @@ int cs_get_spectra(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo,
  * for accumulate_spectra(acc, spectra) (spectral.py:244-261). */
 int cs_put_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, int n_bins, int slot0,
                    void* stream);
+/* Same, into taper (or welch segment) index `taper` of each slot; with weight w
+ * applied to the stored values (a welch trial of S segments is stored with
+ * w = 1/sqrt(S), so that its summed CSD is the segment mean of
+ * spectral.py:272-283 even when trials of different S share one ring). */
+int cs_put_taper_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, int n_bins, int slot0,
+                         int taper, double w, void* stream);
 
 /* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
  * range of shard `shard` of `n_shards` (balanced by tile count) and the

@@ -240,19 +240,30 @@ def band_reduce(metric: str, per_bin: np.ndarray):
 # --------------------------------------------------------------------------
 # whole-path driver
 # --------------------------------------------------------------------------
-def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None, method: str = "fft"):
+def segments(ep: np.ndarray, nfft: int) -> list:
+    """Welch mode (spectral.py:100-111): consecutive non-overlapping nfft segments."""
+    n_seg = max(1, ep.shape[1] // nfft)
+    return [ep[:, s * nfft:(s + 1) * nfft] for s in range(n_seg)]
+
+
+def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None, method: str = "fft",
+            mode: str = "fixed"):
     """All requested metrics for trials ``epochs`` (list/array of [C, T]) over the
     inclusive bin range [lo, hi].
 
     ``taper``: None (reference rectangular), a 1-D taper, or a 2-D [L, T_eff]
-    DPSS stack (multitaper extension).
+    DPSS stack (multitaper extension).  ``mode="welch"``: trials with
+    T >= 2 nfft fold the segment-mean CSD / PSD (spectral.py:264-283).
     Returns {metric: {"bins": [P, nb], "band": [P], "cband": complex [P] | None}}.
     """
     epochs = [np.asarray(e, dtype=np.float64) for e in epochs]
     C = epochs[0].shape[0]
     acc = Sums(C, hi - lo + 1)
     for ep in epochs:
-        if taper is not None and np.ndim(taper) == 2:
+        if mode == "welch" and ep.shape[1] >= 2 * nfft:
+            spec_l = np.stack([trial_spectra(sg, nfft, None, method)[:, lo:hi + 1] for sg in segments(ep, nfft)])
+            accumulate_multitaper(acc, spec_l)
+        elif taper is not None and np.ndim(taper) == 2:
             spec_l = np.stack([trial_spectra(ep, nfft, tp, method)[:, lo:hi + 1] for tp in taper])
             accumulate_multitaper(acc, spec_l)
         else:
@@ -269,11 +280,11 @@ def compute(epochs, nfft: int, lo: int, hi: int, metrics=METRICS, taper=None, me
     return out, acc
 
 
-def well_conditioned(epochs, nfft, lo, hi, metrics, tol, taper=None, ref=None):
+def well_conditioned(epochs, nfft, lo, hi, metrics, tol, taper=None, ref=None, mode="fixed"):
     """Per-metric boolean masks [P, nb] of entries on which two independent fp64
     spectral algorithms (rfft vs direct DFT) agree within tol[m]/2."""
-    a = ref if ref is not None else compute(epochs, nfft, lo, hi, metrics, taper)[0]
-    b = compute(epochs, nfft, lo, hi, metrics, taper, method="dft")[0]
+    a = ref if ref is not None else compute(epochs, nfft, lo, hi, metrics, taper, mode=mode)[0]
+    b = compute(epochs, nfft, lo, hi, metrics, taper, method="dft", mode=mode)[0]
     out = {}
     for m in metrics:
         if a.get(m) is None:
@@ -282,7 +293,7 @@ def well_conditioned(epochs, nfft, lo, hi, metrics, tol, taper=None, ref=None):
     return out
 
 
-def flush_sensitive(epochs, nfft, lo, hi, taper=None, lo_ratio=1e-15, hi_ratio=1e-11):
+def flush_sensitive(epochs, nfft, lo, hi, taper=None, lo_ratio=1e-15, hi_ratio=1e-11, mode="fixed"):
     """Boolean [P, nb]: (pair, bin) entries where some trial has
     |Im CSD| / |Re CSD| within two decades of the reference's 1e-13 flush
     threshold (spectral.py:227-228).  There the reference's sign(Im) is decided
@@ -292,7 +303,12 @@ def flush_sensitive(epochs, nfft, lo, hi, taper=None, lo_ratio=1e-15, hi_ratio=1
     C = epochs[0].shape[0]
     out = np.zeros((C * (C - 1) // 2, hi - lo + 1), dtype=bool)
     for ep in epochs:
-        if taper is not None and np.ndim(taper) == 2:
+        if mode == "welch" and ep.shape[1] >= 2 * nfft:
+            csd = 0
+            for sg in segments(ep, nfft):
+                c, _ = trial_csd_psd(trial_spectra(sg, nfft, None)[:, lo:hi + 1], C)
+                csd = csd + c
+        elif taper is not None and np.ndim(taper) == 2:
             csd = 0
             for tp in taper:
                 c, _ = trial_csd_psd(trial_spectra(ep, nfft, tp)[:, lo:hi + 1], C)

@@ -15,7 +15,8 @@ void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns
 void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb, cudaStream_t st);
 void run_get_spectra(const Plan& p, const int* slots, int ns, int bin_lo, int nbins, void* dst,
                      cudaStream_t st);
-void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, cudaStream_t st);
+void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, int taper, double w,
+                     cudaStream_t st);
 struct LagArgs;
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st);
@@ -164,8 +165,16 @@ int cs_row_tile_range(int n_nodes, int n_shards, int shard, int* rb, int* re, in
 
 int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, int hi, int L,
                    const double* tapers, int slot_cap, double scale, unsigned flags) {
-  (void)flags;
   if (!out) return CS_EPARAM;
+  if (flags & ~CS_PLAN_WELCH) { cs_set_error("unknown plan flags 0x%x", flags); return CS_EPARAM; }
+  int seg_stride = 0;
+  if (flags & CS_PLAN_WELCH) {  // segments on the taper axis (spectral.py:100-111, 272-283)
+    if (tapers || L != 1) { cs_set_error("welch mode takes no tapers"); return CS_EPARAM; }
+    if (nfft >= 2 && T >= 2 * nfft) {
+      L = T / nfft;
+      seg_stride = nfft;
+    }
+  }
   *out = nullptr;
   if (nfft < 2) { cs_set_error("nfft must be >= 2, got %d", nfft); return CS_EPARAM; }
   if (N < 1) { cs_set_error("need at least one channel"); return CS_EPARAM; }
@@ -175,7 +184,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
     cs_set_error("invalid band bins [%d, %d] for %d bins", lo, hi, nbins);
     return CS_EPARAM;
   }
-  if (L < 1 || (!tapers && L != 1)) { cs_set_error("bad taper count %d", L); return CS_EPARAM; }
+  if (L < 1 || (!tapers && L != 1 && !seg_stride)) { cs_set_error("bad taper count %d", L); return CS_EPARAM; }
   if (slot_cap < 1) { cs_set_error("slot_capacity must be >= 1"); return CS_EPARAM; }
   if (scale == 0.0) scale = 1.0;
   if (!(scale > 0.0) || !is_pow2(scale)) {
@@ -187,6 +196,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   p->device = device;
   p->N = N; p->T = T; p->nfft = nfft; p->lo = lo; p->hi = hi; p->nb = hi - lo + 1; p->L = L;
   p->T_eff = T < nfft ? T : nfft;
+  p->seg_stride = seg_stride;
   p->slot_cap = slot_cap;
   p->scale = (float)scale;
   p->dc_local = (lo == 0) ? 0 : -1;
@@ -378,8 +388,13 @@ int cs_get_spectra(cs_plan* p, const int* slots, int ns, int bin_lo, int nbins, 
 }
 
 int cs_put_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbins, int slot0, void* stream) {
+  return cs_put_taper_spectra(p, src, n, bin_lo, nbins, slot0, 0, 1.0, stream);
+}
+
+int cs_put_taper_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbins, int slot0, int taper,
+                         double w, void* stream) {
   if (!p || !src) { cs_set_error("cs_put_spectra: null argument"); return CS_EPARAM; }
-  if (p->L != 1) { cs_set_error("cs_put_spectra: single-taper plans only"); return CS_EPARAM; }
+  if (taper < 0 || taper >= p->L) { cs_set_error("cs_put_spectra: taper %d outside [0, %d)", taper, p->L); return CS_EPARAM; }
   if (bin_lo < 0 || nbins < 1 || bin_lo + nbins > p->nb || slot0 < 0) {
     cs_set_error("cs_put_spectra: bad bins/slot");
     return CS_EPARAM;
@@ -388,7 +403,7 @@ int cs_put_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbins, in
   DeviceGuard g(p->device);
   {
     cs::PhaseMark ph(*p, "put_spectra", (cudaStream_t)stream);
-    cs::run_put_spectra(*p, src, n, bin_lo, nbins, slot0 % p->slot_cap, (cudaStream_t)stream);
+    cs::run_put_spectra(*p, src, n, bin_lo, nbins, slot0 % p->slot_cap, taper, w, (cudaStream_t)stream);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_put_spectra");
   return CS_OK;

@@ -296,7 +296,9 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           // the odd-K phantom contributed the unit phasor (0, 1) to the PLV sums
           const float pr = lo_of(pvr[p]) + hi_of(pvr[p]);
           const float pim = lo_of(pvi[p]) + hi_of(pvi[p]) - (odd ? 1.f : 0.f);
-          const float plv = dead ? 0.f : sqrt_approx(pr * pr + pim * pim) * invK;
+          // a real bin (Nyquist) still has phases 0 / pi: only a zero spectrum makes PLV 0
+          const bool dead_plv = rPi[r] * rPj[c] == 0.f;
+          const float plv = dead_plv ? 0.f : sqrt_approx(pr * pr + pim * pim) * invK;
           if (bin_mask & 32u) __stcs(&a.plv_bins[rowoff + j], plv);  // streaming: keep the operands in L2
           if (band_mask & 32u) band_s[(5 * kTile + li) * kTile + lj] += plv;
           pvr[p] = pvi[p] = 0ull;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kSpecNodes)
 k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N,
           int T_eff, int nb, int L, const double2* __restrict__ tww, const double2* __restrict__ wsum,
           int slot0, int slot_cap, double2* __restrict__ X64, float2* __restrict__ X32, float scale,
-          int dc_local, int nyq_local, int vec16) {
+          int dc_local, int nyq_local, int vec16, int seg_stride) {
   using Sh = SpecShape<Tin, NBT, NS>;
   constexpr int ROWS = Sh::ROWS, TC = Sh::TC, RS = Sh::RS;
   extern __shared__ __align__(16) unsigned char spec_smem[];
@@ -67,7 +67,7 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
   const int k = blockIdx.z / L;
   const int l = blockIdx.z % L;
   const int nbt = min(NBT, nb - b0);
-  const Tin* xk = x + (int64_t)k * trial_stride;
+  const Tin* xk = x + (int64_t)k * trial_stride + (int64_t)l * seg_stride;  // welch: segment l
   const double2* twl = tww + ((int64_t)l * nb + b0) * T_eff;
   const int n_chunk = (T_eff + TC - 1) / TC;
 
@@ -218,11 +218,12 @@ static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns,
     configured = true;
   }
   const int vec16 = ((uintptr_t)x % 16 == 0) && ((ns * (int64_t)sizeof(Tin)) % 16 == 0) &&
-                    ((ts * (int64_t)sizeof(Tin)) % 16 == 0);
+                    ((ts * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.seg_stride * (int64_t)sizeof(Tin)) % 16 == 0);
   dim3 grid((p.N + Sh::ROWS - 1) / Sh::ROWS, (p.nb + NBT - 1) / NBT, kc * p.L);
   k_spectra<Tin, NBT, NS><<<grid, kSpecNodes, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
                                                            p.L, p.tww, p.wsum, slot0, p.slot_cap, p.X64,
-                                                           p.X32, p.scale, p.dc_local, p.nyq_local, vec16);
+                                                           p.X32, p.scale, p.dc_local, p.nyq_local, vec16,
+                                                           p.seg_stride);
 }
 
 template <typename Tin>
@@ -390,22 +391,25 @@ extern "C" int cs_probe_peaks(int device, double* fp32_lane_ops, double* fp64_fm
 // ring slots slot0.. (taper 0, plan-local bins [bin_lo, bin_lo + nbins)).
 namespace cs {
 __global__ void k_put_spectra(const double2* __restrict__ src, int n, int N, int nb, int L, int bin_lo,
-                              int nbins, int slot0, int slot_cap, float scale, double2* __restrict__ X64,
-                              float2* __restrict__ X32) {
+                              int nbins, int slot0, int slot_cap, int taper, double w, float scale,
+                              double2* __restrict__ X64, float2* __restrict__ X32) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
   if (idx >= (int64_t)N * nbins) return;
   const int node = (int)(idx / nbins), bl = (int)(idx % nbins);
-  const double2 v = src[((int64_t)k * N + node) * nbins + bl];
+  double2 v = src[((int64_t)k * N + node) * nbins + bl];
+  v.x *= w;
+  v.y *= w;
   const int slot = (slot0 + k) % slot_cap;
-  const int64_t o = (((int64_t)slot * L) * nb + bin_lo + bl) * N + node;
+  const int64_t o = (((int64_t)slot * L + taper) * nb + bin_lo + bl) * N + node;
   X64[o] = v;
   X32[o] = make_float2((float)(v.x * (double)scale), (float)(v.y * (double)scale));
 }
-void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, cudaStream_t st) {
+void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, int taper, double w,
+                     cudaStream_t st) {
   dim3 grid((unsigned)(((int64_t)p.N * nbins + 255) / 256), n);
   k_put_spectra<<<grid, 256, 0, st>>>((const double2*)src, n, p.N, p.nb, p.L, bin_lo, nbins, slot0, p.slot_cap,
-                                       p.scale, p.X64, p.X32);
+                                       taper, w, p.scale, p.X64, p.X32);
 }
 }  // namespace cs
 
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(kFftWarps * 32)
 k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N, int T_eff, int nfft,
               int log2M, int lo, int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw,
               const double2* __restrict__ post_tw, int slot0, int slot_cap, double2* __restrict__ X64,
-              float2* __restrict__ X32, float scale, int dc_local, int nyq_local) {
+              float2* __restrict__ X32, float scale, int dc_local, int nyq_local, int seg_stride) {
   extern __shared__ double2 fft_smem[];
   const int M = nfft >> 1;
   double2* stw = fft_smem;                                  // [M/2] twiddles, shared by the CTA
@@ -438,17 +442,21 @@ k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stri
   if (n >= N) return;  // warp-uniform
   const Tin* xr = x + (int64_t)k * trial_stride + (int64_t)n * node_stride;
 
-  // mean of the real samples, shifted by the first sample (fp64); samples stay in L1 for the taper loop
-  const double c = (double)xr[0];
-  double s = 0.0;
-  for (int t = lane; t < T_eff; t += 32) s += (double)xr[t] - c;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const double mu = c + s / (double)T_eff;
   const int slot = (slot0 + k) % slot_cap;
-
+  double mu = 0.0;
+  const Tin* xr0 = xr;
   for (int l = 0; l < L; ++l) {  // all tapers of this signal in one warp: samples read once from HBM
     const double* w = taper ? taper + (int64_t)l * T_eff : nullptr;
+    if (l == 0 || seg_stride) {  // welch: segment l has its own samples and mean
+      xr = xr0 + (int64_t)l * seg_stride;
+      // mean of the real samples, shifted by the first sample (fp64)
+      const double c = (double)xr[0];
+      double s = 0.0;
+      for (int t = lane; t < T_eff; t += 32) s += (double)xr[t] - c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      mu = c + s / (double)T_eff;
+    }
     // z_q = v_2q + i v_2q+1 (v = (x - mu) * taper, zero padded), stored at bitrev(q)
     for (int q = lane; q < M; q += 32) {
       const int t0 = 2 * q, t1 = 2 * q + 1;
@@ -569,7 +577,7 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
                int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw4,
                const double2* __restrict__ post_tw, const double2* __restrict__ wsum, int slot0, int slot_cap,
                double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local, int nyq_local,
-               int n_trials, int vec16) {
+               int n_trials, int vec16, int seg_stride) {
   constexpr int R = 32 / A, M = 32 * A, S = 32 + R, PAD = 8 / R;
   constexpr int BUF = (A * S > M + PAD * R) ? A * S : M + PAD * R;
   extern __shared__ double2 f4_smem[];
@@ -583,13 +591,15 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
   Tin* stage = (Tin*)(w32 + 32 + kFft4Warps * BUF) + warp * (32 * A * 2);
   const int ka2 = lane / R, h = lane % R;
   const int j_out = R == 4 ? (((h & 1) << 1) | (h >> 1)) : h;  // R-point DIF output order
-  const int64_t n_sig = (int64_t)N * n_trials;
+  // unit = (node, trial) with all tapers; welch: (node, trial, segment), one segment each
+  const int n_units_l = seg_stride ? L : 1;
+  const int64_t n_sig = (int64_t)N * n_trials * n_units_l;
   const int64_t gw = (int64_t)blockIdx.x * kFft4Warps + warp, nw = (int64_t)gridDim.x * kFft4Warps;
   constexpr int V = 16 / sizeof(Tin);  // elements per 16-byte copy
   auto prefetch = [&](int64_t sig) {
     if (sig < n_sig) {
-      const int n = (int)(sig % N), k = (int)(sig / N);
-      const Tin* xr = x + (int64_t)k * trial_stride + (int64_t)n * node_stride;
+      const int n = (int)(sig % N), k = (int)((sig / N) % n_trials), ls = (int)(sig / N / n_trials);
+      const Tin* xr = x + (int64_t)k * trial_stride + (int64_t)n * node_stride + (int64_t)ls * seg_stride;
       if (vec16) {
         for (int e = lane * V; e < T_eff; e += 32 * V) cp_async16(stage + e, xr + e, 16);
       } else {
@@ -600,7 +610,8 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
   };
   prefetch(gw);
   for (int64_t sig = gw; sig < n_sig; sig += nw) {
-    const int n = (int)(sig % N), k = (int)(sig / N);
+    const int n = (int)(sig % N), k = (int)((sig / N) % n_trials);
+    const int l_begin = seg_stride ? (int)(sig / N / n_trials) : 0, l_end = seg_stride ? l_begin + 1 : L;
     const int slot = (slot0 + k) % slot_cap;
     cp_async_wait0();
     __syncwarp();
@@ -609,7 +620,7 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
     // (plan table wsum)
     const double c = (double)stage[0];
     double mean_d = 0.0;
-    for (int l = 0; l < L; ++l) {
+    for (int l = l_begin; l < l_end; ++l) {
       const double* w = taper ? taper + (int64_t)l * T_eff : nullptr;
       double2 v[A];
       double sum = 0.0;
@@ -622,11 +633,11 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
         v[a] = w ? make_double2(d0 * (t0 < T_eff ? w[t0] : 0.0), d1 * (t0 + 1 < T_eff ? w[t0 + 1] : 0.0))
                  : make_double2(d0, d1);
       }
-      if (l == L - 1) {  // samples are in registers: stream the next signal in
+      if (l == l_end - 1) {  // samples are in registers: stream the next signal in
         __syncwarp();
         prefetch(sig + nw);
       }
-      if (l == 0) {
+      if (l == l_begin) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         mean_d = sum / (double)T_eff;
@@ -709,16 +720,17 @@ void launch_fft4(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
-  const int64_t sigs = (int64_t)p.N * kc;
+  const int64_t sigs = (int64_t)p.N * kc * (p.seg_stride ? p.L : 1);
   int64_t grid = (int64_t)nsm * ctas_per_sm;
   const int64_t need = (sigs + kFft4Warps - 1) / kFft4Warps;
   if (grid > need) grid = need;
   // 16-byte staging copies when every row start and the row length allow it
   const int vec16 = ((uintptr_t)x % 16 == 0) && ((ts * (int64_t)sizeof(Tin)) % 16 == 0) &&
-                    ((ns * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.T_eff * (int)sizeof(Tin)) % 16 == 0);
+                    ((ns * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.T_eff * (int)sizeof(Tin)) % 16 == 0) &&
+                    ((p.seg_stride * (int64_t)sizeof(Tin)) % 16 == 0);
   k_spectra_fft4<Tin, A><<<(unsigned)grid, kFft4Warps * 32, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff,
       p.lo, p.nb, p.L, p.taper, p.fft4_tw, p.post_tw, p.wsum, slot0, p.slot_cap, p.X64, p.X32, p.scale,
-      p.dc_local, p.nyq_local, kc, vec16);
+      p.dc_local, p.nyq_local, kc, vec16, p.seg_stride);
 }
 
 bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0, int kc,
@@ -742,12 +754,14 @@ bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_
     static bool cfg = false;
     if (!cfg) { cudaFuncSetAttribute(k_spectra_fft<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
     k_spectra_fft<double><<<grid, kFftWarps * 32, smem, st>>>((const double*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
-        p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local);
+        p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
+        p.seg_stride);
   } else {
     static bool cfg = false;
     if (!cfg) { cudaFuncSetAttribute(k_spectra_fft<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
     k_spectra_fft<float><<<grid, kFftWarps * 32, smem, st>>>((const float*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
-        p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local);
+        p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
+        p.seg_stride);
   }
   return true;
 }

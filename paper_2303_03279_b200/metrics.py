@@ -237,8 +237,8 @@ class ConnectivityEngine:
                  accumulate_band: tuple | None = None, taper=None, slot_capacity: int = 64):
         if spectral_mode not in ("fixed", "welch"):
             raise ParameterError(f"unknown spectral mode {spectral_mode!r}")
-        if spectral_mode == "welch":
-            raise ParameterError("welch spectral mode is not built on the device path yet")
+        if spectral_mode == "welch" and taper is not None:
+            raise ParameterError("welch mode takes no taper")
         self.n_channels = n_channels
         self.nfft = nfft
         self.sfreq = sfreq
@@ -260,19 +260,22 @@ class ConnectivityEngine:
         self._T = None
         self._next_slot = 0
         self._slot_of: dict = {}
+        self._seg0_of: dict = {}     # welch: slot holding only the first segment (the cached spectra)
         self._sum_trials: list = []
+        self._fold_slots: list = []  # ring slot of every fold, in order
         self.n_trials = 0
 
     # -- ring ------------------------------------------------------------------
     def _ensure_plan(self, T: int, scale: float):
         if self._plan is not None and T != self._T:
             raise ParameterError("epochs of one engine must share n_samples")
-        need = self._next_slot + 1
+        need = self._next_slot + 2
         if self._plan is None or need > self._plan.slot_capacity:
             cap = self._slot_capacity if self._plan is None else 2 * self._plan.slot_capacity
             new = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper,
                              slot_capacity=cap, device=spectral._device(),
-                             scale=self._plan.scale if self._plan is not None else scale)
+                             scale=self._plan.scale if self._plan is not None else scale,
+                             welch=self.spectral_mode == "welch")
             if self._plan is not None:
                 o64, o32 = self._plan.ring()
                 n64, n32 = new.ring()
@@ -295,12 +298,33 @@ class ConnectivityEngine:
             self._next_slot += 1
             self._plan.spectra(x[None].contiguous(), slot)
             spectral._count_ffts(self.n_channels * self._plan.n_tapers)
+            if self._plan.welch:
+                # the reference caches the first segment's spectra (spectral.py:286) and
+                # re-folds cached trials in fixed mode (metrics.py:337-341, 450-460):
+                # keep that segment in a slot of its own, then weight the welch slot's
+                # S segments by 1/sqrt(S) so its summed CSD is the segment mean
+                S = self._plan.n_tapers
+                r64, r32 = self._plan.ring()
+                s0 = self._next_slot
+                self._next_slot += 1
+                r64[s0].zero_()
+                r32[s0].zero_()
+                r64[s0, 0].copy_(r64[slot, 0])
+                r32[s0, 0].copy_(r32[slot, 0])
+                w = 1.0 / float(np.sqrt(S))
+                r64[slot].mul_(w)
+                r32[slot].mul_(w)
+                self._seg0_of[idx] = s0
             self._slot_of[idx] = slot
             if self.cache.enabled:
                 self.cache.spectra[idx] = slot
+            fold_slot = slot
+        else:  # cached trial: the reference folds its cached (first-segment) spectra
+            fold_slot = self._seg0_of.get(idx, self._slot_of[idx])
         if self.cache.enabled:
             self.cache.epochs[idx] = epoch
         self._sum_trials.append(idx)
+        self._fold_slots.append(fold_slot)
         self.n_trials += 1
 
     def ensure_band(self, band: FrequencyBand) -> None:
@@ -310,8 +334,7 @@ class ConnectivityEngine:
 
     # -- finalization ---------------------------------------------------------------
     def _slots(self):
-        return torch.tensor([self._slot_of[i] for i in self._sum_trials], dtype=torch.int32,
-                            device=self._plan.device)
+        return torch.tensor(self._fold_slots, dtype=torch.int32, device=self._plan.device)
 
     def finalize(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
         metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
@@ -343,6 +366,8 @@ class ConnectivityEngine:
             raise ParameterError("trial-window rebuild requires storage mode")
         keep = sorted(self.cache.epochs)[-n_last:] if n_last > 0 else []
         self._sum_trials = list(keep)
+        # re-added from the cache: fixed-mode folds of the cached spectra
+        self._fold_slots = [self._seg0_of.get(i, self._slot_of[i]) for i in keep]
         self.n_trials = len(keep)
 
 

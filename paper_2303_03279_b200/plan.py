@@ -57,7 +57,12 @@ class DevicePlan:
     [lo, hi] of an nfft-point one-sided spectrum."""
 
     def __init__(self, n_nodes: int, n_samples: int, nfft: int, lo: int, hi: int, taper=None,
-                 slot_capacity: int = 1, device=None, scale: float = 1.0):
+                 slot_capacity: int = 1, device=None, scale: float = 1.0, welch: bool = False,
+                 n_tapers: int | None = None):
+        """welch: segment mode (spectral.py:100-111, 264-283) -- trials of
+        n_samples >= 2 nfft become n_samples // nfft demeaned nfft segments on the
+        taper axis.  n_tapers (no taper given): a rectangular ring with that many
+        taper slots, filled by put_spectra(..., taper=l) (mixed welch trials)."""
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2303_03279_b200 needs a CUDA device (B200); there is no CPU fallback")
         dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -67,9 +72,14 @@ class DevicePlan:
         self.n_nodes, self.n_samples, self.nfft = int(n_nodes), int(n_samples), int(nfft)
         self.lo, self.hi = int(lo), int(hi)
         self.n_bins = self.hi - self.lo + 1
-        self.n_eff = min(self.n_samples, self.nfft)
+        self.welch = bool(welch) and self.n_samples >= 2 * self.nfft
+        if welch and taper is not None:
+            raise ParameterError("welch mode takes no taper")
+        self.n_eff = self.nfft if self.welch else min(self.n_samples, self.nfft)
         tap = make_taper(taper, self.n_eff)
-        self.n_tapers = 1 if tap is None else tap.shape[0]
+        if tap is None and n_tapers is not None and int(n_tapers) > 1:
+            tap = np.ones((int(n_tapers), self.n_eff))  # rectangular taper slots
+        self.n_tapers = (self.n_samples // self.nfft if self.welch else 1) if tap is None else tap.shape[0]
         self.slot_capacity = int(slot_capacity)
         self.scale = float(scale)
         L = _lib.lib()
@@ -80,8 +90,8 @@ class DevicePlan:
             tptr = self._taper.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         with torch.cuda.device(self.device):
             _lib.check(L.cs_plan_create(ctypes.byref(h), self.device.index, self.n_nodes, self.n_samples,
-                                        self.nfft, self.lo, self.hi, self.n_tapers, tptr,
-                                        self.slot_capacity, self.scale, 0))
+                                        self.nfft, self.lo, self.hi, 1 if tap is None else self.n_tapers, tptr,
+                                        self.slot_capacity, self.scale, _lib.CS_PLAN_WELCH if welch else 0))
         self._h = h
 
     def __del__(self):
@@ -199,14 +209,17 @@ class DevicePlan:
         return (_wrap(x64.value, shape, torch.complex128, self.device, self),
                 _wrap(x32.value, shape, torch.complex64, self.device, self))
 
-    def put_spectra(self, spectra: torch.Tensor, slot0: int, bin_lo: int = 0, stream=None) -> None:
-        """Upload complex128 spectra [n, N, nbins] (trial_spectra layout) into slots slot0..."""
+    def put_spectra(self, spectra: torch.Tensor, slot0: int, bin_lo: int = 0, stream=None, taper: int = 0,
+                    weight: float = 1.0) -> None:
+        """Upload complex128 spectra [n, N, nbins] (trial_spectra layout) into taper
+        slot ``taper`` of slots slot0.., multiplied by ``weight``."""
         spectra = spectra.to(device=self.device, dtype=torch.complex128).contiguous()
         if spectra.dim() != 3 or spectra.shape[1] != self.n_nodes:
             raise ParameterError(f"spectra must be [n, {self.n_nodes}, bins], got {tuple(spectra.shape)}")
         self._last_put = spectra
-        _lib.check(_lib.lib().cs_put_spectra(self._h, ctypes.c_void_p(spectra.data_ptr()), int(spectra.shape[0]),
-                                             int(bin_lo), int(spectra.shape[2]), int(slot0), _stream_ptr(stream)))
+        _lib.check(_lib.lib().cs_put_taper_spectra(self._h, ctypes.c_void_p(spectra.data_ptr()),
+                                                   int(spectra.shape[0]), int(bin_lo), int(spectra.shape[2]),
+                                                   int(slot0), int(taper), float(weight), _stream_ptr(stream)))
 
     def fft_call_count(self) -> int:
         return int(_lib.lib().cs_fft_call_count(self._h))
@@ -247,13 +260,17 @@ def row_tile_range(n_nodes: int, n_shards: int, shard: int):
 
 
 def compute_connectivity(x: torch.Tensor, nfft: int, lo: int, hi: int, metrics=SEVEN, taper=None,
-                         per_bin=True, band=True, plan: DevicePlan | None = None, stream=None):
+                         per_bin=True, band=True, plan: DevicePlan | None = None, stream=None, mode: str = "fixed"):
     """Batch path: all trials of x [K, N, T] (device) -> per-bin [nb, P] and band
-    [P] outputs for ``metrics`` over the inclusive bins [lo, hi]."""
+    [P] outputs for ``metrics`` over the inclusive bins [lo, hi].  mode="welch":
+    the reference's segment mode (spectral.py:264-283)."""
+    if mode not in ("fixed", "welch"):
+        raise ParameterError(f"unknown spectral mode {mode!r}")
     K, N, T = x.shape
     if plan is None:
         scale = pow2_scale(float(x.abs().amax()), min(T, nfft))
-        plan = DevicePlan(N, T, nfft, lo, hi, taper=taper, slot_capacity=K, device=x.device, scale=scale)
+        plan = DevicePlan(N, T, nfft, lo, hi, taper=taper, slot_capacity=K, device=x.device, scale=scale,
+                          welch=(mode == "welch"))
     plan.spectra(x, 0, stream=stream)
     slots = torch.arange(K, dtype=torch.int32, device=x.device)
     out = plan.pair_metrics(slots, metrics, 0, plan.n_bins, per_bin=per_bin, band=band, stream=stream)

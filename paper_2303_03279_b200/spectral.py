@@ -7,7 +7,9 @@ Same names, arguments and errors; the arithmetic runs in libcsconn.so:
     kernels over those slots (the reference's running sums are materialised
     only when an attribute such as ``csd_sum`` is read).
   * accumulate_spectra / accumulate_epoch keep the bins/count semantics of
-    spectral.py:244-286 (fixed mode; welch mode is not built yet).
+    spectral.py:244-286, fixed and welch mode (segments on the ring's taper
+    axis, a welch trial stored with weight 1/sqrt(S) so its summed CSD is the
+    segment mean of spectral.py:272-283).
 
 Reference anchors: spectral.py:18-30 (FFT counter), :49-97 (spectra),
 :114-122 (pair order), :125-201 (SpectrumSet), :204-286 (fold).
@@ -108,14 +110,45 @@ def fft_real(signal, nfft: int, taper=None) -> np.ndarray:
 
 
 def trial_spectra(epoch: EpochMatrix, nfft: int, mode: str = "fixed", taper=None) -> np.ndarray:
-    """Per-channel one-sided spectra, rows = channels (spectral.py:82-97)."""
+    """Per-channel one-sided spectra, rows = channels (spectral.py:82-97).  As in
+    the reference, ``mode`` is validated and the fixed-resolution spectra are
+    returned for both modes (the welch average lives in accumulate_epoch)."""
     if nfft < 2:
         raise ParameterError(f"nfft must be >= 2, got {nfft}")
     if mode not in ("fixed", "welch"):
         raise ParameterError(f"unknown spectral mode {mode!r}")
-    if mode == "welch":
-        raise ParameterError("welch spectral mode is not built on the device path yet")
     return device_trial_spectra(epoch.data, nfft, taper).cpu().numpy()
+
+
+def device_segment_spectra(data, nfft: int) -> torch.Tensor:
+    """complex128 [S, C, nfft//2+1] on the device: K1 over the S = max(1, T // nfft)
+    consecutive non-overlapping nfft segments, each demeaned (spectral.py:100-111)."""
+    x = _as_device_samples(data)
+    if x.dim() == 1:
+        x = x[None]
+    C, T = x.shape
+    S = max(1, T // nfft)
+    if T < nfft:
+        return device_trial_spectra(x, nfft)[None]
+    x = x.contiguous()
+    segs = x.as_strided((S, C, nfft), (nfft, T, 1))       # segment s = samples [s nfft, (s+1) nfft)
+    key = ("seg", C, nfft, S)
+    plan = _SPEC_PLANS.get(key)
+    if plan is None:
+        if len(_SPEC_PLANS) > 16:
+            _SPEC_PLANS.clear()
+        plan = DevicePlan(C, nfft, nfft, 0, nfft // 2, slot_capacity=S, device=_device())
+        _SPEC_PLANS[key] = plan
+    plan.spectra(segs, 0)
+    _count_ffts(S * C)
+    return plan.get_spectra(torch.arange(S, dtype=torch.int32, device=plan.device))
+
+
+def segment_spectra(epoch: EpochMatrix, nfft: int) -> list:
+    """Spectra of consecutive non-overlapping nfft segments ("welch" mode, spectral.py:100-111)."""
+    if nfft < 2:
+        raise ParameterError(f"nfft must be >= 2, got {nfft}")
+    return list(device_segment_spectra(epoch.data, nfft).cpu().numpy())
 
 
 def pair_index(n_channels: int):
@@ -161,30 +194,48 @@ class SpectrumSet:
         return self.n_channels * (self.n_channels - 1) // 2
 
     # -- storage -------------------------------------------------------------
-    def _ensure_capacity(self, extra: int, scale: float = 1.0) -> None:
+    def _ensure_capacity(self, extra: int, scale: float = 1.0, n_tapers: int = 1) -> None:
+        """Room for ``extra`` more slots with at least ``n_tapers`` taper (welch
+        segment) entries per slot; grows by re-planning and copying the ring."""
         need = self._next_slot + extra
-        if self._plan is not None and need <= self._plan.slot_capacity:
+        L_old = self._plan.n_tapers if self._plan is not None else 1
+        L = max(L_old, int(n_tapers))
+        if self._plan is not None and need <= self._plan.slot_capacity and L == L_old:
             return
         cap = max(8, 1 << max(need - 1, 1).bit_length())
+        if self._plan is not None:
+            cap = max(cap, self._plan.slot_capacity)
         new = DevicePlan(self.n_channels, self.nfft, self.nfft, 0, self.n_bins - 1, slot_capacity=cap,
-                         device=_device(), scale=self._plan.scale if self._plan is not None else scale)
+                         device=_device(), scale=self._plan.scale if self._plan is not None else scale,
+                         n_tapers=L)
         if self._plan is not None and self._next_slot:
             o64, o32 = self._plan.ring()
             n64, n32 = new.ring()
-            n64[: self._next_slot].copy_(o64[: self._next_slot])
-            n32[: self._next_slot].copy_(o32[: self._next_slot])
+            n64[: self._next_slot, :L_old].copy_(o64[: self._next_slot])
+            n32[: self._next_slot, :L_old].copy_(o32[: self._next_slot])
         self._plan = new
+
+    def _first_scale(self, spectra: torch.Tensor) -> float:
+        amax = float(spectra.abs().amax()) if spectra.numel() else 0.0
+        return pow2_scale(amax / max(self.nfft, 1) ** 0.5, self.nfft) if amax > 0 else 1.0
 
     def _fold(self, spectra: torch.Tensor, cols: np.ndarray, count: bool) -> None:
         """spectra: complex128 device [C, n_bins] (zeros outside ``cols``)."""
+        self._fold_segments(spectra[None], cols, count)
+
+    def _fold_segments(self, segs: torch.Tensor, cols: np.ndarray, count: bool) -> None:
+        """segs: complex128 device [S, C, n_bins]; S > 1 is a welch trial whose CSD /
+        PSD contribution is the mean over segments (spectral.py:272-283): each
+        segment is stored with weight 1/sqrt(S) on the slot's taper axis."""
+        S = int(segs.shape[0])
         if self._plan is None:
-            amax = float(spectra.abs().amax()) if spectra.numel() else 0.0
-            scale = pow2_scale(amax / max(self.nfft, 1) ** 0.5, self.nfft) if amax > 0 else 1.0
-            self._ensure_capacity(1, scale)
+            self._ensure_capacity(1, self._first_scale(segs), n_tapers=S)
         else:
-            self._ensure_capacity(1)
+            self._ensure_capacity(1, n_tapers=S)
         slot = self._next_slot
-        self._plan.put_spectra(spectra[None], slot)
+        w = 1.0 / float(np.sqrt(S))
+        for l in range(S):
+            self._plan.put_spectra(segs[l:l + 1], slot, taper=l, weight=w if S > 1 else 1.0)
         self._next_slot += 1
         self._entries.append((slot, cols.copy()))
         if count:
@@ -242,7 +293,7 @@ class SpectrumSet:
     def nbytes(self) -> int:
         if self._plan is None:
             return 0
-        return self._next_slot * self.n_channels * self.n_bins * (16 + 8)
+        return self._next_slot * self._plan.n_tapers * self.n_channels * self.n_bins * (16 + 8)
 
     def copy(self) -> "SpectrumSet":
         out = SpectrumSet(self.n_channels, self.nfft)
@@ -255,13 +306,14 @@ class SpectrumSet:
         if (other.n_channels, other.nfft) != (self.n_channels, self.nfft):
             raise ParameterError("cannot merge accumulators of different shape")
         if other._plan is not None and other._entries:
-            slots = torch.tensor([s for s, _ in other._entries], dtype=torch.int32, device=other._plan.device)
-            spec = other._plan.get_spectra(slots)
-            for k, (_, m) in enumerate(other._entries):
+            o64, _ = other._plan.ring()                       # [S, L, nb, N] complex128
+            Lo = other._plan.n_tapers
+            for s_o, m in other._entries:
                 if self._plan is None:
-                    self._ensure_capacity(len(other._entries), other._plan.scale)
-                self._ensure_capacity(1)
-                self._plan.put_spectra(spec[k:k + 1], self._next_slot)
+                    self._ensure_capacity(len(other._entries), other._plan.scale, n_tapers=Lo)
+                self._ensure_capacity(1, n_tapers=Lo)
+                for l in range(Lo):   # stored values already carry their weights
+                    self._plan.put_spectra(o64[s_o, l].transpose(0, 1)[None], self._next_slot, taper=l)
                 self._entries.append((self._next_slot, m.copy()))
                 self._next_slot += 1
         self.n_trials_accumulated += other.n_trials_accumulated
@@ -279,12 +331,12 @@ def _materialise_sums(acc: SpectrumSet) -> dict:
     if not acc._entries:
         return out
     dev = acc._plan.device
-    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.int32, device=dev)
-    X = acc._plan.get_spectra(slots)                       # [K, C, B] complex128
+    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.long, device=dev)
+    X = acc._plan.ring()[0][slots].permute(0, 1, 3, 2)     # [K, L, C, B] complex128 (weighted segments)
     masks = torch.tensor(np.stack([m for _, m in acc._entries]), device=dev)  # [K, B]
     pi, pj = (torch.as_tensor(a, device=dev) for a in pair_index(C))
     tiny = np.finfo(np.float64).tiny
-    psd = (X.abs() ** 2 * masks[:, None, :]).sum(0)
+    psd = ((X.abs() ** 2).sum(1) * masks[:, None, :]).sum(0)
     csd_s = torch.zeros((P, B), dtype=torch.complex128, device=dev)
     plv_s = torch.zeros_like(csd_s)
     pli_s = torch.zeros((P, B), dtype=torch.float64, device=dev)
@@ -292,7 +344,7 @@ def _materialise_sums(acc: SpectrumSet) -> dict:
     step = max(1, (1 << 24) // max(B, 1))
     for p0 in range(0, P, step):
         a, b = pi[p0:p0 + step], pj[p0:p0 + step]
-        csd = X[:, a, :] * torch.conj(X[:, b, :])          # [K, p, B]
+        csd = (X[:, :, a, :] * torch.conj(X[:, :, b, :])).sum(1)   # [K, p, B]: segment mean (welch) or single
         im = csd.imag.clone()
         im[im.abs() <= 1e-13 * csd.real.abs()] = 0.0
         csd = torch.complex(csd.real, im)
@@ -335,10 +387,19 @@ def accumulate_spectra(acc: SpectrumSet, spectra, bins=None, count: bool = True)
 
 
 def accumulate_epoch(acc: SpectrumSet, epoch: EpochMatrix, mode: str = "fixed", bins=None, taper=None):
-    """Compute and accumulate one trial; returns the spectra (spectral.py:264-286)."""
-    if mode == "welch" and epoch.n_samples >= 2 * acc.nfft:
-        raise ParameterError("welch spectral mode is not built on the device path yet")
-    spec = device_trial_spectra(epoch.data, acc.nfft, taper)
+    """Compute and accumulate one trial; returns the spectra (spectral.py:264-286).
+    Welch mode with n_samples >= 2 nfft folds the segment-mean CSD / PSD and
+    returns the first segment's spectra, as the reference does."""
+    if mode not in ("fixed", "welch"):
+        raise ParameterError(f"unknown spectral mode {mode!r}")
     cols = _cols_mask(acc.n_bins, bins)
-    acc._fold(spec if cols.all() else spec * torch.as_tensor(cols, device=spec.device)[None, :], cols, True)
+    cmask = None if cols.all() else torch.as_tensor(cols)
+    if mode == "welch" and epoch.n_samples >= 2 * acc.nfft:
+        if taper is not None:
+            raise ParameterError("welch mode takes no taper")
+        segs = device_segment_spectra(epoch.data, acc.nfft)          # [S, C, B]
+        acc._fold_segments(segs if cmask is None else segs * cmask.to(segs.device)[None, None, :], cols, True)
+        return segs[0].cpu().numpy()
+    spec = device_trial_spectra(epoch.data, acc.nfft, taper)
+    acc._fold(spec if cmask is None else spec * cmask.to(spec.device)[None, :], cols, True)
     return spec.cpu().numpy()

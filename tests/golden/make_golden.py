@@ -41,14 +41,14 @@ def tapered_spectra(data, nfft, taper):
     return out
 
 
-def run_case(name, epochs, nfft, lo, hi, taper=None):
+def run_case(name, epochs, nfft, lo, hi, taper=None, mode="fixed"):
     """epochs: float array [K, C, T]."""
     K, C, _ = epochs.shape
     acc = S.SpectrumSet(C, nfft)
     for k in range(K):
         ep = EpochMatrix(data=epochs[k], sfreq=1000.0, trial_index=k)
         if taper is None:
-            S.accumulate_epoch(acc, ep)
+            S.accumulate_epoch(acc, ep, mode=mode)
         elif taper.ndim == 1:
             S.accumulate_spectra(acc, tapered_spectra(ep.data, nfft, taper))
         else:  # multitaper: mean CSD/PSD over tapers, reference fold
@@ -61,7 +61,7 @@ def run_case(name, epochs, nfft, lo, hi, taper=None):
             S._fold_csd(acc, csd / len(taper), psd / len(taper))
     band = FrequencyBand(lo, hi, 1.0)
     rec = {"epochs": epochs, "nfft": nfft, "lo": lo, "hi": hi,
-           "taper": np.zeros(0) if taper is None else taper}
+           "taper": np.zeros(0) if taper is None else taper, "mode": np.array(mode)}
     for nm in NAMES:
         try:
             rec["bins_" + nm] = M._SPECTRAL_BINS[MetricId[nm]](acc, band)
@@ -116,6 +116,11 @@ def main():
     T = info["trial_samples"]
     eps = np.array([data[:, m:m + T] for m in info["markers"]])
     run_case("sim2024_thresh", eps, 600, 15, 21)
+
+    # welch mode (spectral.py:264-283): 3 segments of 64 (T = 200, 8 samples dropped),
+    # and a short-trial fallback to fixed mode (T < 2 nfft)
+    run_case("welch3", rng.standard_normal((6, 7, 200)), 64, 2, 20, mode="welch")
+    run_case("welch_short", rng.standard_normal((5, 4, 100)), 64, 0, 32, mode="welch")
 
 
 if __name__ == "__main__":

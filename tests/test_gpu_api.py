@@ -337,3 +337,73 @@ def test_host_pipeline_matches_device_path():
         for m in SEVEN + ("COHY",):
             # same kernels; only the band-mean summation order may differ (bins split over CTAs)
             np.testing.assert_allclose(o[m].numpy(), want[m]["band"].cpu().numpy(), rtol=0, atol=2e-6, err_msg=m)
+
+
+# ---------------------------------------------------------------- welch mode (test_spectral.py:138-160)
+class TestWelchMode:
+    def test_welch_averages_segments(self):
+        ep = make_epochs(1, 2, 64, seed=4)[0]
+        acc = S.SpectrumSet(2, 16)
+        S.accumulate_epoch(acc, ep, mode="welch")
+        pi, pj = S.pair_index(2)
+        csd = np.zeros((1, 9), np.complex128)
+        psd = np.zeros((2, 9))
+        for k in range(4):
+            s = S.trial_spectra(EpochMatrix(data=ep.data[:, k * 16:(k + 1) * 16], sfreq=ep.sfreq), 16)
+            csd += s[pi] * np.conj(s[pj])
+            psd += np.abs(s) ** 2
+        np.testing.assert_allclose(acc.csd_sum, csd / 4, atol=1e-10)
+        np.testing.assert_allclose(acc.psd_sum, psd / 4, atol=1e-10)
+
+    def test_welch_falls_back_for_short_trials(self):
+        ep = make_epochs(1, 2, 20, seed=4)[0]
+        a, b = S.SpectrumSet(2, 16), S.SpectrumSet(2, 16)
+        S.accumulate_epoch(a, ep, mode="welch")
+        S.accumulate_epoch(b, ep, mode="fixed")
+        np.testing.assert_allclose(a.csd_sum, b.csd_sum)
+
+    def test_segment_spectra_and_fft_counter(self):
+        ep = make_epochs(1, 3, 70, seed=5)[0]
+        S.reset_fft_call_count()
+        segs = S.segment_spectra(ep, 16)
+        assert len(segs) == 4 and S.fft_call_count() == 4 * 3
+        want = [O.trial_spectra(ep.data[:, k * 16:(k + 1) * 16], 16) for k in range(4)]
+        for g, w in zip(segs, want):
+            np.testing.assert_allclose(g, w, atol=1e-9 * np.abs(w).max())
+
+    def test_mixed_welch_and_fixed_trials(self):
+        """A welch trial folds its segment-mean CSD, a fixed one its own CSD
+        (weights of spectral.py:272-283), in one accumulator."""
+        eps = make_epochs(4, 5, 96, seed=9)
+        acc = S.SpectrumSet(5, 32)
+        ref = O.Sums(5, 17)
+        for k, ep in enumerate(eps):
+            mode = "welch" if k % 2 == 0 else "fixed"
+            S.accumulate_epoch(acc, ep, mode=mode)
+            if mode == "welch":
+                O.accumulate_multitaper(ref, np.stack([O.trial_spectra(sg, 32) for sg in O.segments(ep.data, 32)]))
+            else:
+                O.accumulate(ref, O.trial_spectra(ep.data, 32))
+        band = FrequencyBand(0, 16, 1.0)
+        for metric, fn in M._SPECTRAL_BINS.items():
+            want = O.BINS[metric.value](ref)
+            assert np.abs(fn(acc, band) - want).max() <= TOL[metric.value], metric.value
+
+    def test_engine_welch_then_rebuild_uses_cached_first_segments(self):
+        """ConnectivityEngine(spectral_mode="welch"): first folds are segment means;
+        rebuild_last re-folds the cached first-segment spectra in fixed mode
+        (metrics.py:337-341, 450-460), exactly as the reference does."""
+        eps = make_epochs(6, 6, 128, seed=13)
+        band = FrequencyBand(2, 12, 1.0)
+        eng = M.ConnectivityEngine(6, 32, 600.0, storage_mode=True, spectral_mode="welch")
+        for ep in eps:
+            eng.add_trial(ep)
+        for metric in ("COH", "PLV", "WPLI", "IMAGCOHY"):
+            got = eng.finalize(MetricId[metric], band).weights
+            want, _ = O.compute([e.data for e in eps], 32, 2, 12, metrics=(metric,), mode="welch")
+            assert np.abs(got - want[metric]["band"]).max() <= TOL[metric], metric
+        eng.rebuild_last(4)
+        for metric in ("COH", "PLI", "WPLI"):
+            got = eng.finalize(MetricId[metric], band).weights
+            want, _ = O.compute([e.data[:, :32] for e in eps[-4:]], 32, 2, 12, metrics=(metric,))
+            assert np.abs(got - want[metric]["band"]).max() <= TOL[metric], metric

@@ -28,18 +28,23 @@ def _load(name):
     return {k: z[k] for k in z.files}
 
 
+def _mode(g):
+    return str(g["mode"]) if "mode" in g else "fixed"
+
+
 def _run(g, metrics, dtype=torch.float64):
     from paper_2303_03279_b200 import compute_connectivity
     taper = g["taper"] if g["taper"].size else None
     x = torch.tensor(g["epochs"], dtype=dtype, device="cuda")
-    out, plan = compute_connectivity(x, int(g["nfft"]), int(g["lo"]), int(g["hi"]), metrics=metrics, taper=taper)
+    out, plan = compute_connectivity(x, int(g["nfft"]), int(g["lo"]), int(g["hi"]), metrics=metrics, taper=taper,
+                                     mode=_mode(g))
     nfb = plan.fallback_count()
     torch.cuda.synchronize()
     return {m: {k: (v.cpu().numpy() if v is not None else None) for k, v in d.items()} for m, d in out.items()}, nfb
 
 
 CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg1like",
-         "dpss_small", "zerolag_dead", "zerolag_dead_hann", "sim2024_thresh"]
+         "dpss_small", "zerolag_dead", "zerolag_dead_hann", "sim2024_thresh", "welch3", "welch_short"]
 
 
 # "imag_tc": IMAGCOHY without a sign-based metric is produced by the tensor-core kernel
@@ -58,8 +63,9 @@ def test_metrics_match_reference(case, family):
     taper = g["taper"] if g["taper"].size else None
     ref = {m: {"bins": g["bins_" + m]} for m in metrics}
     masks = O.well_conditioned(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), metrics, TOL,
-                               taper=taper, ref=ref)
-    sens = O.flush_sensitive(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), taper=taper)
+                               taper=taper, ref=ref, mode=_mode(g))
+    sens = O.flush_sensitive(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), taper=taper,
+                             mode=_mode(g))
     masks = {m: v & ~sens for m, v in masks.items()}
     for m in metrics:
         want = g["bins_" + m]                      # [P, nb] reference layout

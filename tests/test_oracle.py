@@ -21,7 +21,8 @@ def _load(name):
 def test_oracle_matches_reference_golden(case):
     g = _load(case)
     taper = g["taper"] if g["taper"].size else None
-    out, _ = O.compute(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), taper=taper)
+    mode = str(g["mode"]) if "mode" in g else "fixed"
+    out, _ = O.compute(list(g["epochs"]), int(g["nfft"]), int(g["lo"]), int(g["hi"]), taper=taper, mode=mode)
     for m in O.METRICS:
         want = g["bins_" + m]
         if want.size == 0:
