@@ -87,13 +87,14 @@ typedef struct cs_outputs {
 } cs_outputs;
 
 /* Running sums (SpectrumSet layout of spectral.py:136-141, restricted to the
- * requested bins, bin-major [nbb][pair_stride]).  Any pointer may be NULL. */
+ * requested bins, bin-major [nbb][pair_stride]), fp64 like the reference.  Any
+ * pointer may be NULL. */
 typedef struct cs_sums {
-  float* csd;      /* complex64 [nbb][pair_stride][2] */
-  float* plv;      /* complex64 [nbb][pair_stride][2] */
-  int32_t* pli;    /* integer-valued sign sums        */
-  float* abs_im;   /* sum |Im CSD|                    */
-  float* psd;      /* [nbb][n_nodes]                  */
+  double* csd;     /* complex128 [nbb][pair_stride][2]: sum_k CSD_k (Im flushed)   */
+  double* plv;     /* complex128 [nbb][pair_stride][2]: sum_k CSD_k / |CSD_k|       */
+  int32_t* pli;    /* [nbb][pair_stride]: sum_k sign(Im CSD_k) (integer-valued)    */
+  double* abs_im;  /* [nbb][pair_stride]: sum_k |Im CSD_k|                         */
+  double* psd;     /* [nbb][n_nodes]: sum_k |X_k|^2                                */
   int64_t pair_base;
   int64_t pair_stride;
 } cs_sums;
@@ -128,7 +129,11 @@ int cs_pair_metrics(cs_plan* plan, const int* slots_dev, int n_slots, unsigned m
                     int bin_lo, int n_bins, int row_tile_begin, int row_tile_end,
                     const cs_outputs* out, void* stream);
 
-/* SpectrumSet-compatible running sums over the same trial / bin selection. */
+/* SpectrumSet-compatible running sums over the same trial / bin selection, from
+ * the fp64 ring with the reference's arithmetic (spectral.py:204-241: per-trial
+ * CSD = sum over tapers / welch segments, Im flush at 1e-13 |Re|, unit phasor
+ * where |CSD| > DBL_MIN, sign(0) = 0) for pairs [pair_base, pair_base +
+ * pair_stride).  An accessor (SpectrumSet.csd_sum etc.), not the metric path. */
 int cs_pair_sums(cs_plan* plan, const int* slots_dev, int n_slots, int bin_lo, int n_bins,
                  const cs_sums* out, void* stream);
 

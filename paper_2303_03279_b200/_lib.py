@@ -24,6 +24,12 @@ class CsOutputs(ctypes.Structure):
                 ("pair_stride", ctypes.c_int64)]
 
 
+class CsSums(ctypes.Structure):
+    _fields_ = [("csd", ctypes.c_void_p), ("plv", ctypes.c_void_p), ("pli", ctypes.c_void_p),
+                ("abs_im", ctypes.c_void_p), ("psd", ctypes.c_void_p),
+                ("pair_base", ctypes.c_int64), ("pair_stride", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -43,6 +49,7 @@ def lib():
     L.cs_pair_metrics.argtypes = [vp, vp, i32, u32, i32, i32, i32, i32, ctypes.POINTER(CsOutputs), vp]
     L.cs_get_spectra.argtypes = [vp, vp, i32, i32, i32, vp, vp]
     L.cs_put_spectra.argtypes = [vp, vp, i32, i32, i32, i32, vp]
+    L.cs_pair_sums.argtypes = [vp, vp, i32, i32, i32, ctypes.POINTER(CsSums), vp]
     L.cs_put_taper_spectra.argtypes = [vp, vp, i32, i32, i32, i32, i32, dbl, vp]
     L.cs_num_row_tiles.argtypes = [i32]
     L.cs_row_tile_range.argtypes = [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),

@@ -17,6 +17,7 @@ void run_get_spectra(const Plan& p, const int* slots, int ns, int bin_lo, int nb
                      cudaStream_t st);
 void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, int taper, double w,
                      cudaStream_t st);
+void run_pair_sums(const Plan& p, const int* slots, int K, int bin_lo, int nbb, const cs_sums* out, cudaStream_t st);
 struct LagArgs;
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st);
@@ -470,9 +471,22 @@ int cs_ring_view(cs_plan* p, void** x64, void** x32, int64_t* n_elems) {
 int64_t cs_fft_call_count(const cs_plan* p) { return p ? p->fft_calls : 0; }
 void cs_reset_fft_call_count(cs_plan* p) { if (p) p->fft_calls = 0; }
 
-int cs_pair_sums(cs_plan*, const int*, int, int, int, const cs_sums*, void*) {
-  cs_set_error("cs_pair_sums: not implemented yet");
-  return CS_EPARAM;
+int cs_pair_sums(cs_plan* p, const int* slots, int K, int bin_lo, int nbb, const cs_sums* out, void* stream) {
+  if (!p || !out || (!slots && K > 0)) { cs_set_error("cs_pair_sums: null argument"); return CS_EPARAM; }
+  if (K < 0) { cs_set_error("cs_pair_sums: negative trial count"); return CS_EPARAM; }
+  if (bin_lo < 0 || nbb < 1 || bin_lo + nbb > p->nb) {
+    cs_set_error("bins [%d, %d) outside the plan's %d bins", bin_lo, bin_lo + nbb, p->nb);
+    return CS_EPARAM;
+  }
+  if (out->pair_base < 0 || out->pair_stride < 0) { cs_set_error("cs_pair_sums: bad pair range"); return CS_EPARAM; }
+  DeviceGuard g(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    cs::PhaseMark ph(*p, "pair_sums", st);
+    cs::run_pair_sums(*p, slots, K, bin_lo, nbb, out, st);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_sums");
+  return CS_OK;
 }
 
 }  // extern "C"

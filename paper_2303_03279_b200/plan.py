@@ -168,6 +168,27 @@ class DevicePlan:
                                               int(row_tiles[1]), ctypes.byref(desc), _stream_ptr(stream)))
         return outputs
 
+    def pair_sums(self, slots: torch.Tensor, bin_lo: int = 0, n_bins: int | None = None, stream=None) -> dict:
+        """The reference's running sums over the trials in ``slots`` (cs_pair_sums):
+        csd / plv complex128 [nbb, P], pli int32 [nbb, P], abs_im float64 [nbb, P],
+        psd float64 [nbb, N] (bin-major; the reference layout is the transpose)."""
+        if n_bins is None:
+            n_bins = self.n_bins - bin_lo
+        if slots.dtype != torch.int32 or slots.device != self.device:
+            slots = slots.to(device=self.device, dtype=torch.int32)
+        P = self.n_pairs
+        o = {"csd": torch.empty((n_bins, P), dtype=torch.complex128, device=self.device),
+             "plv": torch.empty((n_bins, P), dtype=torch.complex128, device=self.device),
+             "pli": torch.empty((n_bins, P), dtype=torch.int32, device=self.device),
+             "abs_im": torch.empty((n_bins, P), dtype=torch.float64, device=self.device),
+             "psd": torch.empty((n_bins, self.n_nodes), dtype=torch.float64, device=self.device)}
+        d = _lib.CsSums(o["csd"].data_ptr(), o["plv"].data_ptr(), o["pli"].data_ptr(), o["abs_im"].data_ptr(),
+                        o["psd"].data_ptr(), 0, P)
+        self._last_slots = slots
+        _lib.check(_lib.lib().cs_pair_sums(self._h, ctypes.c_void_p(slots.data_ptr()), int(slots.numel()),
+                                           int(bin_lo), int(n_bins), ctypes.byref(d), _stream_ptr(stream)))
+        return o
+
     def fallback_count(self, stream=None) -> int:
         n = ctypes.c_int64()
         _lib.check(_lib.lib().cs_last_fallback_count(self._h, _stream_ptr(stream), ctypes.byref(n)))

@@ -322,41 +322,23 @@ class SpectrumSet:
 
 def _materialise_sums(acc: SpectrumSet) -> dict:
     """The reference's running sums (spectral.py:136-141, fold of :216-241) from
-    the cached spectra, evaluated on the device in complex128 (an accessor for
-    callers that read the sums directly; the finalisers never use it)."""
+    the cached spectra by cs_pair_sums (fp64, reference arithmetic) -- an accessor
+    for callers that read the sums directly; the finalisers never use it.  Folds
+    that covered only some columns stored zeros elsewhere, which contribute 0 to
+    every sum (CSD 0, no phasor, sign(0) = 0)."""
     C, B = acc.n_channels, acc.n_bins
     P = acc.n_pairs
     out = {"csd": np.zeros((P, B), np.complex128), "psd": np.zeros((C, B)), "plv": np.zeros((P, B), np.complex128),
            "pli": np.zeros((P, B)), "abs_im": np.zeros((P, B))}
     if not acc._entries:
         return out
-    dev = acc._plan.device
-    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.long, device=dev)
-    X = acc._plan.ring()[0][slots].permute(0, 1, 3, 2)     # [K, L, C, B] complex128 (weighted segments)
-    masks = torch.tensor(np.stack([m for _, m in acc._entries]), device=dev)  # [K, B]
-    pi, pj = (torch.as_tensor(a, device=dev) for a in pair_index(C))
-    tiny = np.finfo(np.float64).tiny
-    psd = ((X.abs() ** 2).sum(1) * masks[:, None, :]).sum(0)
-    csd_s = torch.zeros((P, B), dtype=torch.complex128, device=dev)
-    plv_s = torch.zeros_like(csd_s)
-    pli_s = torch.zeros((P, B), dtype=torch.float64, device=dev)
-    abs_s = torch.zeros_like(pli_s)
-    step = max(1, (1 << 24) // max(B, 1))
-    for p0 in range(0, P, step):
-        a, b = pi[p0:p0 + step], pj[p0:p0 + step]
-        csd = (X[:, :, a, :] * torch.conj(X[:, :, b, :])).sum(1)   # [K, p, B]: segment mean (welch) or single
-        im = csd.imag.clone()
-        im[im.abs() <= 1e-13 * csd.real.abs()] = 0.0
-        csd = torch.complex(csd.real, im)
-        mag = csd.abs()
-        unit = torch.where(mag > tiny, csd / torch.where(mag > tiny, mag, torch.ones_like(mag)), torch.zeros_like(csd))
-        w = masks[:, None, :].to(torch.float64)
-        csd_s[p0:p0 + step] = (csd * w).sum(0)
-        plv_s[p0:p0 + step] = (unit * w).sum(0)
-        pli_s[p0:p0 + step] = (torch.sign(im) * w).sum(0)
-        abs_s[p0:p0 + step] = (im.abs() * w).sum(0)
-    out["csd"], out["psd"], out["plv"] = csd_s.cpu().numpy(), psd.cpu().numpy(), plv_s.cpu().numpy()
-    out["pli"], out["abs_im"] = pli_s.cpu().numpy(), abs_s.cpu().numpy()
+    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.int32, device=acc._plan.device)
+    o = acc._plan.pair_sums(slots)
+    out["csd"] = o["csd"].T.cpu().numpy().copy()
+    out["plv"] = o["plv"].T.cpu().numpy().copy()
+    out["pli"] = o["pli"].T.to(torch.float64).cpu().numpy().copy()
+    out["abs_im"] = o["abs_im"].T.cpu().numpy().copy()
+    out["psd"] = o["psd"].T.cpu().numpy().copy()
     return out
 
 

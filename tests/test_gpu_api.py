@@ -407,3 +407,27 @@ class TestWelchMode:
             got = eng.finalize(MetricId[metric], band).weights
             want, _ = O.compute([e.data[:, :32] for e in eps[-4:]], 32, 2, 12, metrics=(metric,))
             assert np.abs(got - want[metric]["band"]).max() <= TOL[metric], metric
+
+
+@pytest.mark.parametrize("case", ["rect_crop_oddk", "rect_accept", "welch3", "zerolag_dead"])
+def test_running_sums_match_reference(case):
+    """SpectrumSet attributes (cs_pair_sums over the fp64 ring) against the
+    reference-pinned oracle's sums (spectral.py:136-141, 216-241)."""
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / f"{case}.npz")
+    mode = str(g["mode"]) if "mode" in g.files else "fixed"
+    nfft = int(g["nfft"])
+    eps = [EpochMatrix(data=e, sfreq=1000.0, trial_index=k) for k, e in enumerate(g["epochs"])]
+    acc = S.SpectrumSet(eps[0].n_channels, nfft)
+    for ep in eps:
+        S.accumulate_epoch(acc, ep, mode=mode)
+    _, ref = O.compute([e.data for e in eps], nfft, 0, nfft // 2, mode=mode)
+    scale = np.abs(ref.csd_sum).max()
+    np.testing.assert_allclose(acc.csd_sum, ref.csd_sum, atol=1e-9 * scale)
+    np.testing.assert_allclose(acc.psd_sum, ref.psd_sum, atol=1e-9 * np.abs(ref.psd_sum).max())
+    np.testing.assert_allclose(acc.abs_im_sum, ref.abs_im_sum, atol=1e-9 * scale)
+    np.testing.assert_allclose(acc.plv_sum, ref.plv_sum, atol=1e-9)
+    # sign sums are integers: exact wherever the entry is not decided by the 1e-13 flush
+    sens = O.flush_sensitive([e.data for e in eps], nfft, 0, nfft // 2, mode=mode)
+    assert np.array_equal(acc.pli_sum[~sens], ref.pli_sum[~sens])
+    assert acc.n_trials_accumulated == len(eps)
