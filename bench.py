@@ -394,6 +394,38 @@ def main():
                    "note": "fp16 hi/lo split = 3 products per real product; frac = roofline time / measured time"}
     breakdown = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in prof.items()}
 
+    # ---- network post-processing on the device over the COH band weights ----
+    post = None
+    if "COH" in metrics and ws == 1:
+        import ctypes as _ct
+        from paper_2303_03279_b200 import _lib as L_
+        wband = outs["COH"]["band"]
+        wcopy = wband.clone()
+        P_all = wband.numel()
+        keep = int(np.ceil(0.05 * P_all))
+        idx = torch.empty(keep, dtype=torch.int64, device=dev)
+        sp = _ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for _ in range(2):
+            L_.check(L_.lib().cs_net_normalize(_ct.c_void_p(wcopy.data_ptr()), None, P_all, sp))
+            L_.check(L_.lib().cs_net_threshold(_ct.c_void_p(wcopy.data_ptr()), P_all, keep, _ct.c_void_p(idx.data_ptr()), sp))
+        torch.cuda.synchronize()
+        tn, tt = [], []
+        for _ in range(5):
+            a, b, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record()
+            L_.check(L_.lib().cs_net_normalize(_ct.c_void_p(wcopy.data_ptr()), None, P_all, sp))
+            b.record()
+            L_.check(L_.lib().cs_net_threshold(_ct.c_void_p(wcopy.data_ptr()), P_all, keep, _ct.c_void_p(idx.data_ptr()), sp))
+            c2.record()
+            torch.cuda.synchronize()
+            tn.append(a.elapsed_time(b))
+            tt.append(b.elapsed_time(c2))
+        post = {"edges": P_all, "keep_fraction": 0.05, "normalize_ms": float(np.median(tn)),
+                "threshold_ms": float(np.median(tt)),
+                "threshold_gbs": 5 * 4.0 * P_all / (float(np.median(tt)) * 1e-3) / 1e9,
+                "note": "device normalize (max |w| + scale) and top-k threshold (4 radix passes + count + ordered compaction) on the cfg5 COH band weights"}
+        del wcopy, idx
+
     # ---- per metric: each metric alone with K1 + only the kernel it needs ----
     per_metric = None
     if not args.no_per_metric and len(metrics) > 1:
@@ -436,7 +468,8 @@ def main():
                    "outputs": "per-bin [nb,P] + band-mean [P] per metric", "parallelism": f"pair-row-tiles x{ws}",
                    "l2": "inputs 4.1 GB > 126 MB L2 (no flush needed)" if c.cfg == 5 else "inputs > L2" ,
                    "updates_per_step": c.updates},
-        "roofline": roof, "roofline_k2": roof_k2, "per_metric": per_metric, "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
+        "roofline": roof, "roofline_k2": roof_k2, "per_metric": per_metric, "post_processing": post,
+        "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
         "gpu_launches": launches, "clocks": clk.summary(),
         "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma, "hbm_gbs": peaks["hbm_gbs"],
                   "hbm_source": peak_kind},

@@ -154,6 +154,17 @@ int cs_put_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, int n_
 int cs_put_taper_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, int n_bins, int slot0,
                          int taper, double w, void* stream);
 
+/* Network post-processing on the device (core.py:168-205), over band weights
+ * w[n] (fp32, pair order of np.triu_indices) and optional complex weights
+ * cw[n] (complex64):
+ *  cs_net_normalize  divides w (and cw) in place by max |w| (an all-zero network
+ *                    is left unchanged; n >= 1 required),
+ *  cs_net_threshold  writes the pair indices of the `keep` largest |w|, ties at the
+ *                    threshold broken by ascending (i, j), in ascending order into
+ *                    out_idx_dev[keep] (keep = ceil(keep_fraction * n)). */
+int cs_net_normalize(float* w_dev, void* cw_dev, int64_t n, void* stream);
+int cs_net_threshold(const float* w_dev, int64_t n, int64_t keep, int64_t* out_idx_dev, void* stream);
+
 /* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
  * range of shard `shard` of `n_shards` (balanced by tile count) and the
  * contiguous global pair range [pair_begin, pair_end) it covers. */

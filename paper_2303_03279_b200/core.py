@@ -143,9 +143,12 @@ class ConnectivityNetwork:
     """
 
     def __init__(self, metric, band, n_trials, node_ids, positions, weights, edge_i=None, edge_j=None,
-                 complex_weights=None, lags=None, normalized=False, warnings=()):
+                 complex_weights=None, lags=None, normalized=False, warnings=(), pairs=None):
+        """pairs: optional device int64 pair indices (triu order) of the edges when
+        they are a subset (thresholded on the device); None = all i < j pairs."""
         if n_trials < 1:
             raise ParameterError("n_trials must be >= 1")
+        self._pairs = pairs
         self.metric = metric
         self.band = band
         self.n_trials = int(n_trials)
@@ -202,17 +205,30 @@ class ConnectivityNetwork:
             self._cw = self._host(self._cw, np.complex128)
         return self._cw
 
+    def _edges(self):
+        if self._ei is None:
+            if self._pairs is None:
+                self._ei, self._ej = (a.astype(np.int64) for a in _triu(self.n_nodes))
+            else:
+                p = self._host(self._pairs, np.int64)
+                self._ei, self._ej = pair_to_ij(p, self.n_nodes)
+        return self._ei, self._ej
+
     @property
     def edge_i(self) -> np.ndarray:
-        if self._ei is None:
-            self._ei, self._ej = (a.astype(np.int64) for a in _triu(self.n_nodes))
-        return self._ei
+        return self._edges()[0]
 
     @property
     def edge_j(self) -> np.ndarray:
-        if self._ej is None:
-            self._ei, self._ej = (a.astype(np.int64) for a in _triu(self.n_nodes))
-        return self._ej
+        return self._edges()[1]
+
+    def _replace(self, **kw):
+        d = dict(metric=self.metric, band=self.band, n_trials=self.n_trials, node_ids=self.node_ids,
+                 positions=self.positions, weights=self._w, edge_i=self._ei, edge_j=self._ej,
+                 complex_weights=self._cw, lags=self.lags, normalized=self.normalized, warnings=self.warnings,
+                 pairs=self._pairs)
+        d.update(kw)
+        return ConnectivityNetwork(**d)
 
     @property
     def n_nodes(self) -> int:
@@ -231,3 +247,102 @@ def band_average(per_bin_weights, band: FrequencyBand):
         raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {n_bins} bins")
     return per_bin_weights[:, band.lo_bin:band.hi_bin + 1].mean(axis=1) if isinstance(per_bin_weights, np.ndarray) \
         else per_bin_weights[:, band.lo_bin:band.hi_bin + 1].mean(dim=1)
+
+
+def pair_to_ij(p: np.ndarray, n: int):
+    """(i, j) of upper-triangle pair indices p (inverse of spectral.py:119-122)."""
+    p = np.asarray(p, dtype=np.int64)
+    i = np.floor((2 * n - 1 - np.sqrt((2.0 * n - 1) ** 2 - 8.0 * p)) / 2).astype(np.int64)
+    i = np.clip(i, 0, max(n - 2, 0))
+    start = i * (n - 1) - i * (i - 1) // 2
+    fix = start > p                      # guard the float sqrt at row boundaries
+    i[fix] -= 1
+    start = i * (n - 1) - i * (i - 1) // 2
+    nxt = (i + 1) * (n - 1) - (i + 1) * i // 2
+    fix = (nxt <= p) & (i + 1 < n - 1)
+    i[fix] += 1
+    start = i * (n - 1) - i * (i - 1) // 2
+    return i, p - start + i + 1
+
+
+def _is_device(t) -> bool:
+    try:
+        import torch
+        return isinstance(t, torch.Tensor) and t.is_cuda
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def normalize_network(net: ConnectivityNetwork) -> ConnectivityNetwork:
+    """Scale all edge weights by the maximum |weight| (core.py:168-181); an
+    all-zero network is returned unchanged apart from the flag.  Device weights
+    are normalised on the device (cs_net_normalize)."""
+    if net.n_edges < 1:
+        raise ParameterError("cannot normalize a network without edges")
+    if _is_device(net.weights_device):
+        import ctypes
+        import torch
+        from . import _lib
+        w = net.weights_device.to(torch.float32).clone()
+        cw = net._cw.to(torch.complex64).clone() if _is_device(net._cw) else None
+        with torch.cuda.device(w.device):
+            _lib.check(_lib.lib().cs_net_normalize(ctypes.c_void_p(w.data_ptr()),
+                                                   ctypes.c_void_p(cw.data_ptr()) if cw is not None else None,
+                                                   int(w.numel()),
+                                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return net._replace(weights=w, complex_weights=cw if cw is not None else net._cw, normalized=True)
+    wmax = float(np.max(np.abs(net.weights)))
+    if wmax == 0.0:
+        return net._replace(normalized=True)
+    cw = net.complex_weights / wmax if net.complex_weights is not None else None
+    return net._replace(weights=net.weights / wmax, complex_weights=cw, normalized=True)
+
+
+def threshold_network(net: ConnectivityNetwork, keep_fraction: float) -> ConnectivityNetwork:
+    """Keep the ceil(keep_fraction * n_edges) strongest edges by |weight|, ties
+    broken by ascending (i, j) (core.py:184-205).  Device weights are selected on
+    the device (cs_net_threshold: radix select + ordered compaction)."""
+    import math
+    if not (0.0 < keep_fraction <= 1.0):
+        raise ParameterError(f"keep_fraction must be in (0, 1], got {keep_fraction}")
+    n_keep = math.ceil(keep_fraction * net.n_edges)
+    if _is_device(net.weights_device):
+        import ctypes
+        import torch
+        from . import _lib
+        w = net.weights_device.to(torch.float32).contiguous()
+        idx = torch.empty(n_keep, dtype=torch.int64, device=w.device)
+        with torch.cuda.device(w.device):
+            _lib.check(_lib.lib().cs_net_threshold(ctypes.c_void_p(w.data_ptr()), int(w.numel()), int(n_keep),
+                                                   ctypes.c_void_p(idx.data_ptr()),
+                                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        pairs = idx if net._pairs is None else net._pairs[idx]
+        cw = net._cw[idx] if _is_device(net._cw) else (net.complex_weights[idx.cpu().numpy()]
+                                                      if net._cw is not None else None)
+        lags = None if net.lags is None else np.asarray(net.lags)[idx.cpu().numpy()]
+        return net._replace(weights=w[idx], complex_weights=cw, lags=lags, edge_i=None, edge_j=None, pairs=pairs)
+    order = np.lexsort((net.edge_j, net.edge_i, -np.abs(net.weights)))   # last key is primary
+    kept = np.sort(order[:n_keep])
+    return net._replace(weights=net.weights[kept], edge_i=net.edge_i[kept], edge_j=net.edge_j[kept],
+                        complex_weights=net.complex_weights[kept] if net.complex_weights is not None else None,
+                        lags=np.asarray(net.lags)[kept] if net.lags is not None else None, pairs=None)
+
+
+def serialize_network(net: ConnectivityNetwork) -> bytes:
+    """Canonical UTF-8 JSON (core.py:218-243): fixed key order, so
+    re-serialisation is byte-identical."""
+    import json
+    cw = net.complex_weights
+    lags = net.lags
+    ei, ej, w = net.edge_i, net.edge_j, net.weights
+    obj = {
+        "metric": net.metric.value,
+        "band": {"lo_bin": net.band.lo_bin, "hi_bin": net.band.hi_bin, "bin_hz": net.band.bin_hz},
+        "n_trials": net.n_trials,
+        "normalized": net.normalized,
+        "nodes": [{"id": int(nid), "pos": [float(x) for x in pos]} for nid, pos in zip(net.node_ids, net.positions)],
+        "edges": [{"i": int(ei[k]), "j": int(ej[k]), "w": float(w[k]),
+                   "w_im": float(cw[k].imag) if cw is not None else None,
+                   "lag": int(lags[k]) if lags is not None else None} for k in range(net.n_edges)],
+    }
+    return json.dumps(obj, separators=(",", ":")).encode("utf-8")

@@ -116,6 +116,18 @@ def main():
     T = info["trial_samples"]
     eps = np.array([data[:, m:m + T] for m in info["markers"]])
     run_case("sim2024_thresh", eps, 600, 15, 21)
+    # the reference's threshold fixture selections (export_threshold_fixtures.py:47-58),
+    # recomputed with the reference: normalised band networks, kept (i, j) sets
+    from connstream.core import normalize_network, threshold_network
+    rec2 = dict(np.load(OUT / "sim2024_thresh.npz"))
+    eps_m = [EpochMatrix(data=e, sfreq=1000.0, trial_index=k) for k, e in enumerate(eps)]
+    for nm in ("COH", "IMAGCOHY"):
+        dense = normalize_network(M.compute_metric(eps_m, MetricId[nm], 600, FrequencyBand(15, 21, 1.0)))
+        rec2["norm_" + nm] = dense.weights
+        for f in (0.05, 0.10, 0.25):
+            t = threshold_network(dense, f)
+            rec2[f"thresh_{nm}_{f:.2f}"] = np.stack([t.edge_i, t.edge_j], 1)
+    np.savez_compressed(OUT / "sim2024_thresh.npz", **rec2)
 
     # welch mode (spectral.py:264-283): 3 segments of 64 (T = 200, 8 samples dropped),
     # and a short-trial fallback to fixed mode (T < 2 nfft)

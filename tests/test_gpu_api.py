@@ -431,3 +431,49 @@ def test_running_sums_match_reference(case):
     sens = O.flush_sensitive([e.data for e in eps], nfft, 0, nfft // 2, mode=mode)
     assert np.array_equal(acc.pli_sum[~sens], ref.pli_sum[~sens])
     assert acc.n_trials_accumulated == len(eps)
+
+
+# ---------------------------------------------------------------- device network post-processing
+@pytest.mark.parametrize("P,ties", [(6, False), (5000, True), (3_000_000, True), (1_000_001, False)])
+def test_device_threshold_matches_host_semantics(P, ties):
+    """cs_net_threshold (radix select + ordered compaction) = the reference's
+    lexsort selection (core.py:184-205) on the same fp32 weights."""
+    from paper_2303_03279_b200.core import ConnectivityNetwork, pair_to_ij, threshold_network, normalize_network
+    rng = np.random.default_rng(P)
+    w = rng.standard_normal(P).astype(np.float32)
+    if ties:
+        w = np.round(w, 1).astype(np.float32)                 # many exact ties
+    n = int((1 + np.sqrt(1 + 8 * P)) / 2) + 1
+    while n * (n - 1) // 2 < P:
+        n += 1
+    wd = torch.tensor(w, device="cuda")
+    net = ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 2, tuple(range(n)), np.zeros((n, 3)), wd)
+    for f in (1e-6, 0.01, 0.37, 1.0):
+        k = int(np.ceil(f * P))
+        got = threshold_network(net, f)
+        order = np.lexsort((np.arange(P), -np.abs(w.astype(np.float64))))
+        want = np.sort(order[:k])
+        assert got.n_edges == k
+        assert np.array_equal(got._pairs.cpu().numpy(), want), f
+        wi, wj = pair_to_ij(want, n)
+        assert np.array_equal(got.edge_i, wi) and np.array_equal(got.edge_j, wj)
+        assert np.array_equal(got.weights, w[want].astype(np.float64))
+    nn = normalize_network(net)
+    np.testing.assert_allclose(nn.weights, w / np.abs(w).max(), rtol=1e-6)
+
+
+def test_threshold_fixture_selections_on_device():
+    """The reference's threshold fixture (normalised COH / IMAGCOHY networks and
+    their kept edge sets, regenerated from the reference into the golden file)
+    through compute_metric -> normalize_network -> threshold_network on the device."""
+    from conftest import GOLDEN
+    from paper_2303_03279_b200.core import normalize_network, threshold_network
+    g = np.load(GOLDEN / "sim2024_thresh.npz")
+    eps = [EpochMatrix(data=e, sfreq=600.0, trial_index=k) for k, e in enumerate(g["epochs"])]
+    for nm in ("COH", "IMAGCOHY"):
+        dense = normalize_network(M.compute_metric(eps, MetricId[nm], 600, FrequencyBand(15, 21, 1.0)))
+        assert np.abs(dense.weights - g["norm_" + nm]).max() <= 1e-4
+        for f in (0.05, 0.10, 0.25):
+            t = threshold_network(dense, f)
+            want = g[f"thresh_{nm}_{f:.2f}"]
+            assert np.array_equal(np.stack([t.edge_i, t.edge_j], 1), want), (nm, f)

@@ -6,7 +6,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ROOT
+from conftest import REFERENCE_SRC, ROOT
 
 from paper_2303_03279_b200 import _lib, synth
 from paper_2303_03279_b200.core import (DegenerateTrialCountError, EpochMatrix, FrequencyBand, MetricId,
@@ -102,3 +102,58 @@ def test_synthetic_generation_is_node_subset_stable():
     w = synth.generate(synth.CONFIGS[4], "cpu", nodes=slice(0, 8), trials=range(5, 10))
     v = synth.generate(synth.CONFIGS[4], "cpu", nodes=slice(0, 8), trials=range(0, 10))
     assert np.array_equal(w.numpy(), v[5:].numpy())
+
+
+# ---------------------------------------------------------------- network post-processing (core.py:168-243)
+def _net(w, n_nodes, cw=None, lags=None):
+    from paper_2303_03279_b200.core import ConnectivityNetwork
+    return ConnectivityNetwork(MetricId.COH, FrequencyBand(2, 5, 1.0), 3, tuple(range(n_nodes)),
+                               np.zeros((n_nodes, 3)), np.asarray(w, dtype=np.float64), complex_weights=cw, lags=lags)
+
+
+def test_pair_to_ij_inverts_triu_order():
+    from paper_2303_03279_b200.core import pair_to_ij
+    for n in (2, 3, 5, 64, 1001):
+        i, j = np.triu_indices(n, 1)
+        a, b = pair_to_ij(np.arange(len(i)), n)
+        assert np.array_equal(a, i) and np.array_equal(b, j)
+
+
+def test_host_threshold_and_normalize_semantics():
+    from paper_2303_03279_b200.core import normalize_network, threshold_network
+    w = np.array([0.5, -0.9, 0.5, 0.1, -0.5, 0.9])          # n = 4 nodes, 6 edges, ties
+    net = normalize_network(_net(w, 4))
+    assert net.normalized and np.allclose(net.weights, w / 0.9)
+    t = threshold_network(net, 0.5)                          # ceil(3): both 0.9s, then the first 0.5 tie
+    assert t.edge_i.tolist() == [0, 0, 2] and t.edge_j.tolist() == [1, 2, 3]
+    z = normalize_network(_net(np.zeros(3), 3))
+    assert z.normalized and np.all(z.weights == 0)
+    with pytest.raises(ParameterError):
+        threshold_network(net, 0.0)
+
+
+@pytest.mark.skipif(not (REFERENCE_SRC / "connstream").exists(), reason="reference not present (GPU box)")
+def test_post_processing_matches_reference_functions():
+    """Same inputs through the reference's own normalize/threshold/serialize."""
+    import sys
+    sys.path.insert(0, str(REFERENCE_SRC))
+    from connstream import core as RC
+    from paper_2303_03279_b200.core import normalize_network, serialize_network, threshold_network
+    rng = np.random.default_rng(3)
+    n = 23
+    P = n * (n - 1) // 2
+    w = np.round(rng.standard_normal(P), 2)                  # rounding makes ties
+    cw = w + 1j * np.round(rng.standard_normal(P), 2)
+    lags = rng.integers(-5, 5, P)
+    i, j = np.triu_indices(n, 1)
+    ref = RC.ConnectivityNetwork(RC.MetricId.COHY, RC.FrequencyBand(2, 5, 1.0), 3, tuple(range(n)),
+                                 np.zeros((n, 3)), i, j, w, complex_weights=cw, lags=lags)
+    ours = _net(w, n, cw=cw, lags=lags)
+    ours.metric = MetricId.COHY
+    for f in (0.05, 0.3, 1.0):
+        a = RC.threshold_network(RC.normalize_network(ref), f)
+        b = threshold_network(normalize_network(ours), f)
+        assert np.array_equal(a.edge_i, b.edge_i) and np.array_equal(a.edge_j, b.edge_j)
+        assert np.array_equal(a.weights, b.weights) and np.array_equal(a.complex_weights, b.complex_weights)
+        assert np.array_equal(a.lags, b.lags)
+        assert RC.serialize_network(a) == serialize_network(b)
