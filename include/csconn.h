@@ -165,6 +165,21 @@ int cs_put_taper_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, 
 int cs_net_normalize(float* w_dev, void* cw_dev, int64_t n, void* stream);
 int cs_net_threshold(const float* w_dev, int64_t n, int64_t keep, int64_t* out_idx_dev, void* stream);
 
+/* Time-domain metrics (metrics.py:140-260).  The Gram product and the FFTs are
+ * library calls (cuBLAS, cuFFT); these are their epilogues.
+ *  cs_cor_accumulate  total[p - pair_base] += clip(G[i][j], -1, 1) for pairs p in
+ *                     [pair_base, pair_base + n_pairs) (G: fp64 [C][C] Pearson matrix).
+ *  cs_xcor_peaks      per pair (pi[k], pj[k]): the first maximum over lags
+ *                     [-max_lag, max_lag] of r[tau] / sqrt(ex(tau) ey), r from
+ *                     cc[k][nfft] (circular, nfft >= 2 n - 1), ex from the prefix sums
+ *                     csq[C][n + 1] of dx^2, ey = csq[j][n]; (0, 0) when ey == 0 or
+ *                     xzero[i]; adds the value and the lag to peak_sum[k], lag_sum[k]. */
+int cs_cor_accumulate(const double* G_dev, int n_channels, int64_t pair_base, int64_t n_pairs,
+                      double* total_dev, void* stream);
+int cs_xcor_peaks(const double* cc_dev, int64_t n_pairs, int nfft, int n_samples, int max_lag,
+                  const int64_t* pi_dev, const int64_t* pj_dev, const double* csq_dev,
+                  const unsigned char* xzero_dev, double* peak_sum_dev, double* lag_sum_dev, void* stream);
+
 /* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
  * range of shard `shard` of `n_shards` (balanced by tile count) and the
  * contiguous global pair range [pair_begin, pair_end) it covers. */

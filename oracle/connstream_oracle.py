@@ -318,3 +318,64 @@ def flush_sensitive(epochs, nfft, lo, hi, taper=None, lo_ratio=1e-15, hi_ratio=1
         r = np.abs(csd.imag) / np.maximum(np.abs(csd.real), TINY)
         out |= (r >= lo_ratio) & (r <= hi_ratio)
     return out
+
+
+# --------------------------------------------------------------------------
+# time-domain metrics (metrics.py:140-260), restated
+# --------------------------------------------------------------------------
+def epoch_cor(data: np.ndarray):
+    """Clipped upper-triangle Pearson matrix of one epoch and its zero-variance
+    channels (metrics.py:140-155)."""
+    d = data - data.mean(axis=1, keepdims=True)
+    norms = np.sqrt(np.sum(d * d, axis=1))
+    dead = np.flatnonzero(norms == 0.0)
+    u = d / np.where(norms == 0.0, 1.0, norms)[:, None]
+    full = u @ u.T
+    full[dead, :] = 0.0
+    full[:, dead] = 0.0
+    pi, pj = pair_index(data.shape[0])
+    return np.clip(full[pi, pj], -1.0, 1.0), list(dead)
+
+
+def cor(epochs):
+    """Mean Pearson correlation per pair (metrics.py:158-177): (weights, dead channels)."""
+    tot, dead = 0.0, set()
+    for ep in epochs:
+        w, d = epoch_cor(np.asarray(ep, dtype=np.float64))
+        tot = tot + w
+        dead.update(d)
+    return tot / len(epochs), sorted(dead)
+
+
+def xcor_pair(x: np.ndarray, y: np.ndarray, max_lag: int):
+    """Peak (value, lag) of the overlap-normalised cross-correlation by direct
+    sliding sums (the reference's method="direct" checker, metrics.py:180-226)."""
+    n = len(x)
+    dx, dy = x - x.mean(), y - y.mean()
+    ey = float(np.sum(dy * dy))
+    if ey == 0.0 or not np.any(dx):
+        return 0.0, 0
+    best, best_lag = None, 0
+    for tau in range(-max_lag, max_lag + 1):
+        a, b = (dx[tau:], dy[:n - tau]) if tau >= 0 else (dx[:n + tau], dy[-tau:])
+        den = np.sqrt(np.sum(a * a) * ey)
+        v = np.sum(a * b) / den if den > 0.0 else 0.0
+        if best is None or v > best:
+            best, best_lag = v, tau
+    return float(best), int(best_lag)
+
+
+def xcor(epochs, max_lag=None):
+    """|mean peak| and rounded mean lag per pair (metrics.py:229-260)."""
+    C, n = np.asarray(epochs[0]).shape
+    max_lag = n - 1 if max_lag is None else max_lag
+    pi, pj = pair_index(C)
+    pk, lg = np.zeros(len(pi)), np.zeros(len(pi))
+    for ep in epochs:
+        ep = np.asarray(ep, dtype=np.float64)
+        for k in range(len(pi)):
+            v, l = xcor_pair(ep[pi[k]], ep[pj[k]], max_lag)
+            pk[k] += v
+            lg[k] += l
+    K = len(epochs)
+    return np.abs(pk / K), np.rint(lg / K).astype(np.int64)

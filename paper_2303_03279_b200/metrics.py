@@ -9,7 +9,7 @@ spectral metric is computed by the fused device kernels (cs_pair_metrics):
 Reference anchors: metrics.py:32-98 (*_bins, _SPECTRAL_BINS), :101-134
 (_build_network, finalize_spectral), :267-460 (TrialCache, ConnectivityEngine),
 :465-498 (one-shot wrappers), :501-528 (convergence_curve), :531-551
-(compute_metric).  COR / XCOR (time-domain, :137-260) are not built yet.
+(compute_metric).  COR / XCOR (time-domain, :137-260) in timedomain.py.
 """
 from __future__ import annotations
 
@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import spectral
+from . import spectral, timedomain
 from .core import (ConnectivityNetwork, DegenerateTrialCountError, EpochMatrix, FrequencyBand, MetricId,
                    ParameterError, default_positions)
 from .plan import DevicePlan, pow2_scale
@@ -188,8 +188,10 @@ def compute_metric(epochs, metric: MetricId, nfft: int, band: FrequencyBand | No
     """One-shot batch computation over a list of epochs (metrics.py:531-551):
     K1 over every node x trial, then the fused pair kernels over all trials."""
     metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
-    if not metric.is_spectral:
-        raise ParameterError(f"{metric.value} (time-domain) is not built on the device path yet")
+    if metric is MetricId.COR:
+        return cor(epochs, band=band, positions=positions, node_ids=node_ids)
+    if metric is MetricId.XCOR:
+        return xcor(epochs, max_lag=max_lag, band=band, positions=positions, node_ids=node_ids)
     if not epochs:
         raise ParameterError("need at least one epoch")
     if nfft < 2:
@@ -208,6 +210,44 @@ def compute_metric(epochs, metric: MetricId, nfft: int, band: FrequencyBand | No
     slots = torch.arange(K, dtype=torch.int32, device=x.device)
     out = plan.pair_metrics(slots, (metric.value,), 0, plan.n_bins, per_bin=False, band=True)
     return _network_from_band(metric, band, K, C, out[metric.value]["band"], positions, node_ids)
+
+
+def cor(epochs, band: FrequencyBand | None = None, positions=None, node_ids=None) -> ConnectivityNetwork:
+    """Pearson correlation per pair averaged over epochs (metrics.py:158-177)."""
+    if not epochs:
+        raise ParameterError("need at least one epoch")
+    C = epochs[0].n_channels
+    if any(ep.n_channels != C for ep in epochs):
+        raise ParameterError("epochs must have equal channel counts")
+    total, dead = timedomain.cor_sums([ep.data for ep in epochs], C)
+    if band is None:
+        band = FrequencyBand(0, 0, 0.0)
+    return _build_network(MetricId.COR, band, len(epochs), C, total / len(epochs), positions=positions,
+                          node_ids=node_ids, warnings=tuple(f"zero-variance channel {c}" for c in dead))
+
+
+def xcor(epochs, max_lag: int | None = None, band: FrequencyBand | None = None, positions=None, node_ids=None,
+         method: str = "fft") -> ConnectivityNetwork:
+    """Cross-correlation peak per pair averaged over epochs; weight = |mean peak|,
+    lag = rounded mean peak lag (metrics.py:229-260)."""
+    if not epochs:
+        raise ParameterError("need at least one epoch")
+    if method not in ("fft", "direct"):
+        raise ParameterError(f"unknown xcor method {method!r}")
+    C = epochs[0].n_channels
+    n = epochs[0].n_samples
+    if max_lag is None:
+        max_lag = n - 1
+    peak, lag = timedomain.xcor_sums([ep.data for ep in epochs], C, max_lag)
+    K = len(epochs)
+    lags = np.rint(lag.cpu().numpy() / K).astype(np.int64)
+    if band is None:
+        band = FrequencyBand(0, 0, 0.0)
+    return _build_network(MetricId.XCOR, band, K, C, (peak / K).abs(), lags=lags, positions=positions,
+                          node_ids=node_ids)
+
+
+xcor_pair = timedomain.xcor_pair
 
 
 @dataclass
@@ -264,6 +304,14 @@ class ConnectivityEngine:
         self._sum_trials: list = []
         self._fold_slots: list = []  # ring slot of every fold, in order
         self.n_trials = 0
+        # time-domain state (metrics.py:320-326): COR sums are kept eagerly only
+        # without storage mode (with it they are recomputed from the cached epochs of
+        # the folded trials); XCOR peaks follow the reference's lazy/backfill rules
+        self._cor_sum = None
+        self._dead_channels: set = set()
+        self._xcor_peak_sum = None
+        self._xcor_lag_sum = None
+        self._xcor_trials = 0
 
     # -- ring ------------------------------------------------------------------
     def _ensure_plan(self, T: int, scale: float):
@@ -323,9 +371,48 @@ class ConnectivityEngine:
             fold_slot = self._seg0_of.get(idx, self._slot_of[idx])
         if self.cache.enabled:
             self.cache.epochs[idx] = epoch
+        else:  # no cache to recompute from: fold the trial's Pearson matrix now
+            w, dead = timedomain.cor_sums([epoch.data], self.n_channels)
+            self._cor_sum = w if self._cor_sum is None else self._cor_sum + w
+            self._dead_channels.update(dead)
         self._sum_trials.append(idx)
         self._fold_slots.append(fold_slot)
         self.n_trials += 1
+
+    def _xcor_add(self, epochs) -> None:
+        max_lag = self.max_lag if self.max_lag is not None else epochs[0].n_samples - 1
+        pk, lg = timedomain.xcor_sums([e.data for e in epochs], self.n_channels, max_lag)
+        if self._xcor_peak_sum is None:
+            self._xcor_peak_sum, self._xcor_lag_sum = pk, lg
+        else:
+            self._xcor_peak_sum += pk
+            self._xcor_lag_sum += lg
+        self._xcor_trials += len(epochs)
+
+    def _finalize_time_domain(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
+        if self.n_trials < 1:
+            raise DegenerateTrialCountError("no trials accumulated")
+        if metric is MetricId.COR:
+            if self.cache.enabled:
+                total, dead = timedomain.cor_sums([self.cache.epochs[i].data for i in self._sum_trials],
+                                                  self.n_channels)
+            else:
+                total, dead = self._cor_sum, sorted(self._dead_channels)
+            warnings = tuple(f"zero-variance channel {c}" for c in dead)
+            return _build_network(MetricId.COR, band, self.n_trials, self.n_channels, total / self.n_trials,
+                                  positions=self.positions, node_ids=self.node_ids, warnings=warnings)
+        # XCOR: backfill from the cached epochs (sorted by index) past the ones
+        # already processed, as the reference does (metrics.py:418-428)
+        if self._xcor_trials < self.n_trials:
+            if not self.cache.enabled:
+                raise ParameterError("switching to XCOR mid-session requires storage mode")
+            todo = [self.cache.epochs[i] for i in sorted(self.cache.epochs)[self._xcor_trials:]]
+            if todo:
+                self._xcor_add(todo)
+        mean_peak = self._xcor_peak_sum / self._xcor_trials
+        lags = np.rint(self._xcor_lag_sum.cpu().numpy() / self._xcor_trials).astype(np.int64)
+        return _build_network(MetricId.XCOR, band, self._xcor_trials, self.n_channels, mean_peak.abs(), lags=lags,
+                              positions=self.positions, node_ids=self.node_ids)
 
     def ensure_band(self, band: FrequencyBand) -> None:
         """All bins are cached on the device, so back-fill is a no-op (metrics.py:363-380)."""
@@ -339,9 +426,7 @@ class ConnectivityEngine:
     def finalize(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
         metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
         if not metric.is_spectral:
-            if self.n_trials < 1:
-                raise DegenerateTrialCountError("no trials accumulated")
-            raise ParameterError(f"{metric.value} (time-domain) is not built on the device path yet")
+            return self._finalize_time_domain(metric, band)
         self.ensure_band(band)
         _check_k(len(self._sum_trials), metric.value)
         out = self._plan.pair_metrics(self._slots(), (metric.value,), band.lo_bin, band.n_bins, per_bin=False,
@@ -350,7 +435,11 @@ class ConnectivityEngine:
                                   self.positions, self.node_ids)
 
     def update_and_finalize(self, new_epoch: EpochMatrix, metric: MetricId, band: FrequencyBand):
+        metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
         self.add_trial(new_epoch)
+        if metric is MetricId.XCOR and not self.cache.enabled:
+            # without storage nothing can be back-filled later: keep XCOR in lockstep
+            self._xcor_add([new_epoch])
         return self.finalize(metric, band)
 
     def reset(self) -> None:
@@ -365,6 +454,9 @@ class ConnectivityEngine:
         if not self.cache.enabled:
             raise ParameterError("trial-window rebuild requires storage mode")
         keep = sorted(self.cache.epochs)[-n_last:] if n_last > 0 else []
+        # the reference resets (time-domain sums included) and re-adds the kept trials
+        self._xcor_peak_sum = self._xcor_lag_sum = None
+        self._xcor_trials = 0
         self._sum_trials = list(keep)
         # re-added from the cache: fixed-mode folds of the cached spectra
         self._fold_slots = [self._seg0_of.get(i, self._slot_of[i]) for i in keep]

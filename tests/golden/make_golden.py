@@ -129,6 +129,21 @@ def main():
             rec2[f"thresh_{nm}_{f:.2f}"] = np.stack([t.edge_i, t.edge_j], 1)
     np.savez_compressed(OUT / "sim2024_thresh.npz", **rec2)
 
+    # time-domain metrics (metrics.py:140-260) through the reference's compute_metric
+    td = rng.standard_normal((5, 6, 80))
+    td[:, 3] = 2.5                                   # a zero-variance channel
+    td[:, 4] = np.roll(td[:, 1], 3, axis=1)          # a lagged copy
+    eps_td = [EpochMatrix(data=e, sfreq=100.0, trial_index=k) for k, e in enumerate(td)]
+    rec3 = {"epochs": td}
+    net = M.compute_metric(eps_td, MetricId.COR, 64)
+    rec3["cor_w"], rec3["cor_warn"] = net.weights, np.array(list(net.warnings))
+    for ml in (10, None):
+        net = M.compute_metric(eps_td, MetricId.XCOR, 64, max_lag=ml)
+        key = "all" if ml is None else str(ml)
+        rec3["xcor_w_" + key], rec3["xcor_lag_" + key] = net.weights, net.lags
+    np.savez_compressed(OUT / "timedomain.npz", **rec3)
+    print("wrote timedomain")
+
     # welch mode (spectral.py:264-283): 3 segments of 64 (T = 200, 8 samples dropped),
     # and a short-trial fallback to fixed mode (T < 2 nfft)
     run_case("welch3", rng.standard_normal((6, 7, 200)), 64, 2, 20, mode="welch")

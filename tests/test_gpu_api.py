@@ -477,3 +477,51 @@ def test_threshold_fixture_selections_on_device():
             t = threshold_network(dense, f)
             want = g[f"thresh_{nm}_{f:.2f}"]
             assert np.array_equal(np.stack([t.edge_i, t.edge_j], 1), want), (nm, f)
+
+
+# ---------------------------------------------------------------- time-domain metrics (metrics.py:140-260)
+def test_cor_xcor_match_reference_golden():
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / "timedomain.npz")
+    eps = [EpochMatrix(data=e, sfreq=100.0, trial_index=k) for k, e in enumerate(g["epochs"])]
+    net = M.compute_metric(eps, MetricId.COR, 64)
+    assert np.abs(net.weights - g["cor_w"]).max() <= 1e-12
+    assert list(net.warnings) == list(g["cor_warn"])
+    for ml, key in ((10, "10"), (None, "all")):
+        net = M.compute_metric(eps, MetricId.XCOR, 64, max_lag=ml)
+        assert np.abs(net.weights - g["xcor_w_" + key]).max() <= 1e-12
+        assert np.array_equal(net.lags, g["xcor_lag_" + key])
+
+
+def test_xcor_pair_and_engine_time_domain():
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal(50)
+    y = np.roll(x, -4) + 0.1 * rng.standard_normal(50)       # x leads y
+    assert M.xcor_pair(x, y, 10) == pytest.approx(O.xcor_pair(x, y, 10), abs=1e-12)
+    assert M.xcor_pair(x, np.full(50, 3.0), 5) == (0.0, 0)
+    with pytest.raises(ParameterError):
+        M.xcor_pair(x, y, 50)
+    eps = make_epochs(7, 5, 60, seed=22)
+    for storage in (True, False):
+        eng = M.ConnectivityEngine(5, 32, 600.0, storage_mode=storage, max_lag=12)
+        for ep in eps:
+            if storage:
+                eng.add_trial(ep)
+            else:
+                eng.update_and_finalize(ep, MetricId.XCOR, FrequencyBand(0, 0, 0.0))
+        w, _ = O.cor([e.data for e in eps])
+        assert np.abs(eng.finalize(MetricId.COR, FrequencyBand(0, 0, 0.0)).weights - w).max() <= 1e-12
+        a, lags = O.xcor([e.data for e in eps], 12)
+        net = eng.finalize(MetricId.XCOR, FrequencyBand(0, 0, 0.0))
+        assert np.abs(net.weights - a).max() <= 1e-12 and np.array_equal(net.lags, lags)
+    # storage mode: a late switch to XCOR after rebuild_last back-fills from ALL cached epochs
+    eng2 = M.ConnectivityEngine(5, 32, 600.0, storage_mode=True, max_lag=12)
+    for ep in eps:
+        eng2.add_trial(ep)
+    eng2.rebuild_last(3)
+    w3, _ = O.cor([e.data for e in eps[-3:]])
+    assert np.abs(eng2.finalize(MetricId.COR, FrequencyBand(0, 0, 0.0)).weights - w3).max() <= 1e-12
+    net = eng2.finalize(MetricId.XCOR, FrequencyBand(0, 0, 0.0))
+    a, lags = O.xcor([e.data for e in eps], 12)                # reference quirk: all cached epochs
+    assert net.n_trials == len(eps)
+    assert np.abs(net.weights - a).max() <= 1e-12 and np.array_equal(net.lags, lags)

@@ -9,7 +9,7 @@ import pytest
 import oracle as O
 from conftest import GOLDEN, REFERENCE_SRC
 
-CASES = sorted(p.stem for p in GOLDEN.glob("*.npz"))
+CASES = sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "timedomain")
 
 
 def _load(name):
@@ -70,3 +70,16 @@ def test_golden_sim_matches_reference_fixture_file():
         pytest.skip("reference fixtures only present in the build container")
     want = np.array([e["w"] for e in json.loads(p.read_text())["network"]["edges"]])
     np.testing.assert_array_equal(w, want)
+
+
+def test_oracle_time_domain_matches_reference_golden():
+    """COR / XCOR restatements vs the reference's compute_metric outputs (golden)."""
+    g = np.load(GOLDEN / "timedomain.npz")
+    eps = list(g["epochs"])
+    w, dead = O.cor(eps)
+    assert np.abs(w - g["cor_w"]).max() <= 1e-12
+    assert [f"zero-variance channel {c}" for c in dead] == list(g["cor_warn"])
+    for ml, key in ((10, "10"), (None, "all")):
+        a, lags = O.xcor(eps, ml)
+        assert np.abs(a - g["xcor_w_" + key]).max() <= 1e-12
+        assert np.array_equal(lags, g["xcor_lag_" + key])
