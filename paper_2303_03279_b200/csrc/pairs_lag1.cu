@@ -139,14 +139,19 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 
   f2 sim[k1NP];
   float sabs[k1NP], mn[k1NP];
-  int neg[k1NP];
+  // #(t < 0), two trials per PRMT: the sign bytes of (t_a, t_b) replicated into
+  // 0x0000FFFF [t_a < 0] + 0xFFFF0000 [t_b < 0]; two trial pairs are added with one
+  // IADD3 (3 instructions per 4 trials instead of 4 LEA.HI).  Decoded exactly in
+  // the epilogue: A = -acc mod 2^16, B = (65535 A - acc) >> 16 (counts < 2^16).
+  unsigned neg[k1NP], ntmp[k1NP];
   f2 pvr[PLVK ? k1NP : 1], pvi[PLVK ? k1NP : 1];
 #pragma unroll
   for (int p = 0; p < k1NP; ++p) {
     sim[p] = 0ull;
     sabs[p] = 0.f;
     mn[p] = 3.0e38f;
-    neg[p] = 0;
+    neg[p] = 0u;
+    ntmp[p] = 0u;
     if (PLVK) pvr[p] = pvi[p] = 0ull;
   }
 
@@ -162,13 +167,20 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
     const int nkp = min(kc, a.Kp - st * kc);
-    auto stats = [&](int p, f2 tt) {
+    auto stats = [&](int p, f2 tt, int odd) {
       sim[p] = fadd2(sim[p], tt);
       const float tl = lo_of(tt), th = hi_of(tt);
       sabs[p] += fabsf(tl);
       sabs[p] += fabsf(th);
-      neg[p] += (int)(__float_as_uint(tl) >> 31);
-      neg[p] += (int)(__float_as_uint(th) >> 31);
+      if (L == 1) {
+        unsigned r;
+        asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(r) : "r"(__float_as_uint(tl)), "r"(__float_as_uint(th)));
+        if (odd) neg[p] += ntmp[p] + r;
+        else ntmp[p] = r;
+      } else {  // multitaper: registers are tighter, plain counts (LEA.HI)
+        neg[p] += __float_as_uint(tl) >> 31;
+        neg[p] += __float_as_uint(th) >> 31;
+      }
       mn[p] = fminf(mn[p], fminf(fabsf(tl), fabsf(th)));
     };
     auto body = [&](int kp) {
@@ -184,7 +196,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 #pragma unroll
           for (int c = 0; c < k1TC; ++c) {
             const f2 jr = pk(xj[c].x, xj[c].y), jn = pk(xj[c].z, xj[c].w);
-            stats(r * k1TC + c, ffma2(ii, jr, fmul2(ir, jn)));  // Im(X_i conj X_j), trials a, b
+            stats(r * k1TC + c, ffma2(ii, jr, fmul2(ir, jn)), kp & 1);  // Im(X_i conj X_j), trials a, b
           }
         }
       } else {
@@ -213,7 +225,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
                 re2 = ffma2(ii, jn, re2);
               }
             }
-            stats(p, tt);
+            stats(p, tt, kp & 1);
             if (PLVK) {  // unit phasor of the trial's taper-mean CSD
               f2 re;
               asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(re) : "l"(re1), "l"(re2));
@@ -231,6 +243,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     };
 #pragma unroll 2
     for (int kp = 0; kp < nkp; ++kp) body(kp);
+    if (L == 1 && (nkp & 1)) {  // the stage's last trial pair had no partner
+#pragma unroll
+      for (int p = 0; p < k1NP; ++p) neg[p] += ntmp[p];
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (st + 1 < n_stage) continue;
@@ -283,7 +299,9 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const float tph = phI[r] * phJ[c];  // odd-K phantom trial (0 when K is even)
         const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
         const float s_abs = dead ? 0.f : sabs[p] - tph;
-        const int pli_sum = dead ? 0 : a.K - 2 * neg[p];
+        const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
+        const int n_neg = L == 1 ? (int)(nA + nB) : (int)neg[p];
+        const int pli_sum = dead ? 0 : a.K - 2 * n_neg;
         float v[5];
         v[0] = s_im * rPi[r] * rPj[c];
         const float pli = fabsf((float)pli_sum) * invK;
@@ -314,7 +332,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         sim[p] = 0ull;
         sabs[p] = 0.f;
         mn[p] = 3.0e38f;
-        neg[p] = 0;
+        neg[p] = 0u;
       }
     }
   }
