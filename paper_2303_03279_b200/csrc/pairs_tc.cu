@@ -19,8 +19,8 @@
 //   warp 1: single-thread tcgen05.mma issuer, tcgen05.commit to mbarriers
 //   warp 2: TMEM allocator (512 columns: pass 0 -> [0,128), pass 1 -> [128,256),
 //           band-mean accumulators -> [256,512))
-//   warps 4-11: epilogue (tcgen05.ld/st 32x32b; TMEM lane quadrant = warp % 4,
-//           two warps per quadrant split the 64 columns),
+//   warps 4-19: epilogue (tcgen05.ld/st 32x32b.x8; TMEM lane quadrant = warp % 4,
+//           four warps per quadrant split the 64 columns; 96 registers each),
 //           per-bin values leave through a shared-memory transpose buffer as
 //           coalesced row stores; band means accumulate in TMEM across bins.
 // The two passes use disjoint TMEM regions, so the epilogue of one pass overlaps
@@ -43,8 +43,10 @@ constexpr int kTcPlaneA = kTcTile * kTcChunk * 2;       // 8 KB
 constexpr int kTcPlaneB = kTcTileJ * kTcChunk * 2;      // 4 KB
 constexpr int kTcStageBytes = 4 * kTcPlaneA + 4 * kTcPlaneB;  // 48 KB
 constexpr int kTcXStride = kTcTileJ + 1;                // transpose buffer row stride (float2)
-constexpr int kTcThreads = 384;   // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-11: epilogue
-constexpr int kTcEpiWarps = 8;
+constexpr int kTcEpiWarps = 16;   // 4 per TMEM lane quadrant
+constexpr int kTcThreads = (4 + kTcEpiWarps) * 32;  // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-19: epilogue
+constexpr int kTcColsPerWarp = kTcTileJ / (kTcEpiWarps / 4);  // TMEM-phase columns per epilogue warp (16)
+constexpr int kTcRowsPerWarp = kTcTile / kTcEpiWarps;         // store-phase rows per epilogue warp (8)
 // TMEM columns: [0,128) pass-0 accumulators (re | im), [128,256) pass-1,
 // [256,512) band sums: COH, PLV, COHY re, COHY im (64 each)
 constexpr int kTmBand = 256;
@@ -113,6 +115,38 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float* v, uint32_t tb, 
     v[q] = __uint_as_float(r[q]);
     w[q] = __uint_as_float(s[q]);
   }
+}
+
+// 8-column variants (16 epilogue warps: 96 registers per thread)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
+}
+__device__ __forceinline__ void tmem_ld8x2(uint32_t ta, float* v, uint32_t tb, float* w) {
+  uint32_t r[8], s[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(ta));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]), "=r"(s[7])
+               : "r"(tb));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    v[q] = __uint_as_float(r[q]);
+    w[q] = __uint_as_float(s[q]);
+  }
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
 }
 
 // K-major operand tile [128 rows x 32 fp16] written by TMA with SWIZZLE_64B:
@@ -287,10 +321,10 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    // warp e = warp - 4: TMEM lane quadrant q = warp % 4 (hardware rule), column half h
+    // warp e = warp - 4: TMEM lane quadrant q = warp % 4 (hardware rule), column group h
     const int e = warp - 4, q = warp & 3, h = e >> 2;
     const int r = q * 32 + lane;             // tile row owned in the TMEM phase
-    const int cb = h * 32;                   // first tile column owned in the TMEM phase
+    const int cb = h * kTcColsPerWarp;       // first tile column owned in the TMEM phase
     const float inv_nb = 1.f / (float)a.nbb;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const int et = e * 32 + lane;            // 0..255 within the epilogue group
@@ -340,14 +374,14 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         tc_fence_after();
         const uint32_t t_acc = tmem + lane_addr + reg * 128;
 #pragma unroll
-        for (int c1 = 0; c1 < 32; c1 += 16) {
+        for (int c1 = 0; c1 < kTcColsPerWarp; c1 += 8) {
           const int c0 = cb + c1;
-          float vr[16], vi[16];
-          tmem_ld16x2(t_acc + c0, vr, t_acc + 64 + c0, vi);
+          float vr[8], vi[8];
+          tmem_ld8x2(t_acc + c0, vr, t_acc + 64 + c0, vi);
           if (TC_ABL(2)) { sts_f2(xrow + c0 * 8u, vr[3], vi[5]); continue; }
           if (pass == 0) {
 #pragma unroll
-            for (int u4 = 0; u4 < 16; u4 += 4) {
+            for (int u4 = 0; u4 < 8; u4 += 4) {
               const float4 cf = lds_f4(cfb + (uint32_t)(c0 + u4) * 4u);
               const float rs[4] = {rsi * cf.x, rsi * cf.y, rsi * cf.z, rsi * cf.w};
 #pragma unroll
@@ -372,54 +406,54 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               }
             }
             if (a.coh_band || !cohy) {
-              float m[16];
+              float m[8];
 #pragma unroll
-              for (int u = 0; u < 16; ++u) m[u] = sqrt_approx(vr[u] * vr[u] + vi[u] * vi[u]);
+              for (int u = 0; u < 8; ++u) m[u] = sqrt_approx(vr[u] * vr[u] + vi[u] * vi[u]);
               if (!cohy)
 #pragma unroll
-                for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, m[u], vi[u]);
+                for (int u = 0; u < 8; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, m[u], vi[u]);
               if (a.coh_band) {
-                float b[16];
-                if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + c0, b);
+                float b[8];
+                if (acc_band) tmem_ld8(tmem + lane_addr + kTmBand + c0, b);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) b[u] = acc_band ? fmaf(m[u], inv_nb, b[u]) : m[u] * inv_nb;
-                tmem_st16(tmem + lane_addr + kTmBand + c0, b);
+                for (int u = 0; u < 8; ++u) b[u] = acc_band ? fmaf(m[u], inv_nb, b[u]) : m[u] * inv_nb;
+                tmem_st8(tmem + lane_addr + kTmBand + c0, b);
               }
             }
             if (a.imag_band && !a.cohy_band) {  // IMAGCOHY band mean in the COHY-im columns
-              float bi[16];
-              if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+              float bi[8];
+              if (acc_band) tmem_ld8(tmem + lane_addr + kTmBand + 192 + c0, bi);
 #pragma unroll
-              for (int u = 0; u < 16; ++u) bi[u] = acc_band ? fmaf(vi[u], inv_nb, bi[u]) : vi[u] * inv_nb;
-              tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+              for (int u = 0; u < 8; ++u) bi[u] = acc_band ? fmaf(vi[u], inv_nb, bi[u]) : vi[u] * inv_nb;
+              tmem_st8(tmem + lane_addr + kTmBand + 192 + c0, bi);
             }
             if (cohy) {
 #pragma unroll
-              for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, vr[u], vi[u]);
+              for (int u = 0; u < 8; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, vr[u], vi[u]);
               if (a.cohy_band) {
-                float br[16], bi[16];
-                if (acc_band) tmem_ld16x2(tmem + lane_addr + kTmBand + 128 + c0, br, tmem + lane_addr + kTmBand + 192 + c0, bi);
+                float br[8], bi[8];
+                if (acc_band) tmem_ld8x2(tmem + lane_addr + kTmBand + 128 + c0, br, tmem + lane_addr + kTmBand + 192 + c0, bi);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
+                for (int u = 0; u < 8; ++u) {
                   br[u] = acc_band ? fmaf(vr[u], inv_nb, br[u]) : vr[u] * inv_nb;
                   bi[u] = acc_band ? fmaf(vi[u], inv_nb, bi[u]) : vi[u] * inv_nb;
                 }
-                tmem_st16(tmem + lane_addr + kTmBand + 128 + c0, br);
-                tmem_st16(tmem + lane_addr + kTmBand + 192 + c0, bi);
+                tmem_st8(tmem + lane_addr + kTmBand + 128 + c0, br);
+                tmem_st8(tmem + lane_addr + kTmBand + 192 + c0, bi);
               }
             }
           } else {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < 8; ++u) {
               vr[u] = sqrt_approx(vr[u] * vr[u] + vi[u] * vi[u]) * a.invK;
               sts_f32(xrow + (uint32_t)(c0 + u) * 8u, vr[u]);
             }
             if (a.plv_band) {
-              float b[16];
-              if (acc_band) tmem_ld16(tmem + lane_addr + kTmBand + 64 + c0, b);
+              float b[8];
+              if (acc_band) tmem_ld8(tmem + lane_addr + kTmBand + 64 + c0, b);
 #pragma unroll
-              for (int u = 0; u < 16; ++u) b[u] = acc_band ? fmaf(vr[u], inv_nb, b[u]) : vr[u] * inv_nb;
-              tmem_st16(tmem + lane_addr + kTmBand + 64 + c0, b);
+              for (int u = 0; u < 8; ++u) b[u] = acc_band ? fmaf(vr[u], inv_nb, b[u]) : vr[u] * inv_nb;
+              tmem_st8(tmem + lane_addr + kTmBand + 64 + c0, b);
             }
           }
         }
@@ -429,19 +463,19 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[reg]);
         epi_bar();
-        // per-bin outputs: warp e stores rows [16 e, 16 e + 16), 64 contiguous pairs each;
+        // per-bin outputs: warp e stores rows [8 e, 8 e + 8), 64 contiguous pairs each;
         // four rows per group, all shared loads of a group issued before its stores
         if (!TC_ABL(1)) {
           float* const px = pass == 0 ? a.coh_bins : a.plv_bins;   // .x: COH (or |COHY|) / PLV
           float* const py = pass == 0 ? a.imag_bins : nullptr;     // .y: IMAGCOHY
           float2* const pc = (pass == 0 && cohy) ? a.cohy_bins : nullptr;
           const bool magx = pass == 0 && cohy;                     // buffer holds COHY: COH = |.|
-          for (int g = 0; g < 16; g += 4) {
+          for (int g = 0; g < kTcRowsPerWarp; g += 4) {
             long long ro[4];
             float2 v0[4], v1[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const int row = e * 16 + g + t;
+              const int row = e * kTcRowsPerWarp + g + t;
               ro[t] = lds_s64(rob + (uint32_t)row * 8u);
               const uint32_t xa = xb + (uint32_t)(row * kTcXStride + lane) * 8u;
               v0[t] = lds_f2(xa);
@@ -449,7 +483,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const int row = e * 16 + g + t;
+              const int row = e * kTcRowsPerWarp + g + t;
               const int clo = iBase + row + 1 - jBase;
               const bool live = ro[t] != INT64_MIN;
               const bool ok0 = live && lane >= clo && lane < chi;
@@ -483,19 +517,19 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             (kind == 3 && (!a.imag_band || a.cohy_band)))
           continue;
 #pragma unroll
-        for (int c1 = 0; c1 < 32; c1 += 16) {
+        for (int c1 = 0; c1 < kTcColsPerWarp; c1 += 8) {
           const int c0 = cb + c1;
-          float b0[16], b1[16];
+          float b0[8], b1[8];
           const uint32_t col = kTmBand + (kind >= 2 ? (kind == 3 ? 192 : 128) : kind * 64) + c0;
-          if (kind == 2) tmem_ld16x2(tmem + lane_addr + col, b0, tmem + lane_addr + kTmBand + 192 + c0, b1);
-          else tmem_ld16(tmem + lane_addr + col, b0);
+          if (kind == 2) tmem_ld8x2(tmem + lane_addr + col, b0, tmem + lane_addr + kTmBand + 192 + c0, b1);
+          else tmem_ld8(tmem + lane_addr + col, b0);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, b0[u], kind == 2 ? b1[u] : 0.f);
+          for (int u = 0; u < 8; ++u) sts_f2(xrow + (uint32_t)(c0 + u) * 8u, b0[u], kind == 2 ? b1[u] : 0.f);
         }
         epi_bar();
         float* dst1 = kind == 0 ? a.coh_band : (kind == 1 ? a.plv_band : a.imag_band);
-        for (int rr = 0; rr < 16; ++rr) {
-          const int row = e * 16 + rr;
+        for (int rr = 0; rr < kTcRowsPerWarp; ++rr) {
+          const int row = e * kTcRowsPerWarp + rr;
           const long long ro = lds_s64(rob + (uint32_t)row * 8u);
           if (ro == INT64_MIN) continue;
           const int clo = iBase + row + 1 - jBase;
