@@ -251,6 +251,34 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   }
   cudaMemcpy(p->tww, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
   cudaMemcpy(p->wsum, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  // tensor-core DFT: B fragments of mma.m8n8k4.f64 in lane order; columns 2b, 2b+1 =
+  // taper x twiddle (Re, Im) of bin b, column 2 nb = 1 (untapered sample sum)
+  if (!p->use_fft && 2 * p->nb + 1 <= 24 && !(getenv("CSCONN_DFT") && getenv("CSCONN_DFT")[0] == 'f')) {
+    const int NT = (2 * p->nb + 1 + 7) / 8, nks = (p->T_eff + 3) / 4;
+    std::vector<double> tf((size_t)L * nks * NT * 32, 0.0);
+    for (int l = 0; l < L; ++l)
+      for (int kk = 0; kk < nks; ++kk)
+        for (int nt = 0; nt < NT; ++nt)
+          for (int ln = 0; ln < 32; ++ln) {
+            const int t = 4 * kk + (ln & 3), col = nt * 8 + (ln >> 2);
+            double v = 0.0;
+            if (t < p->T_eff) {
+              if (col < 2 * p->nb) {
+                const double2 w = tw[((size_t)l * p->nb + col / 2) * p->T_eff + t];
+                v = (col & 1) ? w.y : w.x;
+              } else if (col == 2 * p->nb) {
+                v = 1.0;
+              }
+            }
+            tf[(((size_t)l * nks + kk) * NT + nt) * 32 + ln] = v;
+          }
+    if (cudaMalloc(&p->dft_tf, tf.size() * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      p->dft_tf = nullptr;  // the DFMA kernel needs no extra table
+    } else {
+      cudaMemcpy(p->dft_tf, tf.data(), tf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
   if (p->use_fft) {
     const int M = nfft / 2;
     std::vector<double2> ft(M / 2 > 0 ? M / 2 : 1), pt(M + 1);
@@ -313,7 +341,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
 int cs_plan_destroy(cs_plan* p) {
   if (!p) return CS_OK;
   DeviceGuard g(p->device);
-  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->fft4_tw); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
+  cudaFree(p->tww); cudaFree(p->wsum); cudaFree(p->taper); cudaFree(p->fft_tw); cudaFree(p->post_tw); cudaFree(p->fft4_tw); cudaFree(p->dft_tf); cudaFree(p->X64); cudaFree(p->X32); cudaFree(p->psd); cudaFree(p->mag); cudaFree(p->nscale);
   if (p->tc_ops) cudaFree(p->tc_ops);
   for (auto& e : p->tc_tiles)
     if (e.ptr) cudaFree(e.ptr);

@@ -28,6 +28,7 @@ struct Plan {
   double2* fft4_tw = nullptr;    // [A][32] W_M^{b k_a}, then [32] W_32^j       -- four-step FFT (M = 32 A)
   bool use_fft = false;          // power-of-two nfft and a band wide enough to prefer the FFT
   int seg_stride = 0;            // welch: sample offset between segments (= nfft), else 0
+  double* dft_tf = nullptr;      // [L][ceil(T_eff/4)][NT][32] fp64 DFT B fragments (tensor-core DFT), or null
   double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
   float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra
   float* psd = nullptr;          // [nb][N] per-call node statistics
