@@ -241,7 +241,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         }
       }
     };
-#pragma unroll 2
+    constexpr int kUnroll = L == 1 ? 2 : 1;  // multitaper: one trial pair at a time (registers)
+#pragma unroll kUnroll
     for (int kp = 0; kp < nkp; ++kp) body(kp);
     if (L == 1 && (nkp & 1)) {  // the stage's last trial pair had no partner
 #pragma unroll
