@@ -525,3 +525,41 @@ def test_xcor_pair_and_engine_time_domain():
     a, lags = O.xcor([e.data for e in eps], 12)                # reference quirk: all cached epochs
     assert net.n_trials == len(eps)
     assert np.abs(net.weights - a).max() <= 1e-12 and np.array_equal(net.lags, lags)
+
+
+# ---------------------------------------------------------------- upstream
+@pytest.mark.parametrize("taper", [None, "hann", ("dpss", 2.0, 3)])
+def test_source_connectivity_projects_the_spectra(taper):
+    """K1 on sensors + spectral projection = the reference path on M @ x."""
+    from paper_2303_03279_b200.plan import make_taper
+    from paper_2303_03279_b200.upstream import source_connectivity
+    rng = np.random.default_rng(31)
+    K, C, T, Ns, nfft, lo, hi = 8, 6, 96, 11, 128, 3, 20
+    x = rng.standard_normal((K, C, T))
+    Mx = rng.standard_normal((Ns, C))
+    out, _ = source_connectivity(torch.tensor(x, device="cuda"), Mx, nfft, lo, hi, taper=taper)
+    tp = make_taper(taper, min(T, nfft))
+    tp = None if tp is None else (tp[0] if tp.shape[0] == 1 else tp)
+    want, _ = O.compute([Mx @ e for e in x], nfft, lo, hi, taper=tp)
+    for m in ("COH", "IMAGCOHY", "PLV", "PLI", "WPLI"):
+        got = out[m]["bins"].T.cpu().numpy()
+        assert np.abs(got - want[m]["bins"]).max() <= TOL[m], m
+
+
+def test_apply_inverse_and_overlap_add_filter():
+    from paper_2303_03279_b200.upstream import OverlapAddFilter, apply_inverse, filter_offline
+    rng = np.random.default_rng(32)
+    M_ = rng.standard_normal((9, 4))
+    ep = EpochMatrix(data=rng.standard_normal((4, 50)), sfreq=100.0, trial_index=3)
+    src = apply_inverse(M_, ep)
+    np.testing.assert_allclose(src.data.cpu().numpy(), M_ @ ep.data, atol=1e-12)
+    assert src.trial_index == 3
+    taps = rng.standard_normal(21)
+    sig = rng.standard_normal((3, 257))
+    want = np.stack([np.convolve(s, taps)[:257] for s in sig])
+    f = OverlapAddFilter(taps)
+    got = np.concatenate([f.process(sig[:, a:b]).cpu().numpy() for a, b in ((0, 40), (40, 41), (41, 200), (200, 257))], 1)
+    np.testing.assert_allclose(got, want, atol=1e-10)
+    np.testing.assert_allclose(filter_offline(taps, sig).cpu().numpy(), want, atol=1e-10)
+    with pytest.raises(ParameterError):
+        f.process(sig[:2, :5])
