@@ -51,7 +51,11 @@ struct Lag1Args {
 // then allows 96 registers, enough for the single-taper loop); L > 1 needs 128
 // registers, so 16 warps with the TMA issued from warp 0 (measured: the dedicated
 // warp is 2.7 % faster for L == 1 on cfg5).
-template <int L, bool PLVK>
+// STATS: which per-pair trial statistics the requested metrics need (the exact-sign
+// guard min |t| is always kept): 1 = #(t < 0) (PLI, USPLI), 2 = sum t (IMAGCOHY, WPLI,
+// DSWPLI), 4 = sum |t| (WPLI, DSWPLI).  Single taper only; multitaper runs all.
+constexpr unsigned kStSign = 1, kStSum = 2, kStAbs = 4, kStAll = 7;
+template <int L, bool PLVK, unsigned STATS = kStAll>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -168,11 +172,14 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     const float4* sJ = XJ + s * k1StageF4;
     const int nkp = min(kc, a.Kp - st * kc);
     auto stats = [&](int p, f2 tt, int odd) {
-      sim[p] = fadd2(sim[p], tt);
+      if (STATS & kStSum) sim[p] = fadd2(sim[p], tt);
       const float tl = lo_of(tt), th = hi_of(tt);
-      sabs[p] += fabsf(tl);
-      sabs[p] += fabsf(th);
-      if (L == 1) {
+      if (STATS & kStAbs) {
+        sabs[p] += fabsf(tl);
+        sabs[p] += fabsf(th);
+      }
+      if (!(STATS & kStSign)) {
+      } else if (L == 1) {
         unsigned r;
         asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(r) : "r"(__float_as_uint(tl)), "r"(__float_as_uint(th)));
         if (odd) neg[p] += ntmp[p] + r;
@@ -244,7 +251,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     constexpr int kUnroll = L == 1 ? 2 : 1;  // multitaper: one trial pair at a time (registers)
 #pragma unroll kUnroll
     for (int kp = 0; kp < nkp; ++kp) body(kp);
-    if (L == 1 && (nkp & 1)) {  // the stage's last trial pair had no partner
+    if (L == 1 && (STATS & kStSign) && (nkp & 1)) {  // the stage's last trial pair had no partner
 #pragma unroll
       for (int p = 0; p < k1NP; ++p) neg[p] += ntmp[p];
     }
@@ -406,6 +413,15 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
   const unsigned grid = (unsigned)(n_tiles * nbc);
   const bool plvk = plv_bins || plv_band;
+#define CS_LAG1S(LL, PV, SS)                                                                           \
+  do {                                                                                                   \
+    static bool cfg = false;                                                                             \
+    if (!cfg) {                                                                                          \
+      cudaFuncSetAttribute(k_pairs_lag1<LL, PV, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cfg = true;                                                                                        \
+    }                                                                                                    \
+    k_pairs_lag1<LL, PV, SS><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);        \
+  } while (0)
 #define CS_LAG1(LL, PV)                                                                              \
   do {                                                                                                   \
     static bool cfg = false;                                                                             \
@@ -416,7 +432,17 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
   } while (0)
   if (L == 1) {
-    CS_LAG1(1, false);
+    // statistics the requested outputs need (bins / band pointers: IMAG, PLI, USPLI, WPLI, DSWPLI)
+    auto want = [&](int m) { return bins[m] || band[m]; };
+    const unsigned need = ((want(1) || want(2)) ? kStSign : 0u) | ((want(0) || want(3) || want(4)) ? kStSum : 0u) |
+                          ((want(3) || want(4)) ? kStAbs : 0u);
+    switch (need) {
+      case kStSign: CS_LAG1S(1, false, kStSign); break;
+      case kStSum: CS_LAG1S(1, false, kStSum); break;
+      case kStSign | kStSum: CS_LAG1S(1, false, kStSign | kStSum); break;
+      case kStSum | kStAbs: CS_LAG1S(1, false, kStSum | kStAbs); break;
+      default: CS_LAG1(1, false); break;
+    }
   } else if (L == 2) {
     if (plvk) CS_LAG1(2, true);
     else CS_LAG1(2, false);
@@ -428,6 +454,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     else CS_LAG1(4, false);
   }
 #undef CS_LAG1
+#undef CS_LAG1S
   return true;
 }
 

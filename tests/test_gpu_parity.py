@@ -49,7 +49,9 @@ CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg
 
 # "imag_tc": IMAGCOHY without a sign-based metric is produced by the tensor-core kernel
 FAMILIES = {"lag": LAG, "coherency": COHF, "imag_tc": ("IMAGCOHY",), "coh_imag_tc": ("COH", "IMAGCOHY", "PLV"),
-            "cohy_imag": ("COHY", "IMAGCOHY")}
+            "cohy_imag": ("COHY", "IMAGCOHY"),
+            # phase-lag kernel variants that skip statistics no requested metric needs
+            "pli_only": ("PLI", "USPLI"), "wpli_only": ("WPLI", "DSWPLI"), "imag_pli": ("IMAGCOHY", "PLI")}
 
 
 @pytest.mark.parametrize("family", list(FAMILIES))
