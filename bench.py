@@ -121,9 +121,17 @@ def dist_setup():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         import torch.distributed as dist
         lr = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(lr)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
-        return dist, dist.get_rank(), ws, lr
+        # BENCH_DEVICE_OF_RANK=0 + BENCH_BACKEND=gloo: a host-side smoke test of the N > 1
+        # path with every rank on one GPU (collectives staged through host memory, so no
+        # kernel of one rank waits on another's); timings from such a run are not scaling
+        dev_idx = int(os.environ.get("BENCH_DEVICE_OF_RANK", lr))
+        torch.cuda.set_device(dev_idx)
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
+        return dist, dist.get_rank(), ws, dev_idx
     torch.cuda.set_device(0)
     return None, 0, 1, 0
 
@@ -350,23 +358,34 @@ def main():
     per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}  # ms per launch
     dom = max(per, key=per.get)
     lag_ms = per.get("pairs_lag", 0.0)
-    roof = None
-    if dom.endswith("pairs_lag"):
+    spec_key = "local_spectra" if "local_spectra" in per else "spectra"
+    roof = roof_k3 = roof_k1 = None
+    if lag_ms > 0:
         # algorithmic FP32-pipe work: t = FMUL+FFMA (2), sum t (1), sum |t| (1) lane-ops per update
         P_loc = p1 - p0
         upd = P_loc * c.n_bins * c.K
         ach = 4.0 * upd / (lag_ms * 1e-3)
-        roof = {"kernel": "k_pairs_lag", "bound": "fp32", "achieved": ach / 1e12, "peak": fp32_ops / 1e12,
+        roof_k3 = {"kernel": "k_pairs_lag", "bound": "fp32", "achieved": ach / 1e12, "peak": fp32_ops / 1e12,
                 "unit": "T FP32-pipe lane-ops/s", "frac": ach / fp32_ops, "traffic": None,
                 "peak_source": "measured live on this GPU by cs_probe_peaks (dependent FFMA chains)",
                 "work_per_update": "4 FP32 lane-ops (FMUL+FFMA for Im, FADD sum Im, FADD sum |Im|)"}
-    elif dom.endswith("spectra"):
-        k1_ms = per[dom]
-        flop_dfma = c.K * nloc * min(c.T, c.nfft) * c.n_bins * 2 * (1 if not isinstance(c.taper, tuple) else c.taper[2])
-        bytes_ = c.K * nloc * c.T * x.element_size() + c.K * nloc * c.n_bins * 24
-        roof = {"kernel": "k_spectra", "bound": "fp64", "achieved": flop_dfma / (k1_ms * 1e-3) / 1e12,
-                "peak": fp64_fma / 1e12, "unit": "T DFMA/s", "frac": flop_dfma / (k1_ms * 1e-3) / fp64_fma,
-                "traffic": None, "hbm_frac": bytes_ / (k1_ms * 1e-3) / (peaks["hbm_gbs"] * 1e9)}
+    if per.get(spec_key, 0.0) > 0:
+        k1_ms = per[spec_key]
+        L_ = 1 if not isinstance(c.taper, tuple) else c.taper[2]
+        kind = local.k1_kind
+        if kind.startswith("fft"):   # 5 M log2 M + 16 M fp64 flops per signal-taper, M = nfft / 2 (2 flops per DFMA)
+            M_ = c.nfft // 2
+            fma = c.K * nloc * L_ * (5 * M_ * math.log2(M_) + 16 * M_) / 2
+            work = "fp64 FMA-equivalents of a 5 M log2 M + 16 M real-input FFT"
+        else:                        # direct DFT: 2 FMA per sample and plan bin
+            fma = c.K * nloc * L_ * min(c.T, c.nfft) * c.n_bins * 2
+            work = "2 fp64 FMA per sample and plan bin"
+        bytes_ = c.K * nloc * c.T * x.element_size() + c.K * nloc * L_ * c.n_bins * 24
+        roof_k1 = {"kernel": "k_spectra", "k1_kind": kind, "bound": "fp64", "achieved": fma / (k1_ms * 1e-3) / 1e12,
+                "peak": fp64_fma / 1e12, "unit": "T FP64 FMA/s", "frac": fma / (k1_ms * 1e-3) / fp64_fma,
+                "traffic": None, "hbm_frac": bytes_ / (k1_ms * 1e-3) / (peaks["hbm_gbs"] * 1e9),
+                "work": work}
+    roof = roof_k3 if dom.endswith("pairs_lag") else (roof_k1 if dom.endswith("spectra") else None)
     # dram traffic per launch of the dominant kernel from the committed ncu --set full capture
     tr = _ncu_traffic(c.cfg, roof["kernel"] if roof else None, ws)
     if roof is not None:
@@ -392,6 +411,8 @@ def main():
                    "frac": max(t_tc, t_hbm) / (tc_ms * 1e-3),
                    "raw_tflops": flops / (tc_ms * 1e-3) / 1e12, "ms": tc_ms,
                    "note": "fp16 hi/lo split = 3 products per real product; frac = roofline time / measured time"}
+    if roof is None and dom.endswith("pairs_tc"):
+        roof = roof_k2
     breakdown = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in prof.items()}
 
     # ---- network post-processing on the device over the COH band weights ----
@@ -468,7 +489,8 @@ def main():
                    "outputs": "per-bin [nb,P] + band-mean [P] per metric", "parallelism": f"pair-row-tiles x{ws}",
                    "l2": "inputs 4.1 GB > 126 MB L2 (no flush needed)" if c.cfg == 5 else "inputs > L2" ,
                    "updates_per_step": c.updates},
-        "roofline": roof, "roofline_k2": roof_k2, "per_metric": per_metric, "post_processing": post,
+        "roofline": roof, "roofline_k1": roof_k1, "roofline_k2": roof_k2, "roofline_k3": roof_k3,
+        "per_metric": per_metric, "post_processing": post,
         "breakdown": breakdown, "fp64_fallback_entries": n_fallback,
         "gpu_launches": launches, "clocks": clk.summary(),
         "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma, "hbm_gbs": peaks["hbm_gbs"],

@@ -180,6 +180,11 @@ int cs_xcor_peaks(const double* cc_dev, int64_t n_pairs, int nfft, int n_samples
                   const int64_t* pi_dev, const int64_t* pj_dev, const double* csq_dev,
                   const unsigned char* xzero_dev, double* peak_sum_dev, double* lag_sum_dev, void* stream);
 
+/* Which K1 kernel the plan runs (for rooflines / reports): 0 direct DFT on the
+ * FP64 pipe, 1 direct DFT on the fp64 tensor cores, 2 four-step register FFT,
+ * 3 radix-2 shared-memory FFT; -1 for a null plan. */
+int cs_plan_k1_kind(const cs_plan* plan);
+
 /* Tiling helpers for sharding (multi-GPU): number of 64-node tiles, the row-tile
  * range of shard `shard` of `n_shards` (balanced by tile count) and the
  * contiguous global pair range [pair_begin, pair_end) it covers. */

@@ -53,6 +53,7 @@ def lib():
     L.cs_net_threshold.argtypes = [vp, i64, i64, vp, vp]
     L.cs_cor_accumulate.argtypes = [vp, i32, i64, i64, vp, vp]
     L.cs_xcor_peaks.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    L.cs_plan_k1_kind.argtypes = [vp]
     L.cs_pair_sums.argtypes = [vp, vp, i32, i32, i32, ctypes.POINTER(CsSums), vp]
     L.cs_put_taper_spectra.argtypes = [vp, vp, i32, i32, i32, i32, i32, dbl, vp]
     L.cs_num_row_tiles.argtypes = [i32]
@@ -78,7 +79,7 @@ def lib():
 CS_PLAN_WELCH = 1
 
 EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_sums",
-            "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count",
+            "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count",
             "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
             "cs_launch_count", "cs_ring_view", "cs_probe_peaks", "cs_last_error", "cs_version")
 

@@ -497,6 +497,12 @@ int cs_ring_view(cs_plan* p, void** x64, void** x32, int64_t* n_elems) {
 }
 
 int64_t cs_fft_call_count(const cs_plan* p) { return p ? p->fft_calls : 0; }
+
+int cs_plan_k1_kind(const cs_plan* p) {
+  if (!p) return -1;
+  if (p->use_fft) return (p->fft4_tw && (p->nfft == 512 || p->nfft == 1024)) ? 2 : 3;
+  return p->dft_tf ? 1 : 0;
+}
 void cs_reset_fft_call_count(cs_plan* p) { if (p) p->fft_calls = 0; }
 
 int cs_pair_sums(cs_plan* p, const int* slots, int K, int bin_lo, int nbb, const cs_sums* out, void* stream) {

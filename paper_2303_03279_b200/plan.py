@@ -242,6 +242,11 @@ class DevicePlan:
                                                    int(spectra.shape[0]), int(bin_lo), int(spectra.shape[2]),
                                                    int(slot0), int(taper), float(weight), _stream_ptr(stream)))
 
+    @property
+    def k1_kind(self) -> str:
+        """The K1 kernel this plan runs: dft_fp64 | dft_tensor | fft4 | fft_radix2."""
+        return ("dft_fp64", "dft_tensor", "fft4", "fft_radix2")[_lib.lib().cs_plan_k1_kind(self._h)]
+
     def fft_call_count(self) -> int:
         return int(_lib.lib().cs_fft_call_count(self._h))
 

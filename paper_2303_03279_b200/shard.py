@@ -29,10 +29,16 @@ def allgather_ring(local: torch.Tensor, full: torch.Tensor, dist, scratch: torch
     ws = dist.get_world_size()
     if scratch is None:
         scratch = torch.empty((ws,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    # complex rings travel as their real (re, im) views
+    loc_r = torch.view_as_real(local) if local.is_complex() else local
+    scr_r = torch.view_as_real(scratch) if scratch.is_complex() else scratch
     if dist.get_backend() == "nccl":
-        dist.all_gather_into_tensor(scratch.view(-1), local.reshape(-1))
-    else:
-        dist.all_gather(list(scratch.unbind(0)), local.contiguous())
+        dist.all_gather_into_tensor(scr_r.reshape(-1), loc_r.contiguous().reshape(-1))
+    else:  # gloo: host tensors (device rings are staged through host memory)
+        parts = [torch.empty_like(loc_r, device="cpu") for _ in range(ws)]
+        dist.all_gather(parts, loc_r.contiguous().cpu())
+        for w in range(ws):
+            scr_r[w].copy_(parts[w])
     full.copy_(assemble_ring(scratch, full.shape[-1]))
     return full
 
