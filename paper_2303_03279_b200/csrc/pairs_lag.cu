@@ -85,20 +85,24 @@ __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict
   PkJ[o] = make_float4(va.x, wb.x, -va.y, wb.y);
 }
 
-// fp64 recomputation of flagged (pair, bin) entries: one warp per entry, lanes
-// over trials; reference arithmetic of spectral.py:204-241 in complex128.
+// fp64 recomputation of flagged (pair, bin) entries: an 8-lane group per entry
+// (four entries per warp, so the per-entry fp64 finalisation runs four-wide),
+// lanes over trials; reference arithmetic of spectral.py:204-241 in complex128.
 __global__ void k_lag_fallback(const LagArgs a) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int n_warps = (gridDim.x * blockDim.x) >> 5;
+  const int group = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int lane = threadIdx.x & 7;
+  const int n_groups = (gridDim.x * blockDim.x) >> 3;
   const int count = min(a.counters[0], a.flag_cap);
   const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
-  for (int w = warp; w < count; w += n_warps) {
-    const int4 f = a.flags[w];
+  for (int w0 = group - (group & 3); w0 < count; w0 += n_groups) {  // warp-uniform trip count
+    const int w = w0 + (group & 3);
+    const bool live = w < count;
+    const int4 f = live ? __ldg(&a.flags[w]) : make_int4(0, 1, 0, 0);
     const int i = f.x, j = f.y, bl = f.z, b = a.bin_lo + bl;
     double s_im = 0.0, s_abs = 0.0;
     int s_sign = 0;
-    for (int k = lane; k < a.K; k += 32) {
+#pragma unroll 4
+    for (int k = lane; k < (live ? a.K : 0); k += 8) {  // unrolled: the trials' loads are independent
       const int slot = a.slots[k];
       double re = 0.0, im = 0.0;
       for (int l = 0; l < a.L; ++l) {
@@ -114,12 +118,12 @@ __global__ void k_lag_fallback(const LagArgs a) {
       s_sign += (im > 0.0) - (im < 0.0);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 4; o > 0; o >>= 1) {
       s_im += __shfl_xor_sync(0xffffffffu, s_im, o);
       s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
       s_sign += __shfl_xor_sync(0xffffffffu, s_sign, o);
     }
-    if (lane == 0) {
+    if (lane == 0 && live) {
       float v[5];
       const float psd_i = a.psd[(int64_t)bl * a.N + i], psd_j = a.psd[(int64_t)bl * a.N + j];
       // IMAGCOHY in fp64 then rounded; the ratios are scale invariant
@@ -174,7 +178,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
   }
   {
     PhaseMark ph(p, "lag_fallback", st);
-    k_lag_fallback<<<148 * 4, 256, 0, st>>>(a);
+    k_lag_fallback<<<148 * 8, 256, 0, st>>>(a);
   }
   return true;
 }
@@ -283,7 +287,7 @@ int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     a.counters = p.counters;
     a.flag_cap = p.flag_cap;
     PhaseMark ph(p, "lag_fallback", st);
-    k_lag_fallback<<<148 * 4, 256, 0, st>>>(a);
+    k_lag_fallback<<<148 * 8, 256, 0, st>>>(a);
   }
   return 0;  // launches are counted by the phase marks
 }
