@@ -386,12 +386,13 @@ def main():
                 "traffic": None, "hbm_frac": bytes_ / (k1_ms * 1e-3) / (peaks["hbm_gbs"] * 1e9),
                 "work": work}
     roof = roof_k3 if dom.endswith("pairs_lag") else (roof_k1 if dom.endswith("spectra") else None)
-    # dram traffic per launch of the dominant kernel from the committed ncu --set full capture
-    tr = _ncu_traffic(c.cfg, roof["kernel"] if roof else None, ws)
-    if roof is not None:
-        roof["traffic"] = tr["bytes_per_launch"] if tr else None
-        if tr:
-            roof["traffic_source"] = tr["source"]
+    # dram traffic per launch from the committed ncu --set full capture (same config)
+    for rf in (roof_k1, roof_k3):
+        if rf is not None:
+            tr = _ncu_traffic(c.cfg, rf["kernel"], ws)
+            rf["traffic"] = tr["bytes_per_launch"] if tr else None
+            if tr:
+                rf["traffic_source"] = tr["source"]
     # K2 (tensor cores): SURVEY 8(d) roofline = max(3 x flops / bf16 sustained, output bytes / HBM)
     roof_k2 = None
     tc_ms = per.get("pairs_tc", 0.0)
@@ -411,6 +412,11 @@ def main():
                    "frac": max(t_tc, t_hbm) / (tc_ms * 1e-3),
                    "raw_tflops": flops / (tc_ms * 1e-3) / 1e12, "ms": tc_ms,
                    "note": "fp16 hi/lo split = 3 products per real product; frac = roofline time / measured time"}
+    if roof_k2 is not None:
+        tr = _ncu_traffic(c.cfg, "k_pairs_tc", ws)
+        roof_k2["traffic"] = tr["bytes_per_launch"] if tr else None
+        if tr:
+            roof_k2["traffic_source"] = tr["source"]
     if roof is None and dom.endswith("pairs_tc"):
         roof = roof_k2
     breakdown = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in prof.items()}
