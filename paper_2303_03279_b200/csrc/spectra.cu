@@ -235,7 +235,7 @@ static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns,
 // (tf[l][k-step][nt][lane]), so every lane reads consecutive doubles.
 constexpr int kDW = 8;                 // warps per CTA
 constexpr int kDRows = 8 * kDW;        // signals per CTA
-constexpr int kDTC = 32;               // samples per staged chunk
+constexpr int kDTC = 64;               // samples per staged chunk
 
 template <typename Tin, int NT>
 __global__ void __launch_bounds__(kDW * 32)
