@@ -114,3 +114,27 @@ def test_float32_input_path():
     out, _ = _run(g2, LAG, dtype=torch.float32)
     for m in LAG:
         assert np.abs(out[m]["bins"].T - ref[m]["bins"]).max() <= TOL[m], m
+
+
+@pytest.mark.parametrize("N,K,T,nfft,lo,hi,taper", [
+    (2, 1, 40, 64, 1, 1, None), (3, 2, 64, 64, 0, 32, None), (63, 3, 100, 128, 5, 9, "hann"),
+    (65, 7, 128, 128, 2, 40, None), (129, 5, 90, 128, 10, 10, "hann"), (130, 4, 256, 256, 1, 127, ("dpss", 2.0, 2)),
+    (200, 9, 300, 300, 3, 30, None)])
+def test_tile_boundary_shapes(N, K, T, nfft, lo, hi, taper):
+    """Node counts around the 64 / 128 tile edges, K = 1, 2 and odd, single-bin
+    bands, non-power-of-two nfft, all metrics against the oracle."""
+    import oracle as O
+    from paper_2303_03279_b200 import compute_connectivity
+    from paper_2303_03279_b200.plan import make_taper
+    rng = np.random.default_rng(N * 1000 + K)
+    x = rng.standard_normal((K, N, T))
+    metrics = [m for m in ("COHY", "COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI") if not (m == "USPLI" and K < 2)]
+    out, _ = compute_connectivity(torch.tensor(x, device="cuda"), nfft, lo, hi, metrics=metrics, taper=taper)
+    tp = make_taper(taper, min(T, nfft))
+    tp = None if tp is None else (tp[0] if tp.shape[0] == 1 else tp)
+    want, _ = O.compute(list(x), nfft, lo, hi, metrics, taper=tp)
+    sens = O.flush_sensitive(list(x), nfft, lo, hi, taper=tp)
+    for m in metrics:
+        got = out[m]["bins"].T.cpu().numpy()
+        err = np.where(~sens, np.abs(got - want[m]["bins"]), 0.0)
+        assert err.max() <= TOL[m], f"{m}: {err.max():.3g}"
