@@ -10,7 +10,8 @@ import ctypes
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libcsconn.so"
+# CSCONN_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("CSCONN_LIB") or Path(__file__).resolve().parent / "libcsconn.so")
 
 CS_OK, CS_EPARAM, CS_EDEGENERATE, CS_ECUDA, CS_ENOMEM = 0, 1, 2, 3, 4
 CS_F32, CS_F64 = 0, 1

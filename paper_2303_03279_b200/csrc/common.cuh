@@ -3,11 +3,27 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/csconn.h"
 
 #ifndef __CUDA_ARCH__
 #define CS_HOST_ONLY 1
 #endif
+
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per device (the
+// attribute belongs to the kernel on the current device; plans may live on several).
+#define CS_SMEM_ONCE(fn, bytes)                                                                  \
+  do {                                                                                           \
+    static std::atomic<unsigned long long> done_{0};                                              \
+    int dev_ = 0;                                                                                \
+    cudaGetDevice(&dev_);                                                                        \
+    const unsigned long long bit_ = 1ull << (dev_ & 63);                                         \
+    if (!(done_.load(std::memory_order_relaxed) & bit_)) {                                       \
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes));        \
+      done_.fetch_or(bit_);                                                                      \
+    }                                                                                            \
+  } while (0)
 
 namespace cs {
 

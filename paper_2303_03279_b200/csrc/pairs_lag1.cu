@@ -415,20 +415,12 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   const bool plvk = plv_bins || plv_band;
 #define CS_LAG1S(LL, PV, SS)                                                                           \
   do {                                                                                                   \
-    static bool cfg = false;                                                                             \
-    if (!cfg) {                                                                                          \
-      cudaFuncSetAttribute(k_pairs_lag1<LL, PV, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      cfg = true;                                                                                        \
-    }                                                                                                    \
+    CS_SMEM_ONCE((k_pairs_lag1<LL, PV, SS>), smem);                                                     \
     k_pairs_lag1<LL, PV, SS><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);        \
   } while (0)
 #define CS_LAG1(LL, PV)                                                                              \
   do {                                                                                                   \
-    static bool cfg = false;                                                                             \
-    if (!cfg) {                                                                                          \
-      cudaFuncSetAttribute(k_pairs_lag1<LL, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      cfg = true;                                                                                        \
-    }                                                                                                    \
+    CS_SMEM_ONCE((k_pairs_lag1<LL, PV>), smem);                                                         \
     k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
   } while (0)
   if (L == 1) {

@@ -720,11 +720,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   { const char* d = getenv("CSCONN_TC_DBG"); a.dbg = d ? atoi(d) : 0; }
 #endif
   const size_t smem = tc_smem_bytes();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_pairs_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  CS_SMEM_ONCE(k_pairs_tc, smem);
   {
     PhaseMark ph(p, "pairs_tc", st);
     if (a.nbc > 1) {

@@ -212,11 +212,7 @@ static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns,
   constexpr int NS = NBT <= 8 ? 2 : 1;
   using Sh = SpecShape<Tin, NBT, NS>;
   const size_t smem = Sh::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_spectra<Tin, NBT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  CS_SMEM_ONCE((k_spectra<Tin, NBT, NS>), smem);
   const int vec16 = ((uintptr_t)x % 16 == 0) && ((ns * (int64_t)sizeof(Tin)) % 16 == 0) &&
                     ((ts * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.seg_stride * (int64_t)sizeof(Tin)) % 16 == 0);
   dim3 grid((p.N + Sh::ROWS - 1) / Sh::ROWS, (p.nb + NBT - 1) / NBT, kc * p.L);
@@ -351,11 +347,7 @@ template <typename Tin, int NT>
 static void launch_dmma(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0, int kc, cudaStream_t st) {
   constexpr int RS = kDTC + 16 / (int)sizeof(Tin);
   const size_t smem = 2 * (size_t)kDRows * RS * sizeof(Tin) + 2 * (size_t)(kDTC / 4) * NT * 32 * sizeof(double);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(k_spectra_dmma<Tin, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cfg = true;
-  }
+  CS_SMEM_ONCE((k_spectra_dmma<Tin, NT>), smem);
   const int vec16 = ((uintptr_t)x % 16 == 0) && ((ns * (int64_t)sizeof(Tin)) % 16 == 0) &&
                     ((ts * (int64_t)sizeof(Tin)) % 16 == 0) && ((p.seg_stride * (int64_t)sizeof(Tin)) % 16 == 0);
   dim3 grid((p.N + kDRows - 1) / kDRows, kc * p.L);
@@ -857,11 +849,13 @@ void launch_fft4(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0
   constexpr int BUF = (A * S > M + PAD * R) ? A * S : M + PAD * R;
   const size_t smem = (size_t)(A * 32 + 32 + kFft4Warps * BUF) * sizeof(double2) +
                       (size_t)kFft4Warps * 64 * A * sizeof(Tin);
-  static int ctas_per_sm = 0;
+  CS_SMEM_ONCE((k_spectra_fft4<Tin, A>), smem);
+  static std::atomic<int> occ{0};  // same on every B200
+  int ctas_per_sm = occ.load(std::memory_order_relaxed);
   if (!ctas_per_sm) {
-    cudaFuncSetAttribute(k_spectra_fft4<Tin, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_spectra_fft4<Tin, A>, kFft4Warps * 32, smem);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
+    occ.store(ctas_per_sm);
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
@@ -896,14 +890,12 @@ bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_
   const size_t smem = (size_t)(kFftWarps * M + M / 2) * sizeof(double2);
   dim3 grid((p.N + kFftWarps - 1) / kFftWarps, kc);
   if (dtype == CS_F64) {
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(k_spectra_fft<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+    CS_SMEM_ONCE(k_spectra_fft<double>, 200 * 1024);
     k_spectra_fft<double><<<grid, kFftWarps * 32, smem, st>>>((const double*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
         p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
         p.seg_stride);
   } else {
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(k_spectra_fft<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+    CS_SMEM_ONCE(k_spectra_fft<float>, 200 * 1024);
     k_spectra_fft<float><<<grid, kFftWarps * 32, smem, st>>>((const float*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
         p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
         p.seg_stride);
