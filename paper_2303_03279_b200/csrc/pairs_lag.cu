@@ -146,6 +146,14 @@ __global__ void k_lag_fallback(const LagArgs a) {
   }
 }
 
+// Fallback grid: the flagged count is only known on the device; it scales with the
+// pair-bins of the call (~1e-4 of them), so small calls (online windows) launch
+// one block per SM instead of 8.
+static unsigned fallback_blocks(const LagArgs& a) {
+  const int64_t pb = a.pair_stride * (int64_t)a.nbb >> 17;
+  return (unsigned)(pb < 148 ? 148 : (pb > 148 * 8 ? 148 * 8 : pb));
+}
+
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
@@ -178,7 +186,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
   }
   {
     PhaseMark ph(p, "lag_fallback", st);
-    k_lag_fallback<<<148 * 8, 256, 0, st>>>(a);
+    k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
   }
   return true;
 }
@@ -287,7 +295,7 @@ int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     a.counters = p.counters;
     a.flag_cap = p.flag_cap;
     PhaseMark ph(p, "lag_fallback", st);
-    k_lag_fallback<<<148 * 8, 256, 0, st>>>(a);
+    k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
   }
   return 0;  // launches are counted by the phase marks
 }

@@ -402,24 +402,39 @@ void run_spectra(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns
 // Per-call node statistics over the selected trials: psd = sum_k sum_l |X|^2
 // (fp32 scaled units; the 1/L taper mean cancels in every ratio) and
 // mag = max_k sqrt(sum_l |X|^2), the bound used by the exact-sign guard.
-__global__ void k_node_stats(const float2* __restrict__ X32, const int* __restrict__ slots,
-                             int K, int N, int nb, int L, int bin_lo, int nbb,
-                             float* __restrict__ psd, float* __restrict__ mag, float* __restrict__ nscale) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+// 32 nodes x 8 trial lanes per block (small windows would otherwise leave one
+// serial K-loop of dependent gathers per thread and under a wave of blocks).
+constexpr int kNsNodes = 32, kNsLanes = 8;
+__global__ void __launch_bounds__(kNsNodes * kNsLanes)
+k_node_stats(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int N, int nb, int L,
+             int bin_lo, int nbb, float* __restrict__ psd, float* __restrict__ mag, float* __restrict__ nscale) {
+  __shared__ double ss[kNsLanes][kNsNodes];
+  __shared__ float sm[kNsLanes][kNsNodes];
+  const int tx = threadIdx.x, g = threadIdx.y;
+  const int n = blockIdx.x * kNsNodes + tx;
   const int bl = blockIdx.y;  // 0..nbb-1
-  if (n >= N) return;
   const int b = bin_lo + bl;
   double s = 0.0;
   float m = 0.f;
-  for (int k = 0; k < K; ++k) {
-    const int slot = slots[k];
-    float e = 0.f;
-    for (int l = 0; l < L; ++l) {
-      const float2 v = X32[(((int64_t)slot * L + l) * nb + b) * N + n];
-      e = fmaf(v.x, v.x, fmaf(v.y, v.y, e));
+  if (n < N)
+    for (int k = g; k < K; k += kNsLanes) {
+      const int slot = slots[k];
+      float e = 0.f;
+      for (int l = 0; l < L; ++l) {
+        const float2 v = X32[(((int64_t)slot * L + l) * nb + b) * N + n];
+        e = fmaf(v.x, v.x, fmaf(v.y, v.y, e));
+      }
+      s += (double)e;
+      m = fmaxf(m, sqrtf(e));
     }
-    s += (double)e;
-    m = fmaxf(m, sqrtf(e));
+  ss[g][tx] = s;
+  sm[g][tx] = m;
+  __syncthreads();
+  if (g != 0 || n >= N) return;
+#pragma unroll
+  for (int q = 1; q < kNsLanes; ++q) {
+    s += ss[q][tx];
+    m = fmaxf(m, sm[q][tx]);
   }
   psd[(int64_t)bl * N + n] = (float)s;
   mag[(int64_t)bl * N + n] = m;
@@ -430,8 +445,9 @@ __global__ void k_node_stats(const float2* __restrict__ X32, const int* __restri
 
 void run_node_stats(const Plan& p, const int* slots, int K, int bin_lo, int nbb,
                     cudaStream_t st) {
-  dim3 grid((p.N + 127) / 128, nbb);
-  k_node_stats<<<grid, 128, 0, st>>>(p.X32, slots, K, p.N, p.nb, p.L, bin_lo, nbb, p.psd, p.mag, p.nscale);
+  dim3 grid((p.N + kNsNodes - 1) / kNsNodes, nbb);
+  k_node_stats<<<grid, dim3(kNsNodes, kNsLanes), 0, st>>>(p.X32, slots, K, p.N, p.nb, p.L, bin_lo, nbb, p.psd,
+                                                          p.mag, p.nscale);
 }
 
 // complex128 [n_slots][N][nbins] copy-out of the fp64 ring (taper 0), trial_spectra layout.

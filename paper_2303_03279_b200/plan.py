@@ -93,6 +93,7 @@ class DevicePlan:
                                         self.nfft, self.lo, self.hi, 1 if tap is None else self.n_tapers, tptr,
                                         self.slot_capacity, self.scale, _lib.CS_PLAN_WELCH if welch else 0))
         self._h = h
+        self.profiling = False
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -207,6 +208,7 @@ class DevicePlan:
     # -- instrumentation --------------------------------------------------------
     def set_profiling(self, on: bool = True) -> None:
         _lib.check(_lib.lib().cs_plan_set_profiling(self._h, int(bool(on))))
+        self.profiling = bool(on)
 
     def profile(self) -> dict:
         """{phase: (total_ms, count)} since the last read (synchronises)."""
@@ -388,3 +390,88 @@ class HostPipeline:
         host_out = host_out if host_out is not None else self.alloc_host()
         self.submit(xh, host_out).synchronize()
         return host_out
+
+
+class WindowGraph:
+    """The online sliding-window update (``ConnectivityEngine.update_and_finalize``
+    every ``n_new`` trials over the last ``window``; pipeline.py:304-309,
+    metrics.py:450-460) replayed from CUDA graphs.
+
+    The plan's ring holds exactly ``window`` slots: update u writes its ``n_new``
+    trials over the ones that just left the window, and recomputes the metrics
+    over the window's slots.  The (slot0, slot list) pattern repeats every
+    ``window / gcd(window, n_new)`` updates, so one graph per phase is captured
+    on first use (K1 on a fixed staging buffer + the pair kernels into fixed
+    output buffers) and replayed afterwards: an update is one staging copy and
+    one graph launch instead of a dozen launches from Python.
+    """
+
+    def __init__(self, plan: DevicePlan, n_new: int, metrics=SEVEN, bin_lo: int = 0, n_bins: int | None = None,
+                 per_bin=True, band=True, dtype=torch.float32):
+        self.plan = plan
+        self.window = plan.slot_capacity
+        self.n_new = int(n_new)
+        if not 1 <= self.n_new <= self.window:
+            raise ParameterError(f"n_new must be in [1, {self.window}], got {n_new}")
+        self.metrics = tuple(m.upper() for m in metrics)
+        self.bin_lo = int(bin_lo)
+        self.n_bins = plan.n_bins - self.bin_lo if n_bins is None else int(n_bins)
+        self.outputs = plan.alloc_outputs(self.metrics, self.n_bins, per_bin, band)
+        self.staging = torch.empty((self.n_new, plan.n_nodes, plan.n_samples), dtype=dtype, device=plan.device)
+        self.n_phases = self.window // math.gcd(self.window, self.n_new)
+        self._slots = [torch.tensor([(u * self.n_new + k) % self.window for k in range(self.window)],
+                                    dtype=torch.int32, device=plan.device) for u in range(self.n_phases)]
+        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._kernels_per_update = 0
+        self.updates = 0
+
+    def prime(self, x: torch.Tensor) -> dict:
+        """Fill the ring with the first ``window`` trials [window, N, T] and compute
+        the first window's metrics (not graphed)."""
+        if x.shape[0] != self.window:
+            raise ParameterError(f"prime needs {self.window} trials, got {x.shape[0]}")
+        self.plan.spectra(x, 0)
+        self.plan.pair_metrics(self._slots[0], self.metrics, self.bin_lo, self.n_bins, outputs=self.outputs)
+        self.updates = 1
+        return self.outputs
+
+    def _body(self, u: int) -> None:
+        slot0 = ((u - 1) * self.n_new) % self.window
+        self.plan.spectra(self.staging, slot0)
+        self.plan.pair_metrics(self._slots[u % self.n_phases], self.metrics, self.bin_lo, self.n_bins,
+                               outputs=self.outputs)
+
+    def update(self, x_new: torch.Tensor) -> dict:
+        """Append ``n_new`` trials [n_new, N, T] (host or device) and return the
+        outputs of the new window (device buffers, overwritten by the next update)."""
+        if self.updates == 0:
+            raise ParameterError("prime() the first window first")
+        if tuple(x_new.shape) != tuple(self.staging.shape):
+            raise ParameterError(f"expected {tuple(self.staging.shape)} new samples, got {tuple(x_new.shape)}")
+        self.staging.copy_(x_new, non_blocking=True)
+        u = self.updates
+        ph = u % self.n_phases
+        g = self._graphs.get(ph)
+        if g is None:
+            l0 = self.plan.launch_count()
+            self._body(u)  # eager once per phase: lazy allocations happen outside capture
+            self._kernels_per_update = self.plan.launch_count() - l0
+            torch.cuda.current_stream().synchronize()
+            prof = self.plan.profiling
+            if prof:  # per-phase timing events are not captured
+                self.plan.set_profiling(False)
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g):
+                    self._body(u)
+            finally:
+                if prof:
+                    self.plan.set_profiling(True)
+            self._graphs[ph] = g
+        g.replay()
+        self.updates += 1
+        return self.outputs
+
+    def graph_kernels(self) -> int:
+        """Kernels one replay launches (the plan's launch counter over one eager update)."""
+        return self._kernels_per_update

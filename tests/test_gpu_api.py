@@ -339,6 +339,37 @@ def test_host_pipeline_matches_device_path():
             np.testing.assert_allclose(o[m].numpy(), want[m]["band"].cpu().numpy(), rtol=0, atol=2e-6, err_msg=m)
 
 
+def test_window_graph_matches_eager_windows():
+    """WindowGraph (CUDA-graph replays, one graph per ring phase, the ring = the
+    window) returns, update after update, the metrics of a fresh eager plan over
+    the same window of trials -- including after the phases wrap around."""
+    from paper_2303_03279_b200.plan import DevicePlan, WindowGraph, pow2_scale
+    rng = np.random.default_rng(12)
+    win, new, N, T, nfft, lo, hi = 10, 4, 150, 128, 128, 3, 20
+    n_up = 9                                          # 5 phases (10 / gcd(10, 4)), wrapped once
+    x = torch.tensor(rng.standard_normal((win + new * n_up, N, T)), dtype=torch.float32, device="cuda")
+    scale = pow2_scale(float(x.abs().max()), min(T, nfft))
+    metrics = ("COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI")
+    plan = DevicePlan(N, T, nfft, lo, hi, taper="hann", slot_capacity=win, device="cuda", scale=scale)
+    wg = WindowGraph(plan, new, metrics)
+    assert wg.n_phases == 5
+    wg.prime(x[:win])
+    for u in range(1, n_up + 1):
+        got = wg.update(x[win + new * (u - 1): win + new * u])
+        if u in (1, 4, 5, 6, 9):
+            ref = DevicePlan(N, T, nfft, lo, hi, taper="hann", slot_capacity=win, device="cuda", scale=scale)
+            ref.spectra(x[new * u: new * u + win], 0)
+            want = ref.pair_metrics(torch.arange(win, dtype=torch.int32, device="cuda"), metrics)
+            for m in metrics:
+                for part in ("bins", "band"):
+                    # same kernels, the trials in ring (not stream) order: fp32 summation order only
+                    np.testing.assert_allclose(got[m][part].cpu().numpy(), want[m][part].cpu().numpy(),
+                                               rtol=0, atol=2e-5, err_msg=f"{m} {part} update {u}")
+    assert len(wg._graphs) == 5 and wg.graph_kernels() > 0
+    with pytest.raises(ParameterError):
+        wg.update(x[:new + 1])
+
+
 # ---------------------------------------------------------------- welch mode (test_spectral.py:138-160)
 class TestWelchMode:
     def test_welch_averages_segments(self):
