@@ -170,10 +170,29 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
   }
   {
     PhaseMark ph(p, "pairs_lag", st);
-    // small pair spaces (few tiles, many bins): split the bins over CTAs for >= 2 waves
-    int nbc = (int)((2 * 148 + n_tiles - 1) / n_tiles);
-    nbc = nbc < 1 ? 1 : (nbc > a.nbb ? a.nbb : nbc);
-    nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);  // no empty chunks
+    // small pair spaces (few tiles, many bins): split the bins over CTAs.  One CTA per
+    // SM, so the makespan is waves x (per-CTA fixed cost + bins x per-bin cost); the
+    // fixed part (barrier init, band zeroing, first-stage TMA latency, band write-out)
+    // measured ~0.25-0.4 of a bin (cfg1/2/4 sweeps), so pick the split minimising
+    // waves * (0.4 + bins per CTA).
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+    int nbc = 1;
+    double best = 1e300;
+    for (int c = 1; c <= a.nbb; ++c) {
+      const int bpc = (a.nbb + c - 1) / c, chunks = (a.nbb + bpc - 1) / bpc;
+      if (chunks != c) continue;  // no empty chunks
+      const double waves = (double)((n_tiles * chunks + nsm - 1) / nsm);
+      const double cost = waves * (0.4 + bpc);
+      if (cost < best) {
+        best = cost;
+        nbc = c;
+      }
+    }
+    if (const char* e = getenv("CSCONN_K3_NBC")) {  // sweep override
+      nbc = atoi(e) < 1 ? 1 : (atoi(e) > a.nbb ? a.nbb : atoi(e));
+      nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);
+    }
     if (nbc > 1) {
       for (int m = 0; m < 5; ++m)
         if (a.band[m]) cudaMemsetAsync(a.band[m], 0, a.pair_stride * sizeof(float), st);

@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -691,9 +692,24 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   const int64_t n_tiles = tle->n;
   a.n_tiles = (int)n_tiles;
   a.tiles = (const int2*)tle->ptr;
-  {  // small pair spaces: split bins over CTAs for >= ~2 waves
-    int nbc = n_tiles > 0 ? (int)((2 * 148 + n_tiles - 1) / n_tiles) : 1;
-    nbc = nbc < 1 ? 1 : (nbc > nbb ? nbb : nbc);
+  {  // small pair spaces: split bins over CTAs.  Persistent CTAs overlap most of a
+     // work unit's fixed cost, so the time is ~ rounds x (unit overhead + bins x
+     // per-bin cost) with the overhead ~2 bins (cfg1/2/4 sweeps); pick the split
+     // minimising rounds * (2 + bins per unit).
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+    int nbc = 1;
+    double best = 1e300;
+    for (int c = 1; c <= nbb && n_tiles > 0; ++c) {
+      const int bpc = (nbb + c - 1) / c, chunks = (nbb + bpc - 1) / bpc;
+      if (chunks != c) continue;
+      const double cost = (double)((n_tiles * chunks + nsm - 1) / nsm) * (2.0 + bpc);
+      if (cost < best) {
+        best = cost;
+        nbc = c;
+      }
+    }
+    if (const char* e = getenv("CSCONN_K2_NBC")) nbc = atoi(e) < 1 ? 1 : (atoi(e) > nbb ? nbb : atoi(e));
     a.bpc = (nbb + nbc - 1) / nbc;
     a.nbc = (nbb + a.bpc - 1) / a.bpc;
   }
