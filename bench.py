@@ -78,6 +78,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # nvidia-smi takes a moment to start: wait for its first sample and drop it, so
+            # the kept samples fall inside the timed region that starts after __enter__
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
@@ -174,7 +180,7 @@ def run_reference(args, c, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_sub = args.cpu_nodes if args.cpu_nodes else 512  # ~1.8 s per step: the whole run stays within minutes
+    n_sub = min(args.cpu_nodes or 512, c.N)  # cfg5: ~1.8 s per step, the whole run stays within minutes
     samples = []
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(c, n_sub, threads)
@@ -212,7 +218,7 @@ def run_window(args, c, dist, rank, ws, lr):
     cap = 50                       # ring = the window: new trials overwrite the ones that left it
     n_phases = cap // math.gcd(cap, 5)
     warm = max(args.warmup, n_phases)  # every ring phase's graph is captured before the timed region
-    W = min(synth.CFG4_WINDOWS, warm + args.steps + 1)
+    W = min(synth.CFG4_WINDOWS, warm + args.steps + 1)  # windows of the stream (more steps cycle over it)
     n_trials = 5 * (W - 1) + 50
     x = synth.generate(c, dev, trials=range(n_trials))            # [n_trials, N, T] resident in HBM
     plan = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=cap, device=dev,
@@ -220,6 +226,7 @@ def run_window(args, c, dist, rank, ws, lr):
     wg = WindowGraph(plan, 5, c.metrics, 0, c.n_bins)
 
     def window(w):  # trials [5w, 5w + 50): K1 on the 5 new ones, pair kernels over all 50
+        w = 1 + (w - 1) % (W - 1)
         wg.update(x[5 * w + 45: 5 * w + 50])
 
     wg.prime(x[0:50])
@@ -236,6 +243,23 @@ def run_window(args, c, dist, rank, ws, lr):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     launches = wg.graph_kernels() * args.steps
+    # e2e: the online use -- each window's 5 new trials arrive in pinned host memory
+    # (H2D into the staging buffer inside update()), the window's band results are
+    # read back to the host after it
+    n_e2e = min(args.steps, 500)
+    xh = x[: 5 * (W - 1) + 50].cpu().pin_memory()
+    hb = {m: torch.empty(c.n_pairs, dtype=torch.float32).pin_memory() for m in c.metrics}
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for w in range(1 + warm, 1 + warm + n_e2e):
+        wi = 1 + (w - 1) % (W - 1)
+        out = wg.update(xh[5 * wi + 45: 5 * wi + 50])
+        for m in c.metrics:
+            hb[m].copy_(out[m]["band"], non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / n_e2e
     # per-kernel breakdown from an eager (un-graphed, profiled) pass over the same windows
     plan.set_profiling(True)
     plan.profile()
@@ -261,6 +285,11 @@ def run_window(args, c, dist, rank, ws, lr):
             "cuda_graphs": {"phases": n_phases, "kernels_per_window": wg.graph_kernels(),
                             "staging_copy_bytes": int(wg.staging.numel() * wg.staging.element_size())},
             "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": {"value": upd / (e2e_ms * 1e-3), "unit": "updates/s", "ms_per_window": e2e_ms, "windows": n_e2e,
+                    "h2d_bytes_per_step": int(wg.staging.numel() * 4),
+                    "d2h_bytes_per_step": int(sum(v.numel() * 4 for v in hb.values())),
+                    "path": "WindowGraph.update(pinned host trials): H2D into the staging buffer, graph replay, "
+                            "band results D2H per window"},
             "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma}}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -269,7 +298,8 @@ def run_window(args, c, dist, rank, ws, lr):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 50; cfg1/2/4: 4000/1000/3000 so the timed region is ~0.5 s)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -281,6 +311,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-per-metric", action="store_true", help="skip the one-metric-at-a-time runs")
     args = ap.parse_args()
+    if args.steps is None:  # timed regions of >= ~0.5 s, so nvidia-smi samples the clocks in them
+        args.steps = {1: 4000, 2: 1000, 4: 3000}.get(args.config, 50) if args.impl == "ours" else 50
 
     from paper_2303_03279_b200 import synth
     c = synth.CONFIGS[args.config]
@@ -574,7 +606,7 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n_cpu = args.cpu_nodes or 768
+        n_cpu = min(args.cpu_nodes or 768, c.N)
         r = cpu_baseline(c, n_cpu, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": r["updates"] / r["s"], "unit": "updates/s", "cores": 1, "kind": "port",
                                 "sample": f"node subset N'={n_cpu} of cfg{c.cfg}, all K={c.K}, {c.n_bins} bins, "
