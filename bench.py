@@ -252,11 +252,10 @@ def run_window(args, c, dist, rank, ws, lr):
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
-    for w in range(1 + warm, 1 + warm + n_e2e):
+    for w in range(1 + warm, 1 + warm + n_e2e):   # back to back: upload / kernels / download overlap
         wi = 1 + (w - 1) % (W - 1)
-        out = wg.update(xh[5 * wi + 45: 5 * wi + 50])
-        for m in c.metrics:
-            hb[m].copy_(out[m]["band"], non_blocking=True)
+        ev = wg.submit(xh[5 * wi + 45: 5 * wi + 50], hb)
+    torch.cuda.current_stream().wait_event(ev)
     f1.record()
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1) / n_e2e
@@ -288,8 +287,9 @@ def run_window(args, c, dist, rank, ws, lr):
             "e2e": {"value": upd / (e2e_ms * 1e-3), "unit": "updates/s", "ms_per_window": e2e_ms, "windows": n_e2e,
                     "h2d_bytes_per_step": int(wg.staging.numel() * 4),
                     "d2h_bytes_per_step": int(sum(v.numel() * 4 for v in hb.values())),
-                    "path": "WindowGraph.update(pinned host trials): H2D into the staging buffer, graph replay, "
-                            "band results D2H per window"},
+                    "path": "WindowGraph.submit(pinned host trials, pinned host band buffers): H2D into a "
+                            "double-buffered staging buffer, graph replay, band results D2H, on three streams "
+                            "so consecutive windows overlap"},
             "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma}}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -402,14 +402,20 @@ def main():
     spec_key = "local_spectra" if "local_spectra" in per else "spectra"
     roof = roof_k3 = roof_k1 = None
     if lag_ms > 0:
-        # algorithmic FP32-pipe work: t = FMUL+FFMA (2), sum t (1), sum |t| (1) lane-ops per update
+        # algorithmic FP32-pipe work per update (trial): t = sum over L tapers of FMUL+FFMA (2L),
+        # sum t (1), sum |t| (1); multitaper PLV (not separable) adds Re of the
+        # taper-mean CSD (2L), |CSD|^2 (2) and the phasor accumulation (2)
         P_loc = p1 - p0
         upd = P_loc * c.n_bins * c.K
-        ach = 4.0 * upd / (lag_ms * 1e-3)
+        L_k3 = 1 if not isinstance(c.taper, tuple) else c.taper[2]
+        plv_k3 = L_k3 > 1 and "PLV" in metrics
+        w_upd = 2 * L_k3 + 2 + ((2 * L_k3 + 4) if plv_k3 else 0)
+        ach = w_upd * upd / (lag_ms * 1e-3)
         roof_k3 = {"kernel": "k_pairs_lag", "bound": "fp32", "achieved": ach / 1e12, "peak": fp32_ops / 1e12,
                 "unit": "T FP32-pipe lane-ops/s", "frac": ach / fp32_ops, "traffic": None,
                 "peak_source": "measured live on this GPU by cs_probe_peaks (dependent FFMA chains)",
-                "work_per_update": "4 FP32 lane-ops (FMUL+FFMA for Im, FADD sum Im, FADD sum |Im|)"}
+                "work_per_update": (f"{w_upd} FP32 lane-ops: t over {L_k3} taper(s) {2 * L_k3}, sum t 1, sum |t| 1"
+                                    + (f", multitaper PLV {2 * L_k3 + 4}" if plv_k3 else ""))}
     if per.get(spec_key, 0.0) > 0:
         k1_ms = per[spec_key]
         L_ = 1 if not isinstance(c.taper, tuple) else c.taper[2]

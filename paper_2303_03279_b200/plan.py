@@ -400,14 +400,18 @@ class WindowGraph:
     The plan's ring holds exactly ``window`` slots: update u writes its ``n_new``
     trials over the ones that just left the window, and recomputes the metrics
     over the window's slots.  The (slot0, slot list) pattern repeats every
-    ``window / gcd(window, n_new)`` updates, so one graph per phase is captured
-    on first use (K1 on a fixed staging buffer + the pair kernels into fixed
-    output buffers) and replayed afterwards: an update is one staging copy and
-    one graph launch instead of a dozen launches from Python.
+    ``window / gcd(window, n_new)`` updates, so one graph per phase and buffer is
+    captured on first use (K1 on a staging buffer + the pair kernels into an
+    output set) and replayed afterwards: an update is one staging copy and one
+    graph launch instead of a dozen launches from Python.
+
+    Staging buffers and output sets are double-buffered, so ``submit`` (host
+    samples in, host band results out) overlaps update u+1's upload and update
+    u-1's download with update u's kernels on separate copy streams.
     """
 
     def __init__(self, plan: DevicePlan, n_new: int, metrics=SEVEN, bin_lo: int = 0, n_bins: int | None = None,
-                 per_bin=True, band=True, dtype=torch.float32):
+                 per_bin=True, band=True, dtype=torch.float32, buffers: int = 2):
         self.plan = plan
         self.window = plan.slot_capacity
         self.n_new = int(n_new)
@@ -416,45 +420,58 @@ class WindowGraph:
         self.metrics = tuple(m.upper() for m in metrics)
         self.bin_lo = int(bin_lo)
         self.n_bins = plan.n_bins - self.bin_lo if n_bins is None else int(n_bins)
-        self.outputs = plan.alloc_outputs(self.metrics, self.n_bins, per_bin, band)
-        self.staging = torch.empty((self.n_new, plan.n_nodes, plan.n_samples), dtype=dtype, device=plan.device)
+        self.nbuf = max(1, int(buffers))
+        self._outs = [plan.alloc_outputs(self.metrics, self.n_bins, per_bin, band) for _ in range(self.nbuf)]
+        self._stage = [torch.empty((self.n_new, plan.n_nodes, plan.n_samples), dtype=dtype, device=plan.device)
+                       for _ in range(self.nbuf)]
         self.n_phases = self.window // math.gcd(self.window, self.n_new)
         self._slots = [torch.tensor([(u * self.n_new + k) % self.window for k in range(self.window)],
                                     dtype=torch.int32, device=plan.device) for u in range(self.n_phases)]
-        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
         self._kernels_per_update = 0
         self.updates = 0
+        self._cur = 0
+        with torch.cuda.device(plan.device):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+            self._ev_in = [torch.cuda.Event() for _ in range(self.nbuf)]
+            self._ev_used = [torch.cuda.Event() for _ in range(self.nbuf)]   # graph done reading stage / writing outs
+            self._ev_out = [torch.cuda.Event() for _ in range(self.nbuf)]    # download of outs done
+            for e in self._ev_used + self._ev_out:
+                e.record()
+
+    @property
+    def outputs(self) -> dict:
+        """Output set of the latest update."""
+        return self._outs[self._cur]
+
+    @property
+    def staging(self) -> torch.Tensor:
+        return self._stage[0]
 
     def prime(self, x: torch.Tensor) -> dict:
         """Fill the ring with the first ``window`` trials [window, N, T] and compute
         the first window's metrics (not graphed)."""
         if x.shape[0] != self.window:
             raise ParameterError(f"prime needs {self.window} trials, got {x.shape[0]}")
-        self.plan.spectra(x, 0)
-        self.plan.pair_metrics(self._slots[0], self.metrics, self.bin_lo, self.n_bins, outputs=self.outputs)
+        self.plan.spectra(x.to(self.plan.device, non_blocking=True), 0)
+        self.plan.pair_metrics(self._slots[0], self.metrics, self.bin_lo, self.n_bins, outputs=self._outs[0])
+        self._ev_used[0].record()
+        self._cur = 0
         self.updates = 1
-        return self.outputs
+        return self._outs[0]
 
-    def _body(self, u: int) -> None:
+    def _body(self, u: int, b: int) -> None:
         slot0 = ((u - 1) * self.n_new) % self.window
-        self.plan.spectra(self.staging, slot0)
+        self.plan.spectra(self._stage[b], slot0)
         self.plan.pair_metrics(self._slots[u % self.n_phases], self.metrics, self.bin_lo, self.n_bins,
-                               outputs=self.outputs)
+                               outputs=self._outs[b])
 
-    def update(self, x_new: torch.Tensor) -> dict:
-        """Append ``n_new`` trials [n_new, N, T] (host or device) and return the
-        outputs of the new window (device buffers, overwritten by the next update)."""
-        if self.updates == 0:
-            raise ParameterError("prime() the first window first")
-        if tuple(x_new.shape) != tuple(self.staging.shape):
-            raise ParameterError(f"expected {tuple(self.staging.shape)} new samples, got {tuple(x_new.shape)}")
-        self.staging.copy_(x_new, non_blocking=True)
-        u = self.updates
-        ph = u % self.n_phases
-        g = self._graphs.get(ph)
+    def _run(self, u: int, b: int) -> None:
+        key = (u % self.n_phases, b)
+        g = self._graphs.get(key)
         if g is None:
             l0 = self.plan.launch_count()
-            self._body(u)  # eager once per phase: lazy allocations happen outside capture
+            self._body(u, b)  # eager once per key: lazy allocations happen outside capture
             self._kernels_per_update = self.plan.launch_count() - l0
             torch.cuda.current_stream().synchronize()
             prof = self.plan.profiling
@@ -463,14 +480,53 @@ class WindowGraph:
             g = torch.cuda.CUDAGraph()
             try:
                 with torch.cuda.graph(g):
-                    self._body(u)
+                    self._body(u, b)
             finally:
                 if prof:
                     self.plan.set_profiling(True)
-            self._graphs[ph] = g
+            self._graphs[key] = g
         g.replay()
+
+    def submit(self, x_new: torch.Tensor, host_out: dict | None = None):
+        """Append ``n_new`` trials [n_new, N, T] (pinned host or device memory) and
+        enqueue the window update; with ``host_out`` ({metric: pinned float32 [P]})
+        the band results are downloaded into it.  Returns the CUDA event that marks
+        the results (host or device) complete.  Nothing synchronises the host, so
+        consecutive submits pipeline upload, kernels and download."""
+        if self.updates == 0:
+            raise ParameterError("prime() the first window first")
+        if tuple(x_new.shape) != tuple(self._stage[0].shape):
+            raise ParameterError(f"expected {tuple(self._stage[0].shape)} new samples, got {tuple(x_new.shape)}")
+        u = self.updates
+        b = u % self.nbuf
+        cs = torch.cuda.current_stream(self.plan.device)
+        self._h2d.wait_event(self._ev_used[b])        # the graph that last read stage b is done
+        if x_new.is_cuda:
+            self._h2d.wait_stream(cs)                 # device input: ordered after its producer
+        with torch.cuda.stream(self._h2d):
+            self._stage[b].copy_(x_new, non_blocking=True)
+            self._ev_in[b].record()
+        cs.wait_event(self._ev_in[b])
+        cs.wait_event(self._ev_out[b])                # output set b has been downloaded
+        self._run(u, b)
+        self._ev_used[b].record(cs)
+        self._cur = b
         self.updates += 1
-        return self.outputs
+        if host_out is None:
+            return self._ev_used[b]
+        self._d2h.wait_event(self._ev_used[b])
+        with torch.cuda.stream(self._d2h):
+            for m, h in host_out.items():
+                h.copy_(self._outs[b][m]["band"], non_blocking=True)
+            self._ev_out[b].record()
+        return self._ev_out[b]
+
+    def update(self, x_new: torch.Tensor) -> dict:
+        """Append ``n_new`` trials [n_new, N, T] (host or device) and return the
+        outputs of the new window (device buffers, stream-ordered on the current
+        stream; reused ``buffers`` updates later)."""
+        self.submit(x_new)
+        return self._outs[self._cur]
 
     def graph_kernels(self) -> int:
         """Kernels one replay launches (the plan's launch counter over one eager update)."""

@@ -365,9 +365,37 @@ def test_window_graph_matches_eager_windows():
                     # same kernels, the trials in ring (not stream) order: fp32 summation order only
                     np.testing.assert_allclose(got[m][part].cpu().numpy(), want[m][part].cpu().numpy(),
                                                rtol=0, atol=2e-5, err_msg=f"{m} {part} update {u}")
-    assert len(wg._graphs) == 5 and wg.graph_kernels() > 0
+    assert len(wg._graphs) == 9 and wg.graph_kernels() > 0  # (phase, buffer) keys: lcm(5, 2) = 10 > 9 updates
     with pytest.raises(ParameterError):
         wg.update(x[:new + 1])
+
+
+def test_window_graph_submit_pipelined_host_io():
+    """WindowGraph.submit from pinned host samples into pinned host band buffers,
+    many updates in flight (no host sync in between): every window's downloaded
+    band results equal a fresh eager plan's over the same trials."""
+    from paper_2303_03279_b200.plan import DevicePlan, WindowGraph, pow2_scale
+    rng = np.random.default_rng(13)
+    win, new, N, T, nfft, lo, hi = 12, 3, 140, 100, 128, 2, 30
+    n_up = 10
+    xh = torch.tensor(rng.standard_normal((win + new * n_up, N, T)), dtype=torch.float32).pin_memory()
+    scale = pow2_scale(float(xh.abs().max()), min(T, nfft))
+    metrics = ("COH", "PLV", "WPLI")
+    plan = DevicePlan(N, T, nfft, lo, hi, taper="hann", slot_capacity=win, device="cuda", scale=scale)
+    wg = WindowGraph(plan, new, metrics)
+    wg.prime(xh[:win])
+    P = N * (N - 1) // 2
+    outs = [{m: torch.empty(P, dtype=torch.float32).pin_memory() for m in metrics} for _ in range(n_up)]
+    evs = [wg.submit(xh[win + new * (u - 1): win + new * u], outs[u - 1]) for u in range(1, n_up + 1)]
+    for ev in evs:
+        ev.synchronize()
+    for u in (1, 2, 7, n_up):
+        ref = DevicePlan(N, T, nfft, lo, hi, taper="hann", slot_capacity=win, device="cuda", scale=scale)
+        ref.spectra(xh[new * u: new * u + win].cuda(), 0)
+        want = ref.pair_metrics(torch.arange(win, dtype=torch.int32, device="cuda"), metrics)
+        for m in metrics:
+            np.testing.assert_allclose(outs[u - 1][m].numpy(), want[m]["band"].cpu().numpy(), rtol=0, atol=2e-5,
+                                       err_msg=f"{m} update {u}")
 
 
 # ---------------------------------------------------------------- welch mode (test_spectral.py:138-160)
