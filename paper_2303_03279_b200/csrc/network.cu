@@ -57,20 +57,34 @@ __global__ void k_hist(const float* __restrict__ w, int64_t n, const SelState* _
     if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
 }
 
-// one thread: pick the digit holding the k-th largest key, update the state, clear the histogram
-__global__ void k_pick(SelState* __restrict__ s, int shift, unsigned long long* __restrict__ hist) {
-  long long k = s->k, above = 0;
-  int d = 255;
-  for (; d > 0; --d) {
-    const long long c = (long long)hist[d];
-    if (above + c >= k) break;
-    above += c;
+// 256 threads, one digit each: the count of keys in digits above d is a scan from
+// the top; the thread whose digit holds the k-th largest key updates the state,
+// and every thread clears its histogram bin.
+__global__ void __launch_bounds__(256) k_pick(SelState* __restrict__ s, int shift,
+                                              unsigned long long* __restrict__ hist) {
+  __shared__ long long wsum[8];
+  const int d = 255 - (int)threadIdx.x;  // thread 0 holds the top digit
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long c = (long long)hist[d];
+  long long x = c;  // inclusive scan in thread order = count of keys in digits >= d
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  s->prefix |= (unsigned)d << shift;
-  s->mask |= 255u << shift;
-  s->n_gt += above;
-  s->k = k - above;
-  for (int i = 0; i < 256; ++i) hist[i] = 0;
+  if (lane == 31) wsum[warp] = x;
+  const long long k = s->k;
+  __syncthreads();
+  for (int i = 0; i < warp; ++i) x += wsum[i];
+  const long long above = x - c;  // keys in digits > d
+  // the digit holding rank k; digit 0 takes whatever is left (as the serial scan did)
+  if ((above < k && x >= k && d > 0) || (d == 0 && above < k)) {
+    s->prefix |= (unsigned)d << shift;
+    s->mask |= 255u << shift;
+    s->n_gt += above;
+    s->k = k - above;
+  }
+  hist[d] = 0;
 }
 
 constexpr int kSelBlock = 256, kSelItems = 16;  // 4096 elements per compaction block
@@ -160,49 +174,68 @@ __global__ void k_scan(long long* __restrict__ cnt_gt, long long* __restrict__ c
   }
 }
 
-__global__ void k_compact(const float* __restrict__ w, int64_t n, const SelState* __restrict__ s,
-                          const long long* __restrict__ off_gt, const long long* __restrict__ off_tie,
-                          int64_t* __restrict__ out) {
+// exclusive block-wide scan of one int per thread (kSelBlock threads)
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int before = 0;
+#pragma unroll
+  for (int i = 0; i < kSelBlock / 32; ++i) before += i < warp ? wsum[i] : 0;
+  __syncthreads();  // wsum reusable
+  return before + x - v;
+}
+
+// Thread t of block b owns the 16 consecutive elements b*4096 + 16t .. +15 (same
+// block ranges as k_count): one vector load, the ties before it from a block scan,
+// its kept elements decided in order, their output slots from a second scan.
+__global__ void __launch_bounds__(kSelBlock) k_compact(const float* __restrict__ w, int64_t n,
+                                                       const SelState* __restrict__ s,
+                                                       const long long* __restrict__ off_gt,
+                                                       const long long* __restrict__ off_tie,
+                                                       int64_t* __restrict__ out) {
+  __shared__ int wsum[kSelBlock / 32];
   const unsigned tau = s->prefix;
   const long long ties_kept = s->k;  // the tau ties kept (lowest indices first)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ int wsel[kSelBlock / 32], wtie[kSelBlock / 32];
-  __shared__ long long run_sel, run_tie;
-  if (threadIdx.x == 0) {
-    run_tie = off_tie[blockIdx.x];
-    run_sel = off_gt[blockIdx.x] + min(off_tie[blockIdx.x], ties_kept);
-  }
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kSelBlock * kSelItems;
-  for (int q = 0; q < kSelItems; ++q) {  // rows of 256 consecutive elements, in order
-    const int64_t e = base + (int64_t)q * kSelBlock + threadIdx.x;
-    const unsigned key = e < n ? absbits(w[e]) : 0u;
-    const bool is_tie = e < n && key == tau;
-    const unsigned tb = __ballot_sync(0xffffffffu, is_tie);
-    if (lane == 0) wtie[warp] = __popc(tb);
-    __syncthreads();
-    long long tie_before = run_tie;
-    for (int i = 0; i < warp; ++i) tie_before += wtie[i];
-    tie_before += __popc(tb & ((1u << lane) - 1u));
-    const bool sel = e < n && (key > tau || (is_tie && tie_before < ties_kept));
-    const unsigned sb = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) wsel[warp] = __popc(sb);
-    __syncthreads();
-    long long pos = run_sel;
-    for (int i = 0; i < warp; ++i) pos += wsel[i];
-    pos += __popc(sb & ((1u << lane) - 1u));
-    if (sel) out[pos] = e;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int a = 0, b = 0;
-      for (int i = 0; i < kSelBlock / 32; ++i) {
-        a += wsel[i];
-        b += wtie[i];
-      }
-      run_sel += a;
-      run_tie += b;
+  const int64_t base = (int64_t)blockIdx.x * kSelBlock * kSelItems + (int64_t)threadIdx.x * kSelItems;
+  unsigned key[kSelItems];
+  if (base + kSelItems <= n && ((reinterpret_cast<uintptr_t>(w) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < kSelItems / 4; ++q) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(w + base) + q);
+      key[4 * q] = absbits(v.x);
+      key[4 * q + 1] = absbits(v.y);
+      key[4 * q + 2] = absbits(v.z);
+      key[4 * q + 3] = absbits(v.w);
     }
-    __syncthreads();
+  } else {
+#pragma unroll
+    for (int q = 0; q < kSelItems; ++q) key[q] = base + q < n ? absbits(w[base + q]) : 0u;
+  }
+  int nt = 0;
+#pragma unroll
+  for (int q = 0; q < kSelItems; ++q) nt += (base + q < n) && key[q] == tau;
+  long long tie = off_tie[blockIdx.x] + block_excl_scan(nt, wsum);
+  unsigned sel = 0;
+#pragma unroll
+  for (int q = 0; q < kSelItems; ++q) {
+    const bool in = base + q < n;
+    bool keep = in && key[q] > tau;
+    if (in && key[q] == tau) keep = tie++ < ties_kept;
+    sel |= (unsigned)keep << q;
+  }
+  const long long blk_sel = off_gt[blockIdx.x] + min(off_tie[blockIdx.x], ties_kept);
+  long long pos = blk_sel + block_excl_scan(__popc(sel), wsum);
+  while (sel) {
+    const int q = __ffs(sel) - 1;
+    sel &= sel - 1;
+    out[pos++] = base + q;
   }
 }
 
@@ -241,7 +274,7 @@ int cs_net_threshold(const float* w, int64_t n, int64_t keep, int64_t* out_idx, 
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   for (int shift = 24; shift >= 0; shift -= 8) {
     cs::k_hist<<<grid, 256, 0, st>>>(w, n, s, shift, hist);
-    cs::k_pick<<<1, 1, 0, st>>>(s, shift, hist);
+    cs::k_pick<<<1, 256, 0, st>>>(s, shift, hist);
   }
   cs::k_count<<<nblk, cs::kSelBlock, 0, st>>>(w, n, s, cg, ct);
   cs::k_scan<<<1, 1024, 0, st>>>(cg, ct, nblk);
