@@ -189,8 +189,9 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
         nbc = c;
       }
     }
-    if (const char* e = getenv("CSCONN_K3_NBC")) {  // sweep override
-      nbc = atoi(e) < 1 ? 1 : (atoi(e) > a.nbb ? a.nbb : atoi(e));
+    static const int force_nbc = getenv("CSCONN_K3_NBC") ? atoi(getenv("CSCONN_K3_NBC")) : 0;  // sweep override
+    if (force_nbc) {
+      nbc = force_nbc < 1 ? 1 : (force_nbc > a.nbb ? a.nbb : force_nbc);
       nbc = (a.nbb + ((a.nbb + nbc - 1) / nbc) - 1) / ((a.nbb + nbc - 1) / nbc);
     }
     if (nbc > 1) {

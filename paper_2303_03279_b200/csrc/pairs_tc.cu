@@ -709,7 +709,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
         nbc = c;
       }
     }
-    if (const char* e = getenv("CSCONN_K2_NBC")) nbc = atoi(e) < 1 ? 1 : (atoi(e) > nbb ? nbb : atoi(e));
+    static const int force_nbc = getenv("CSCONN_K2_NBC") ? atoi(getenv("CSCONN_K2_NBC")) : 0;  // sweep override
+    if (force_nbc) nbc = force_nbc < 1 ? 1 : (force_nbc > nbb ? nbb : force_nbc);
     a.bpc = (nbb + nbc - 1) / nbc;
     a.nbc = (nbb + a.bpc - 1) / a.bpc;
   }
