@@ -308,7 +308,7 @@ def main():
                     help="node subset for the CPU baseline (default 768; 512 per step for --impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-per-metric", action="store_true", help="skip the one-metric-at-a-time runs")
     args = ap.parse_args()
     if args.steps is None:  # timed regions of >= ~0.5 s, so nvidia-smi samples the clocks in them
