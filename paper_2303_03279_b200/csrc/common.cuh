@@ -110,15 +110,18 @@ __host__ __device__ __forceinline__ int64_t pair_of(int64_t i, int64_t j, int64_
 }
 
 // Decode the t-th tile (I <= J) of the row-tile range starting at row_begin.
+// Upper-triangle tile t (row-major from row_begin, row r holding nt - r tiles) ->
+// (I, J).  The first m rows hold S(m) = m (nt - row_begin) - m (m - 1) / 2 tiles;
+// m comes from the quadratic's root, then at most a step of integer fix-up.
 __device__ __forceinline__ void decode_tile(int64_t t, int nt, int row_begin, int& I, int& J) {
-  int r = row_begin;
-  int64_t left = t;
-  while (left >= nt - r) {
-    left -= nt - r;
-    ++r;
-  }
-  I = r;
-  J = r + (int)left;
+  const int64_t w = nt - row_begin;
+  const double b = (double)w + 0.5;
+  int64_t m = (int64_t)(b - sqrt(fmax(b * b - 2.0 * (double)t, 0.0)));
+  if (m < 0) m = 0;
+  while (m > 0 && m * w - m * (m - 1) / 2 > t) --m;
+  while ((m + 1) * w - (m + 1) * m / 2 <= t) ++m;
+  I = row_begin + (int)m;
+  J = I + (int)(t - (m * w - m * (m - 1) / 2));
 }
 
 // Profiling phase (CUDA events on the launching stream around one kernel);
