@@ -346,26 +346,31 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   }
 
   if (band_mask) {
-    // each thread owns its pairs' band slots: no barrier needed
+    // band write-out by rows: the compute warps' band slots are complete after one
+    // named barrier (the producer warp has left); warp w writes rows w, w + 16, ...
+    // of every requested metric, lanes over 64 contiguous pair columns.
+    asm volatile("bar.sync 1, %0;" ::"n"(k1Threads) : "memory");
     const float inv = 1.f / (float)a.nbb;
-#pragma unroll
-    for (int r = 0; r < k1TR; ++r) {
-      const int li = ty + k1TY * r, i = iBase + li;
+    for (int li = warp; li < kTile; li += k1Warps) {
+      const int i = iBase + li;
+      if (i >= a.N) break;
       const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
 #pragma unroll
-      for (int c = 0; c < k1TC; ++c) {
-        const int lj = tx + k1TX * c, j = jBase + lj;
-        if (!(i < j && j < a.N)) continue;
+      for (int m = 0; m < NM; ++m) {
+        if (!(band_mask & (1u << m))) continue;
+        float* dst = (m < 5 ? a.band[m] : a.plv_band) + rowoff + jBase;
+        const float* bs = band_s + (m * kTile + li) * kTile;
 #pragma unroll
-        for (int m = 0; m < NM; ++m)
-          if (band_mask & (1u << m)) {
-            float* dst = m < 5 ? a.band[m] : a.plv_band;
-            const float v = band_s[(m * kTile + li) * kTile + lj] * inv;
+        for (int c = 0; c < 2; ++c) {
+          const int lj = lane + 32 * c, j = jBase + lj;
+          if (i < j && j < a.N) {
+            const float v = bs[lj] * inv;
             if (a.nbc > 1)
-              atomicAdd(&dst[rowoff + j], v);  // bins split over CTAs: band zeroed by the host
+              atomicAdd(dst + lj, v);  // bins split over CTAs: band zeroed by the host
             else
-              __stcs(&dst[rowoff + j], v);
+              __stcs(dst + lj, v);
           }
+        }
       }
     }
   }
