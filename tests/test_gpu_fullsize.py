@@ -102,3 +102,32 @@ def test_sharded_row_ranges_reproduce_the_single_run(cfg, shards):
         for m in c.metrics:
             assert torch.equal(o[m]["bins"], full[m]["bins"][:, p0:p1]), (s, m)
             assert float((o[m]["band"] - full[m]["band"][p0:p1]).abs().max()) <= 1e-6, (s, m)
+
+
+def test_pair_space_beyond_int32():
+    """N = 65600 nodes: P = 2,151,657,200 pairs, so pair offsets past 2^31 (and
+    i * i past 2^31 from i = 46341 on) must be 64-bit everywhere on the path.  Band
+    outputs of a K2 and a K3 metric each; nodes whose pairs straddle the 2^31 pair
+    index are checked against the oracle on just those nodes."""
+    N, K, T, nfft, lo, hi = 65600, 4, 32, 32, 3, 4
+    P = N * (N - 1) // 2
+    assert P > 2 ** 31
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    x = torch.randn((K, N, T), generator=gen, device="cuda", dtype=torch.float32)
+    metrics = ("COH", "PLV", "PLI", "WPLI")
+    out, plan = compute_connectivity(x, nfft, lo, hi, metrics=metrics, per_bin=False, band=True)
+    idx = np.array([0, 1, 32767, 46340, 46341, 65534, 65535, 65536, 65597, 65598, 65599])
+    pidx = _pair_index(idx, N)
+    assert pidx.max() == P - 1 and (pidx > 2 ** 31).any()
+    sub = x[:, torch.as_tensor(idx, device="cuda"), :].double().cpu().numpy()
+    want, _ = O.compute(list(sub), nfft, lo, hi, metrics)
+    masks = O.well_conditioned(list(sub), nfft, lo, hi, metrics, TOL, ref=want)
+    tp = torch.as_tensor(pidx, device="cuda")
+    for m in metrics:
+        got = out[m]["band"][tp].cpu().numpy()
+        keep = masks[m].all(axis=1)
+        assert keep.mean() > 0.9, m
+        err = np.abs(got - want[m]["band"])[keep]
+        assert err.max() <= TOL[m], f"{m}: max err {err.max():.3g}"
+        tail = out[m]["band"][-4_000_000:]          # the last rows of the pair space
+        assert bool(torch.isfinite(tail).all()) and float(tail.min()) >= -1e-6 and float(tail.max()) <= 1 + 1e-5, m
