@@ -259,6 +259,24 @@ class TestEngine:
 
 
 # ---------------------------------------------------------------- acceptance (test_acceptance.py)
+@pytest.mark.parametrize("C", [1, 2, 3])
+def test_smallest_node_counts(C):
+    """One channel -> an empty network (no pairs), as the reference returns; two and
+    three channels (a single partial tile) match the oracle for every metric."""
+    eps = make_epochs(3, C, 64, seed=20 + C, sfreq=100.0)
+    band = FrequencyBand(2, 5, 100.0 / 32)
+    for m in ("COHY", "COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI", "COR", "XCOR"):
+        net = M.compute_metric(eps, MetricId[m], 32, band=None if m in ("COR", "XCOR") else band)
+        w = np.asarray(net.weights)
+        assert w.shape == (C * (C - 1) // 2,), m
+        if C == 1 or m in ("COR", "XCOR"):
+            continue
+        want, _ = O.compute([e.data for e in eps], 32, 2, 5, (m,))
+        np.testing.assert_allclose(w, want[m]["band"], rtol=0, atol=TOL[m], err_msg=m)
+        if m == "COHY":  # weight = |mean coherency| (metrics.py:126-130)
+            np.testing.assert_allclose(np.abs(np.asarray(net.complex_weights)), w, rtol=1e-6, atol=1e-7)
+
+
 def test_criterion_1_oracle_equivalence():
     epochs = make_epochs(20, 8, 64, seed=101)
     acc = accumulated(epochs, 64)
