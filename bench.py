@@ -229,19 +229,31 @@ def run_window(args, c, dist, rank, ws, lr):
         w = 1 + (w - 1) % (W - 1)
         wg.update(x[5 * w + 45: 5 * w + 50])
 
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
     wg.prime(x[0:50])
     for w in range(1, 1 + warm):
         window(w)
-    torch.cuda.synchronize()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(lr) as clk:
-        torch.cuda.synchronize()
+        barrier()
         e0.record()
         for w in range(1 + warm, 1 + warm + args.steps):
             window(w)
         e1.record()
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)   # replicas: every rank runs its own stream
     launches = wg.graph_kernels() * args.steps
     # e2e: the online use -- each window's 5 new trials arrive in pinned host memory
     # (H2D into the staging buffer inside update()), the window's band results are
@@ -249,7 +261,7 @@ def run_window(args, c, dist, rank, ws, lr):
     n_e2e = min(args.steps, 500)
     xh = x[: 5 * (W - 1) + 50].cpu().pin_memory()
     hb = {m: torch.empty(c.n_pairs, dtype=torch.float32).pin_memory() for m in c.metrics}
-    torch.cuda.synchronize()
+    barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for w in range(1 + warm, 1 + warm + n_e2e):   # back to back: upload / kernels / download overlap
@@ -257,8 +269,8 @@ def run_window(args, c, dist, rank, ws, lr):
         ev = wg.submit(xh[5 * wi + 45: 5 * wi + 50], hb)
     torch.cuda.current_stream().wait_event(ev)
     f1.record()
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / n_e2e
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1) / n_e2e)
     # per-kernel breakdown from an eager (un-graphed, profiled) pass over the same windows
     plan.set_profiling(True)
     plan.profile()
@@ -272,7 +284,8 @@ def run_window(args, c, dist, rank, ws, lr):
     upd = c.n_pairs * c.n_bins * 50
     per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
     fp32_ops, fp64_fma = probe_peaks(lr)
-    line = {"metric": "edge*freq*trial updates/s per online window (config 4, PLV + WPLI)", "value": upd / (ms * 1e-3),
+    line = {"metric": "edge*freq*trial updates/s per online window (config 4, PLV + WPLI)",
+            "value": ws * upd / (ms * 1e-3),
             "unit": "updates/s", "ms_per_window": ms, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY.md 8(d) cfg4 pink noise + planted 20 Hz)",
@@ -284,9 +297,10 @@ def run_window(args, c, dist, rank, ws, lr):
             "cuda_graphs": {"phases": n_phases, "kernels_per_window": wg.graph_kernels(),
                             "staging_copy_bytes": int(wg.staging.numel() * wg.staging.element_size())},
             "gpu_launches": launches, "clocks": clk.summary(),
-            "e2e": {"value": upd / (e2e_ms * 1e-3), "unit": "updates/s", "ms_per_window": e2e_ms, "windows": n_e2e,
-                    "h2d_bytes_per_step": int(wg.staging.numel() * 4),
-                    "d2h_bytes_per_step": int(sum(v.numel() * 4 for v in hb.values())),
+            "e2e": {"value": ws * upd / (e2e_ms * 1e-3), "unit": "updates/s", "ms_per_window": e2e_ms,
+                    "windows": n_e2e,
+                    "h2d_bytes_per_step": int(wg.staging.numel() * 4) * ws,
+                    "d2h_bytes_per_step": int(sum(v.numel() * 4 for v in hb.values())) * ws,
                     "path": "WindowGraph.submit(pinned host trials, pinned host band buffers): H2D into a "
                             "double-buffered staging buffer, graph replay, band results D2H, on three streams "
                             "so consecutive windows overlap"},
