@@ -594,19 +594,37 @@ def main():
                                "pair kernels over row-tile chunks -> band means D2H per chunk; steps enqueued "
                                "back to back (step s+1 upload overlaps step s kernels + download)"}
     elif not args.no_e2e:
+        # N > 1: every rank uploads its node block, runs K1, joins the all-gather, runs its
+        # pair rows and downloads its band means; uploads and downloads run on copy streams
+        # so step s+1's upload overlaps step s's kernels and download (event-ordered)
         xh = x.cpu().pin_memory()
         hb = {m: torch.empty(p1 - p0, dtype=torch.float32).pin_memory() for m in metrics}
         xd = torch.empty_like(x)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in, ev_k1, ev_pm, ev_out = (torch.cuda.Event() for _ in range(4))
+        cur = torch.cuda.current_stream(dev)
+        for ev in (ev_k1, ev_out):
+            ev.record(cur)
 
         def e2e_step():
-            xd.copy_(xh, non_blocking=True)
+            s_in.wait_event(ev_k1)                 # the previous K1 has consumed xd
+            with torch.cuda.stream(s_in):
+                xd.copy_(xh, non_blocking=True)
+                ev_in.record(s_in)
+            cur.wait_event(ev_in)
             local.spectra(xd, 0)
+            ev_k1.record(cur)
             allgather_ring(L32, F32, dist, g32)
             allgather_ring(L64, F64, dist, g64)
+            cur.wait_event(ev_out)                 # the previous download has read the outputs
             o = full.pair_metrics(slots, metrics, 0, c.n_bins, per_bin=False, band=True, row_tiles=(rb, re),
                                   pair_base=p0, pair_count=p1 - p0)
-            for m in metrics:
-                hb[m].copy_(o[m]["band"], non_blocking=True)
+            ev_pm.record(cur)
+            s_out.wait_event(ev_pm)
+            with torch.cuda.stream(s_out):
+                for m in metrics:
+                    hb[m].copy_(o[m]["band"], non_blocking=True)
+                ev_out.record(s_out)
         e2e_step()
         barrier()
         full.set_profiling(False)
@@ -615,6 +633,7 @@ def main():
         e0.record()
         for _ in range(args.e2e_steps):
             e2e_step()
+        cur.wait_event(ev_out)
         e1.record()
         barrier()
         t = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], device=dev)
@@ -622,7 +641,9 @@ def main():
         line["e2e"] = {"value": c.updates / (float(t) * 1e-3), "unit": "updates/s",
                        "h2d_bytes_per_step": xh.numel() * xh.element_size() * ws,
                        "d2h_bytes_per_step": sum(v.numel() * 4 for v in hb.values()) * ws,
-                       "ms_per_step": float(t), "path": "pinned host samples -> H2D -> K1 -> pair kernels -> band means D2H"}
+                       "ms_per_step": float(t), "steps": args.e2e_steps,
+                       "path": "per rank: pinned host node block -> H2D (copy stream) -> K1 -> all-gather -> pair "
+                               "rows -> band means D2H (copy stream); steps back to back"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
