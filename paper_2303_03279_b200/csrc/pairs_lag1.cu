@@ -19,7 +19,7 @@
 
 namespace cs {
 
-constexpr int k1Rows = 25;         // max operand rows (trial pair x taper) per stage
+constexpr int k1Rows = 26;         // max operand rows (trial pair x taper) per stage
 constexpr int k1Stages = 2;
 constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
 constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
@@ -98,7 +98,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   __syncthreads();
 
   const int n_stage = (a.Kp + KCL - 1) / KCL;
-  const int kc = (a.Kp + n_stage - 1) / n_stage;   // balanced stage size (<= KCL trial pairs)
+  int kc = (a.Kp + n_stage - 1) / n_stage;         // balanced stage size (<= KCL trial pairs)
+  if (L == 1 && (kc & 1) && kc < KCL) ++kc;        // even stages: the 2-unrolled loop has no remainder
   const int total = n_stage * nbl;
 
   // TMA issue (warp 0, lane 0): stage t into slot t % stages once every warp has
