@@ -230,6 +230,9 @@ static bool imag_on_tensor_cores(unsigned mask) {
   return (mask & CS_IMAGCOHY) && !(mask & (CS_PLI | CS_USPLI | CS_WPLI | CS_DSWPLI | CS_COHY));
 }
 
+bool run_pairs_lagtc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, float* const* bins,
+                     float* const* band, int64_t pair_base, int64_t pair_stride, cudaStream_t st);
+
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
   if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
@@ -248,7 +251,11 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.N64 = (p.N + kTile - 1) / kTile * kTile;
   a.slots = slots; a.K = K;
   a.Kp = (K + 1) / 2;
-  {
+  // CUDA-core kernel (pairs_lag1.cu) by default; CSCONN_K3=tc selects the single-taper
+  // tensor-core variant (pairs_lagtc.cu: parity-equal, measured slower at cfg5)
+  static const bool want_tc = getenv("CSCONN_K3") && getenv("CSCONN_K3")[0] == 't';
+  const bool use_tc = p.L == 1 && want_tc;
+  if (!use_tc) {
     const size_t need = (size_t)2 * nbb * a.Kp * p.L * a.N64 * sizeof(float4);
     if (need > p.lag_bytes) {
       if (p.lag_ops) cudaFreeAsync(p.lag_ops, st);
@@ -282,6 +289,14 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.flags = p.flags;
   a.counters = p.counters;
   a.flag_cap = p.flag_cap;
+  if (use_tc) {
+    cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
+    if (!run_pairs_lagtc(p, slots, K, bin_lo, nbb, rb, re, a.bins, a.band, a.pair_base, a.pair_stride, st))
+      return -1;
+    PhaseMark ph(p, "lag_fallback", st);
+    k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
+    return 2;
+  }
   int64_t n_tiles = 0;
   for (int I = rb; I < re; ++I) n_tiles += a.nt - I;
   if (!run_pairs_lag(p, a, n_tiles, st)) return -1;

@@ -610,6 +610,45 @@ size_t tc_smem_bytes() {
          kTcTile * 8 + 256;
 }
 
+// Tile list (I, J), J >= 2 I, of 128 x 64 tiles over the row range [i_lo, i_hi), in a
+// grouped order: bands of 8 row tiles swept column by column, so the CTAs resident at
+// once touch ~8 x 128 + 18 x 64 nodes of operands (L2 resident).  Built once per row
+// range and cached in the plan (a blocking upload: first call for that range only).
+const int2* tc_tile_list(Plan& p, int i_lo, int i_hi, int nt64, int64_t* n_tiles, cudaStream_t st) {
+  const int tile_row0 = i_lo / kTcTile;
+  const int tile_row1 = (i_hi + kTcTile - 1) / kTcTile;
+  const uint64_t key = ((uint64_t)tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)nt64;
+  Plan::TileList* tle = nullptr;
+  for (auto& e : p.tc_tiles)
+    if (e.key == key && e.ptr) tle = &e;
+  if (!tle) {
+    std::vector<int2> tl;
+    constexpr int GR = 8;
+    for (int b0 = tile_row0; b0 < tile_row1; b0 += GR)
+      for (int J = 0; J < nt64; ++J)
+        for (int I = b0; I < b0 + GR && I < tile_row1; ++I)
+          if (J >= 2 * I) tl.push_back(make_int2(I, J));
+    tle = &p.tc_tiles[p.tc_tiles_next];
+    p.tc_tiles_next = (p.tc_tiles_next + 1) % Plan::kTileCache;
+    if (tle->ptr) {
+      cudaStreamSynchronize(st);  // the evicted list may still be read by queued work
+      cudaFree(tle->ptr);
+    }
+    tle->ptr = nullptr;
+    tle->key = key;
+    tle->n = (int64_t)tl.size();
+    const size_t bytes = (tl.empty() ? 1 : tl.size()) * sizeof(int2);
+    if (cudaMalloc(&tle->ptr, bytes) != cudaSuccess) {
+      tle->ptr = nullptr;
+      cs_set_error("device allocation failed (tile list)");
+      return nullptr;
+    }
+    if (!tl.empty()) cudaMemcpy(tle->ptr, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  }
+  *n_tiles = tle->n;
+  return (const int2*)tle->ptr;
+}
+
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
                   bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
@@ -658,40 +697,10 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.i_hi = re * kTile < p.N ? re * kTile : p.N;
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
   a.tile_row0 = a.i_lo / kTcTile;
-  const int tile_row1 = (a.i_hi + kTcTile - 1) / kTcTile;
-  // grouped tile order: bands of 8 row tiles swept column by column, so the CTAs
-  // resident at once touch ~8 x 128 + 18 x 64 nodes of operands (L2 resident)
-  const uint64_t key = ((uint64_t)a.tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)a.nt;
-  Plan::TileList* tle = nullptr;
-  for (auto& e : p.tc_tiles)
-    if (e.key == key && e.ptr) tle = &e;
-  if (!tle) {  // build once per row range (a blocking upload: first call for that range only)
-    std::vector<int2> tl;
-    constexpr int GR = 8;
-    for (int b0 = a.tile_row0; b0 < tile_row1; b0 += GR)
-      for (int J = 0; J < a.nt; ++J)
-        for (int I = b0; I < b0 + GR && I < tile_row1; ++I)
-          if (J >= 2 * I) tl.push_back(make_int2(I, J));
-    tle = &p.tc_tiles[p.tc_tiles_next];
-    p.tc_tiles_next = (p.tc_tiles_next + 1) % Plan::kTileCache;
-    if (tle->ptr) {
-      cudaStreamSynchronize(st);  // the evicted list may still be read by queued work
-      cudaFree(tle->ptr);
-    }
-    tle->ptr = nullptr;
-    tle->key = key;
-    tle->n = (int64_t)tl.size();
-    const size_t bytes = (tl.empty() ? 1 : tl.size()) * sizeof(int2);
-    if (cudaMalloc(&tle->ptr, bytes) != cudaSuccess) {
-      tle->ptr = nullptr;
-      cs_set_error("device allocation failed (tile list)");
-      return false;
-    }
-    if (!tl.empty()) cudaMemcpy(tle->ptr, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice);
-  }
-  const int64_t n_tiles = tle->n;
+  int64_t n_tiles = 0;
+  a.tiles = tc_tile_list(p, a.i_lo, a.i_hi, a.nt, &n_tiles, st);
+  if (!a.tiles) return false;
   a.n_tiles = (int)n_tiles;
-  a.tiles = (const int2*)tle->ptr;
   {  // small pair spaces: split bins over CTAs.  Persistent CTAs overlap most of a
      // work unit's fixed cost, so the time is ~ rounds x (unit overhead + bins x
      // per-bin cost) with the overhead ~2 bins (cfg1/2/4 sweeps); pick the split
