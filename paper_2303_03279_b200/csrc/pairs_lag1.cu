@@ -26,7 +26,10 @@ constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
 constexpr int k1NP = k1TR * k1TC;
 constexpr int k1Warps = k1TY * k1TX / 32;  // compute warps
 constexpr int k1Threads = k1Warps * 32;        // multitaper: lane 0 of warp 0 also issues the TMA loads
-constexpr int k1ThreadsP = k1Threads + 32;     // single taper: plus a dedicated TMA producer warp
+// single taper: plus a producer warpgroup (warp 16 issues the TMA loads, 17-19 idle) whose
+// registers go to the compute warps with setmaxnreg (launch pool 640 x 96 = 128 x 24 +
+// 512 x 112), so the compute warps run with 112 registers instead of 96
+constexpr int k1ThreadsP = k1Threads + 128;
 constexpr int k1StageF4 = k1Rows * kTile;  // float4 per side per stage
 constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 
@@ -47,15 +50,16 @@ struct Lag1Args {
   int flag_cap;
 };
 
-// L == 1 uses a dedicated producer warp (17 warps: the per-SMSP register file
-// then allows 96 registers, enough for the single-taper loop); L > 1 needs 128
-// registers, so 16 warps with the TMA issued from warp 0 (measured: the dedicated
-// warp is 2.7 % faster for L == 1 on cfg5).
+// L == 1 uses a dedicated producer warpgroup (20 warps; setmaxnreg gives the 16 compute
+// warps 112 registers and the producers 24); L > 1 needs 128 registers, so 16 warps
+// with the TMA issued from warp 0.
 // STATS: which per-pair trial statistics the requested metrics need (the exact-sign
 // guard min |t| is always kept): 1 = #(t < 0) (PLI, USPLI), 2 = sum t (IMAGCOHY, WPLI,
 // DSWPLI), 4 = sum |t| (WPLI, DSWPLI).  Single taper only; multitaper runs all.
 constexpr unsigned kStSign = 1, kStSum = 2, kStAbs = 4, kStAll = 7;
-template <int L, bool PLVK, unsigned STATS = kStAll>
+// FULL: every per-bin and band output is requested (the fused all-metrics call), so the
+// epilogue needs no per-store pointer checks.
+template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -86,6 +90,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     bin_mask |= (a.plv_bins != nullptr) << 5;
     band_mask |= (a.plv_band != nullptr) << 5;
   }
+  if (FULL) bin_mask = band_mask = 31u;
   if (threadIdx.x == 0) {
     for (int s = 0; s < k1Stages; ++s) {
       mbar_init(&full[s], 1);
@@ -118,8 +123,9 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     }
   };
   if (kDedicated) {
-    if (warp == k1Warps) {  // producer warp: the whole stage sequence
-      if (lane == 0)
+    if (warp >= k1Warps) {  // producer warpgroup: 24 registers; warp 16 lane 0 issues the stages
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+      if (warp == k1Warps && lane == 0)
         for (int t = 0; t < total; ++t) {
           const int s = t % k1Stages;
           mbar_wait_backoff(&empty[s], ((t / k1Stages) & 1) ^ 1);
@@ -131,6 +137,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         }
       return;
     }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
   } else {
     for (int t = 0; t < k1Stages - 1; ++t) issue(t);
   }
@@ -439,7 +446,17 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
       case kStSum: CS_LAG1S(1, false, kStSum); break;
       case kStSign | kStSum: CS_LAG1S(1, false, kStSign | kStSum); break;
       case kStSum | kStAbs: CS_LAG1S(1, false, kStSum | kStAbs); break;
-      default: CS_LAG1(1, false); break;
+      default: {
+        bool full = true;
+        for (int m = 0; m < 5; ++m) full = full && bins[m] && band[m];
+        if (full) {
+          CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, true>), smem);
+          k_pairs_lag1<1, false, kStAll, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
+        } else {
+          CS_LAG1(1, false);
+        }
+        break;
+      }
     }
   } else if (L == 2) {
     if (plvk) CS_LAG1(2, true);
