@@ -244,6 +244,10 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   const int npass = a.do_x + a.do_u;
   const int pass0 = a.do_x ? 0 : 1;
 
+  // register budgets: warps 0-3 (TMA, MMA, TMEM allocator, spare) drop to 32, the
+  // epilogue warps rise to 112 (launch pool 640 x 96 = 128 x 32 + 512 x 112)
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -320,7 +324,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
           tc_commit_elect(&tfull[reg]);      // accumulators of (bin, pass) complete
         }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
     // ------------------------------------------------------------ epilogue
     // warp e = warp - 4: TMEM lane quadrant q = warp % 4 (hardware rule), column group h
     const int e = warp - 4, q = warp & 3, h = e >> 2;
