@@ -51,7 +51,9 @@ CASES = ["rect_small", "rect_accept", "rect_crop_oddk", "rect_pad_k1", "hann_cfg
 FAMILIES = {"lag": LAG, "coherency": COHF, "imag_tc": ("IMAGCOHY",), "coh_imag_tc": ("COH", "IMAGCOHY", "PLV"),
             "cohy_imag": ("COHY", "IMAGCOHY"),
             # phase-lag kernel variants that skip statistics no requested metric needs
-            "pli_only": ("PLI", "USPLI"), "wpli_only": ("WPLI", "DSWPLI"), "imag_pli": ("IMAGCOHY", "PLI")}
+            "pli_only": ("PLI", "USPLI"), "wpli_only": ("WPLI", "DSWPLI"), "imag_pli": ("IMAGCOHY", "PLI"),
+            # the fused seven (no COHY): IMAGCOHY from the tensor-core pass, sum Im for WPLI read from it
+            "fused7": ("COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI")}
 
 
 @pytest.mark.parametrize("family", list(FAMILIES))
@@ -120,15 +122,18 @@ def test_float32_input_path():
     (2, 1, 40, 64, 1, 1, None), (3, 2, 64, 64, 0, 32, None), (63, 3, 100, 128, 5, 9, "hann"),
     (65, 7, 128, 128, 2, 40, None), (129, 5, 90, 128, 10, 10, "hann"), (130, 4, 256, 256, 1, 127, ("dpss", 2.0, 2)),
     (200, 9, 300, 300, 3, 30, None)])
-def test_tile_boundary_shapes(N, K, T, nfft, lo, hi, taper):
+@pytest.mark.parametrize("with_cohy", [True, False])
+def test_tile_boundary_shapes(N, K, T, nfft, lo, hi, taper, with_cohy):
     """Node counts around the 64 / 128 tile edges, K = 1, 2 and odd, single-bin
-    bands, non-power-of-two nfft, all metrics against the oracle."""
+    bands, non-power-of-two nfft, all metrics against the oracle (with and without
+    COHY: without it IMAGCOHY comes from the tensor-core pass and feeds WPLI)."""
     import oracle as O
     from paper_2303_03279_b200 import compute_connectivity
     from paper_2303_03279_b200.plan import make_taper
     rng = np.random.default_rng(N * 1000 + K)
     x = rng.standard_normal((K, N, T))
-    metrics = [m for m in ("COHY", "COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI") if not (m == "USPLI" and K < 2)]
+    metrics = [m for m in ("COHY", "COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI")
+               if not (m == "USPLI" and K < 2) and (with_cohy or m != "COHY")]
     out, _ = compute_connectivity(torch.tensor(x, device="cuda"), nfft, lo, hi, metrics=metrics, taper=taper)
     tp = make_taper(taper, min(T, nfft))
     tp = None if tp is None else (tp[0] if tp.shape[0] == 1 else tp)
