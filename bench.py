@@ -648,8 +648,10 @@ def main():
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         n_cpu = min(args.cpu_nodes or 768, c.N)
-        r = cpu_baseline(c, n_cpu, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": r["updates"] / r["s"], "unit": "updates/s", "cores": 1, "kind": "port",
+        n_thr = os.cpu_count() or 1
+        r = cpu_baseline(c, n_cpu, n_thr)
+        # cores = the threads the run used (the FFT pool); the fold itself is single-threaded
+        line["cpu_baseline"] = {"value": r["updates"] / r["s"], "unit": "updates/s", "cores": n_thr, "kind": "port",
                                 "sample": f"node subset N'={n_cpu} of cfg{c.cfg}, all K={c.K}, {c.n_bins} bins, "
                                           f"{len(c.metrics)} finalizers; fold single-threaded as in the reference "
                                           f"(FFT pool of {os.cpu_count()} threads)",
