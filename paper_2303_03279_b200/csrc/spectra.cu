@@ -668,7 +668,7 @@ k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stri
 // register DFT over m, twiddle W_32^{h k'} and an R-point DFT across the R lanes
 // by shuffles.  Shared memory is touched twice per element (no per-stage
 // exchanges), butterflies stay in registers: FP64-pipe bound.
-constexpr int kFft4Warps = 4;
+constexpr int kFft4Warps = 8;
 
 __constant__ double2 c_w16[16] = {
     {1.0, 0.0},
@@ -725,7 +725,7 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
 }
 
 template <typename Tin, int A>
-__global__ void __launch_bounds__(kFft4Warps * 32, 4)
+__global__ void __launch_bounds__(kFft4Warps * 32, 2)
 k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N, int T_eff, int lo,
                int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw4,
                const double2* __restrict__ post_tw, const double2* __restrict__ wsum, int slot0, int slot_cap,
