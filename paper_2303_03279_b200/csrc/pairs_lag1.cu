@@ -19,8 +19,14 @@
 
 namespace cs {
 
-constexpr int k1Rows = 26;         // max operand rows (trial pair x taper) per stage
-constexpr int k1Stages = 2;
+#ifndef CS_K3_ROWS
+#define CS_K3_ROWS 26
+#endif
+#ifndef CS_K3_STAGES
+#define CS_K3_STAGES 2
+#endif
+constexpr int k1Rows = CS_K3_ROWS;       // max operand rows (trial pair x taper) per stage
+constexpr int k1Stages = CS_K3_STAGES;   // (build-time overrides for stage sweeps)
 constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
 constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
 constexpr int k1NP = k1TR * k1TC;
