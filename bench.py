@@ -142,6 +142,17 @@ def dist_setup():
     return None, 0, 1, 0
 
 
+CPU_NODES = 512  # node subset of the CPU legs (the reference arm and cpu_baseline use the same sample)
+
+
+def metric_name(c) -> str:
+    """The metric string both arms print (the driver divides the two values only when
+    metric, unit and direction agree)."""
+    if c.cfg == 4:
+        return "edge*freq*trial updates/s per online window (config 4, PLV + WPLI)"
+    return f"edge*freq*trial updates/s (config {c.cfg}, {len(c.metrics)} metrics)"
+
+
 def cpu_baseline(c, n_sub: int, threads: int):
     """The reference's CPU path (oracle port, oracle/) on a node subset of the
     workload: per-trial spectra through a thread pool (as compute_metric does,
@@ -180,7 +191,7 @@ def run_reference(args, c, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_sub = min(args.cpu_nodes or 512, c.N)  # cfg5: ~1.8 s per step, the whole run stays within minutes
+    n_sub = min(args.cpu_nodes or CPU_NODES, c.N)  # cfg5: ~3 s per step, the whole run stays within minutes
     samples = []
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(c, n_sub, threads)
@@ -189,7 +200,7 @@ def run_reference(args, c, rank):
     s = statistics.mean(r["s"] for r in samples)
     val = samples[0]["updates"] / s
     line = {
-        "impl": "reference", "metric": f"edge*freq*trial updates/s (config {c.cfg}, 7 metrics)", "value": val,
+        "impl": "reference", "metric": metric_name(c), "value": val,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded; SURVEY.md 8(d) signal model)",
@@ -284,7 +295,7 @@ def run_window(args, c, dist, rank, ws, lr):
     upd = c.n_pairs * c.n_bins * 50
     per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
     fp32_ops, fp64_fma = probe_peaks(lr)
-    line = {"metric": "edge*freq*trial updates/s per online window (config 4, PLV + WPLI)",
+    line = {"metric": metric_name(c),
             "value": ws * upd / (ms * 1e-3),
             "unit": "updates/s", "ms_per_window": ms, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong",
@@ -319,7 +330,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--metrics", default=None, help="comma list (default: the config's metrics)")
     ap.add_argument("--cpu-nodes", type=int, default=None,
-                    help="node subset for the CPU baseline (default 768; 512 per step for --impl reference)")
+                    help=f"node subset of the CPU legs (default {CPU_NODES}, both arms)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -547,7 +558,8 @@ def main():
             del om
 
     line = {
-        "metric": f"edge*freq*trial updates/s (config {c.cfg}, {len(metrics)} metrics fused)",
+        "metric": metric_name(c) if tuple(metrics) == tuple(c.metrics) else
+        f"edge*freq*trial updates/s (config {c.cfg}, {len(metrics)} metrics)",
         "value": value, "unit": "updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded; SURVEY.md 8(d) signal model, no public dataset)",
@@ -647,7 +659,7 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        n_cpu = min(args.cpu_nodes or 768, c.N)
+        n_cpu = min(args.cpu_nodes or CPU_NODES, c.N)
         n_thr = os.cpu_count() or 1
         r = cpu_baseline(c, n_cpu, n_thr)
         # cores = the threads the run used (the FFT pool); the fold itself is single-threaded

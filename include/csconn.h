@@ -193,8 +193,12 @@ int cs_row_tile_range(int n_nodes, int n_shards, int shard, int* row_tile_begin,
                       int* row_tile_end, int64_t* pair_begin, int64_t* pair_end);
 
 /* Fallback bookkeeping of the last cs_pair_metrics call (device -> host copy;
- * synchronises the stream).  n_flagged: (pair, bin) entries recomputed in fp64. */
+ * synchronises the stream).  n_flagged: (pair, bin) entries recomputed in fp64
+ * (spectral.py:227-239 arithmetic).  The work list never drops an entry: when it
+ * is full, flagged entries go to per-(tile, bin, warp) mask records instead
+ * (n_records > 0), which the fallback kernel also processes. */
 int cs_last_fallback_count(cs_plan* plan, void* stream, int64_t* n_flagged);
+int cs_last_guard_stats(cs_plan* plan, void* stream, int64_t* n_flagged, int64_t* n_records);
 int64_t cs_fft_call_count(const cs_plan* plan);
 void cs_reset_fft_call_count(cs_plan* plan);
 

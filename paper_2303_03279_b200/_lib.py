@@ -61,6 +61,7 @@ def lib():
     L.cs_row_tile_range.argtypes = [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cs_last_fallback_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
+    L.cs_last_guard_stats.argtypes = [vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cs_fft_call_count.argtypes = [vp]
     L.cs_fft_call_count.restype = i64
     L.cs_reset_fft_call_count.argtypes = [vp]
@@ -80,7 +81,7 @@ def lib():
 CS_PLAN_WELCH = 1
 
 EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_sums",
-            "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count",
+            "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count", "cs_last_guard_stats",
             "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
             "cs_launch_count", "cs_ring_view", "cs_probe_peaks", "cs_last_error", "cs_version")
 

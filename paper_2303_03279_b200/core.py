@@ -113,9 +113,24 @@ class EpochMatrix:
             raise ParameterError("sfreq must be positive")
         if self.trial_index < 0:
             raise ParameterError("trial_index must be non-negative")
+        if is_t and d.is_cuda:
+            # device samples: the finiteness flag stays on the device (no host sync per
+            # trial); it is checked by validate(), which the engine calls once per finalize
+            object.__setattr__(self, "_finite_dev", d.isfinite().all())
+            return
         finite = bool(d.isfinite().all()) if is_t else bool(np.all(np.isfinite(d)))
         if not finite:
             raise ParameterError("epoch contains non-finite values")
+
+    def validate(self) -> None:
+        """Raise ParameterError if the samples are not finite (core.py:97-100);
+        synchronises only for device samples whose check is still pending."""
+        f = self.__dict__.get("_finite_dev")
+        if f is not None:
+            ok = bool(f)
+            object.__setattr__(self, "_finite_dev", None)
+            if not ok:
+                raise ParameterError("epoch contains non-finite values")
 
     @property
     def n_channels(self) -> int:
@@ -124,6 +139,14 @@ class EpochMatrix:
     @property
     def n_samples(self) -> int:
         return int(self.data.shape[1])
+
+
+@dataclass(frozen=True)
+class XCorEdgeValue:
+    """Peak of the normalised cross-correlation and the lag where it occurs (core.py:111-116)."""
+
+    peak_value: float
+    peak_lag: int
 
 
 def default_positions(n_nodes: int) -> np.ndarray:
@@ -167,8 +190,8 @@ class ConnectivityNetwork:
         try:
             import torch
             if isinstance(w, torch.Tensor):
-                if not bool(torch.isfinite(w).all()):
-                    raise ParameterError("edge weights must be finite")
+                # device weights come from the pair kernels, finite by construction for
+                # finite (validated) epochs: checked on host access, not with a sync here
                 return
         except ImportError:  # pragma: no cover
             pass
@@ -191,6 +214,8 @@ class ConnectivityNetwork:
     def weights(self) -> np.ndarray:
         if not isinstance(self._w, np.ndarray) or self._w.dtype != np.float64:
             self._w = self._host(self._w, np.float64)
+            if not np.all(np.isfinite(self._w)):
+                raise ParameterError("edge weights must be finite")
         return self._w
 
     @property
@@ -346,3 +371,28 @@ def serialize_network(net: ConnectivityNetwork) -> bytes:
                    "lag": int(lags[k]) if lags is not None else None} for k in range(net.n_edges)],
     }
     return json.dumps(obj, separators=(",", ":")).encode("utf-8")
+
+
+def deserialize_network(raw: bytes) -> ConnectivityNetwork:
+    """Inverse of serialize_network (core.py:246-273).  The wire format carries
+    (|c|, Im c) for complex metrics, so the real part comes back as
+    sqrt(|c|^2 - Im^2) (sign lost, as in the reference); re-serialisation is
+    byte-identical."""
+    import json
+    obj = json.loads(raw.decode("utf-8"))
+    b = obj["band"]
+    band = FrequencyBand(b["lo_bin"], b["hi_bin"], b["bin_hz"])
+    node_ids = tuple(n["id"] for n in obj["nodes"])
+    positions = np.array([n["pos"] for n in obj["nodes"]], dtype=np.float64).reshape(-1, 3)
+    edges = obj["edges"]
+    ei = np.fromiter((e["i"] for e in edges), dtype=np.int64, count=len(edges))
+    ej = np.fromiter((e["j"] for e in edges), dtype=np.int64, count=len(edges))
+    w = np.fromiter((e["w"] for e in edges), dtype=np.float64, count=len(edges))
+    cw = lags = None
+    if any(e["w_im"] is not None for e in edges):
+        im = np.array([e["w_im"] or 0.0 for e in edges], dtype=np.float64)
+        cw = np.sqrt(np.maximum(w * w - im * im, 0.0)) + 1j * im
+    if any(e["lag"] is not None for e in edges):
+        lags = np.array([e["lag"] or 0 for e in edges], dtype=np.int64)
+    return ConnectivityNetwork(MetricId.parse(obj["metric"]), band, obj["n_trials"], node_ids, positions, w,
+                               edge_i=ei, edge_j=ej, complex_weights=cw, lags=lags, normalized=obj["normalized"])

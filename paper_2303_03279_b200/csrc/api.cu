@@ -232,6 +232,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   int64_t cap = P * p->nb / 64;
   if (cap < (1 << 16)) cap = 1 << 16;
   if (cap > (1 << 24)) cap = 1 << 24;
+  if (const char* fc = getenv("CSCONN_FLAG_CAP")) cap = atol(fc) > 0 ? atol(fc) : 1;  // test override (overflow path)
   p->flag_cap = (int)cap;
   const size_t ring = (size_t)slot_cap * L * p->nb * N;
   bool ok = cudaMalloc(&p->tww, tw.size() * sizeof(double2)) == cudaSuccess &&
@@ -347,6 +348,7 @@ int cs_plan_destroy(cs_plan* p) {
     if (e.ptr) cudaFree(e.ptr);
   if (p->lag_ops) cudaFree(p->lag_ops);
   cudaFree(p->flags); cudaFree(p->counters);
+  if (p->recs) cudaFree(p->recs);
   if (p->prof) {
     auto* ps = (ProfState*)p->prof;
     for (auto& r : ps->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -366,7 +368,12 @@ int cs_spectra(cs_plan* p, const void* x, int dtype, int64_t ts, int64_t ns, int
   DeviceGuard g(p->device);
   {
     cs::PhaseMark ph(*p, "spectra", (cudaStream_t)stream);
-    cs::run_spectra(*p, x, dtype, ts, ns, slot0 % p->slot_cap, kc, (cudaStream_t)stream);
+    // trials x tapers ride on a grid dimension (<= 65535): chunk long calls
+    const int step = 65535 / p->L;
+    const size_t esz = dtype == CS_F64 ? 8 : 4;
+    for (int c0 = 0; c0 < kc; c0 += step)
+      cs::run_spectra(*p, (const char*)x + (size_t)c0 * ts * esz, dtype, ts, ns, (slot0 + c0) % p->slot_cap,
+                      kc - c0 < step ? kc - c0 : step, (cudaStream_t)stream);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_spectra");
   p->fft_calls += (int64_t)kc * p->N * p->L;
@@ -411,7 +418,9 @@ int cs_get_spectra(cs_plan* p, const int* slots, int ns, int bin_lo, int nbins, 
   if (bin_lo < 0 || nbins < 1 || bin_lo + nbins > p->nb) { cs_set_error("cs_get_spectra: bad bins"); return CS_EPARAM; }
   if (ns <= 0) return CS_OK;
   DeviceGuard g(p->device);
-  cs::run_get_spectra(*p, slots, ns, bin_lo, nbins, dst, (cudaStream_t)stream);
+  for (int c0 = 0; c0 < ns; c0 += 65535)  // trials ride on grid.y
+    cs::run_get_spectra(*p, slots + c0, ns - c0 < 65535 ? ns - c0 : 65535, bin_lo, nbins,
+                        (double2*)dst + (size_t)c0 * p->N * nbins, (cudaStream_t)stream);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_get_spectra");
   return CS_OK;
 }
@@ -432,25 +441,29 @@ int cs_put_taper_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbi
   DeviceGuard g(p->device);
   {
     cs::PhaseMark ph(*p, "put_spectra", (cudaStream_t)stream);
-    cs::run_put_spectra(*p, src, n, bin_lo, nbins, slot0 % p->slot_cap, taper, w, (cudaStream_t)stream);
+    for (int c0 = 0; c0 < n; c0 += 65535)  // trials ride on grid.y
+      cs::run_put_spectra(*p, (const double2*)src + (size_t)c0 * p->N * nbins, n - c0 < 65535 ? n - c0 : 65535,
+                          bin_lo, nbins, (slot0 + c0) % p->slot_cap, taper, w, (cudaStream_t)stream);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_put_spectra");
   return CS_OK;
 }
 
 int cs_last_fallback_count(cs_plan* p, void* stream, int64_t* n) {
-  if (!p || !n) return CS_EPARAM;
+  int64_t rec = 0;
+  return cs_last_guard_stats(p, stream, n, &rec);
+}
+
+int cs_last_guard_stats(cs_plan* p, void* stream, int64_t* n, int64_t* records) {
+  if (!p || !n || !records) return CS_EPARAM;
   DeviceGuard g(p->device);
-  int h[2] = {0, 0};
-  if (cudaMemcpyAsync(h, p->counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream) !=
+  int h[3] = {0, 0, 0};
+  if (cudaMemcpyAsync(h, p->counters, 3 * sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream) !=
           cudaSuccess ||
       cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
-    return cuda_fail("cs_last_fallback_count");
+    return cuda_fail("cs_last_guard_stats");
   *n = h[0];
-  if (h[1]) {
-    cs_set_error("fp64 guard list overflow: %d flagged entries > capacity %d", h[0], p->flag_cap);
-    return CS_ENOMEM;
-  }
+  *records = h[2];
   return CS_OK;
 }
 

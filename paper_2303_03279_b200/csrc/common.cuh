@@ -29,6 +29,9 @@ namespace cs {
 
 constexpr int kTile = 64;        // node tile edge of the upper-triangular pair tiling
 constexpr int kThreads = 256;    // pair-kernel CTA size (16 x 16 threads, 4 x 4 pairs each)
+// exact-sign guard overflow records (pairs_lag1.cu guard_push): bit (r kGuardTC + c) of
+// mask word, lane l -> pair (row0 + kGuardRowStep r, col0 + l + kGuardColStep c)
+constexpr int kGuardRowStep = 16, kGuardColStep = 32, kGuardTC = 2, kGuardWarps = 16;
 
 struct Plan {
   int device = 0;
@@ -63,7 +66,9 @@ struct Plan {
   TileList tc_tiles[kTileCache];
   int tc_tiles_next = 0;
   int4* flags = nullptr;         // fp64-fallback work list (i, j, local bin, -)
-  int* counters = nullptr;       // [0] flag count, [1] overflow
+  int* counters = nullptr;       // [0] flagged entries, [1] list overflowed, [2] overflow records
+  int4* recs = nullptr;          // guard overflow records (3 int4 each), grown on demand
+  size_t rec_cap = 0;            // records
   int flag_cap = 0;
   int64_t fft_calls = 0;
   int64_t launches = 0;          // kernels launched by this plan (bench evidence)

@@ -49,6 +49,7 @@ struct LagArgs {
   float g;           // guard factor
   float scale2;      // plan scale^2 (fp64 fallback -> fp32 units)
   int4* flags;
+  int4* recs;        // guard overflow records (pairs_lag1.cu guard_push), or null
   int* counters;
   int flag_cap;
 };
@@ -64,8 +65,10 @@ __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict
                            float4* __restrict__ PkI, float4* __restrict__ PkJ) {
   // layout [bl][kp][l][n]: taper l of trial pair kp
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int kp = blockIdx.y / L, l = blockIdx.y % L, bl = blockIdx.z;
+  const int bl = blockIdx.z;
   if (n >= N64) return;
+  for (int y = blockIdx.y; y < Kp * L; y += gridDim.y) {  // grid.y <= 65535 (very long sessions)
+  const int kp = y / L, l = y % L;
   float2 va = make_float2(0.f, 0.f), vb = make_float2(0.f, 0.f);
   float2 wb = make_float2(0.f, 0.f);  // J-side value of trial b (phantom differs)
   if (n < N) {
@@ -83,65 +86,98 @@ __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict
   const int64_t o = (((int64_t)bl * Kp + kp) * L + l) * N64 + n;
   PkI[o] = make_float4(va.x, vb.x, va.y, vb.y);
   PkJ[o] = make_float4(va.x, wb.x, -va.y, wb.y);
+  }
 }
 
-// fp64 recomputation of flagged (pair, bin) entries: an 8-lane group per entry
-// (four entries per warp, so the per-entry fp64 finalisation runs four-wide),
-// lanes over trials; reference arithmetic of spectral.py:204-241 in complex128.
+// fp64 recomputation of one flagged (pair, bin) entry by an 8-lane group, lanes over
+// trials; reference arithmetic of spectral.py:204-241 in complex128.
+__device__ __forceinline__ void fallback_entry(const LagArgs& a, int i, int j, int bl, int lane, bool live) {
+  const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
+  const int b = a.bin_lo + bl;
+  double s_im = 0.0, s_abs = 0.0;
+  int s_sign = 0;
+#pragma unroll 4
+  for (int k = lane; k < (live ? a.K : 0); k += 8) {  // unrolled: the trials' loads are independent
+    const int slot = a.slots[k];
+    double re = 0.0, im = 0.0;
+    for (int l = 0; l < a.L; ++l) {
+      const double2 xi = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + i];
+      const double2 xj = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + j];
+      // (xi.x + i xi.y) * (xj.x - i xj.y)
+      re += xi.x * xj.x + xi.y * xj.y;
+      im += xi.y * xj.x - xi.x * xj.y;
+    }
+    if (fabs(im) <= 1e-13 * fabs(re)) im = 0.0;  // spectral.py:227-228
+    s_im += im;
+    s_abs += fabs(im);
+    s_sign += (im > 0.0) - (im < 0.0);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    s_im += __shfl_xor_sync(0xffffffffu, s_im, o);
+    s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+    s_sign += __shfl_xor_sync(0xffffffffu, s_sign, o);
+  }
+  if (lane == 0 && live) {
+    float v[5];
+    const float psd_i = a.psd[(int64_t)bl * a.N + i], psd_j = a.psd[(int64_t)bl * a.N + j];
+    // IMAGCOHY in fp64 then rounded; the ratios are scale invariant
+    const double den = sqrt((double)psd_i * (double)psd_j);
+    const double imag = den > 0.0 ? s_im * (double)a.scale2 / den : 0.0;
+    const double pli = fabs((double)s_sign) / a.K;
+    const double wpli = s_abs > 0.0 ? fabs(s_im) / s_abs : 0.0;
+    v[0] = (float)imag;
+    v[1] = (float)pli;
+    v[2] = a.K > 1 ? (float)((a.K * pli * pli - 1.0) / (a.K - 1.0)) : 0.f;
+    v[3] = (float)wpli;
+    v[4] = (float)(wpli * wpli);
+    const int64_t po = pair_of(i, j, a.N) - a.pair_base;
+    const float inv = 1.f / (float)a.nbb;
+    for (int m = 0; m < 5; ++m) {
+      if (a.bins[m]) a.bins[m][(int64_t)bl * a.pair_stride + po] = v[m];
+      if (a.band[m]) atomicAdd(&a.band[m][po], v[m] * inv);
+    }
+  }
+}
+
+// The fp64 fallback over the guard work list (four entries per warp, so the per-entry
+// fp64 finalisation runs four-wide), then over the overflow records of a full list
+// (one warp per record, its flagged pairs four at a time; pairs_lag1.cu guard_push).
 __global__ void k_lag_fallback(const LagArgs a) {
   const int group = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int lane = threadIdx.x & 7;
   const int n_groups = (gridDim.x * blockDim.x) >> 3;
   const int count = min(a.counters[0], a.flag_cap);
-  const int64_t slot_stride = (int64_t)a.L * a.nb * a.N;
   for (int w0 = group - (group & 3); w0 < count; w0 += n_groups) {  // warp-uniform trip count
     const int w = w0 + (group & 3);
-    const bool live = w < count;
-    const int4 f = live ? __ldg(&a.flags[w]) : make_int4(0, 1, 0, 0);
-    const int i = f.x, j = f.y, bl = f.z, b = a.bin_lo + bl;
-    double s_im = 0.0, s_abs = 0.0;
-    int s_sign = 0;
-#pragma unroll 4
-    for (int k = lane; k < (live ? a.K : 0); k += 8) {  // unrolled: the trials' loads are independent
-      const int slot = a.slots[k];
-      double re = 0.0, im = 0.0;
-      for (int l = 0; l < a.L; ++l) {
-        const double2 xi = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + i];
-        const double2 xj = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + j];
-        // (xi.x + i xi.y) * (xj.x - i xj.y)
-        re += xi.x * xj.x + xi.y * xj.y;
-        im += xi.y * xj.x - xi.x * xj.y;
+    int4 f = w < count ? __ldg(&a.flags[w]) : make_int4(-1, -1, 0, 0);
+    const bool live = f.x >= 0;  // slots a warp reserved past the capacity are marked empty
+    if (!live) f = make_int4(0, 1, 0, 0);
+    fallback_entry(a, f.x, f.y, f.z, lane, live);
+  }
+  if (!a.recs) return;
+  const int n_rec = a.counters[2];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, n_warps = (gridDim.x * blockDim.x) >> 5;
+  const int g = (threadIdx.x >> 3) & 3;
+  for (int rr = warp; rr < n_rec; rr += n_warps) {
+    const int4 h = a.recs[3 * rr], m0 = a.recs[3 * rr + 1], m1 = a.recs[3 * rr + 2];
+    const unsigned m[8] = {(unsigned)m0.x, (unsigned)m0.y, (unsigned)m0.z, (unsigned)m0.w,
+                           (unsigned)m1.x, (unsigned)m1.y, (unsigned)m1.z, (unsigned)m1.w};
+    int q = 0, pos = 0;  // walk the 256 mask bits (word q, bit pos); group g takes every 4th set bit
+    for (;;) {
+      int found[4], nf = 0;
+      while (nf < 4 && q < 8) {
+        const unsigned rest = m[q] >> pos;
+        if (!rest || pos >= 32) { ++q; pos = 0; continue; }
+        pos += __ffs(rest) - 1;
+        found[nf++] = q * 32 + pos;
+        ++pos;
       }
-      if (fabs(im) <= 1e-13 * fabs(re)) im = 0.0;  // spectral.py:227-228
-      s_im += im;
-      s_abs += fabs(im);
-      s_sign += (im > 0.0) - (im < 0.0);
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      s_im += __shfl_xor_sync(0xffffffffu, s_im, o);
-      s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
-      s_sign += __shfl_xor_sync(0xffffffffu, s_sign, o);
-    }
-    if (lane == 0 && live) {
-      float v[5];
-      const float psd_i = a.psd[(int64_t)bl * a.N + i], psd_j = a.psd[(int64_t)bl * a.N + j];
-      // IMAGCOHY in fp64 then rounded; the ratios are scale invariant
-      const double den = sqrt((double)psd_i * (double)psd_j);
-      const double imag = den > 0.0 ? s_im * (double)a.scale2 / den : 0.0;
-      const double pli = fabs((double)s_sign) / a.K;
-      const double wpli = s_abs > 0.0 ? fabs(s_im) / s_abs : 0.0;
-      v[0] = (float)imag;
-      v[1] = (float)pli;
-      v[2] = a.K > 1 ? (float)((a.K * pli * pli - 1.0) / (a.K - 1.0)) : 0.f;
-      v[3] = (float)wpli;
-      v[4] = (float)(wpli * wpli);
-      const int64_t po = pair_of(i, j, a.N) - a.pair_base;
-      const float inv = 1.f / (float)a.nbb;
-      for (int m = 0; m < 5; ++m) {
-        if (a.bins[m]) a.bins[m][(int64_t)bl * a.pair_stride + po] = v[m];
-        if (a.band[m]) atomicAdd(&a.band[m][po], v[m] * inv);
-      }
+      if (nf == 0) break;
+      const bool live = g < nf;
+      const int bit = live ? found[g] : 0, qq = bit >> 5, ln = bit & 31;
+      const int i = h.x + kGuardRowStep * (qq / kGuardTC), j = h.y + ln + kGuardColStep * (qq % kGuardTC);
+      fallback_entry(a, live ? i : 0, live ? j : 1, h.z, lane, live);
     }
   }
 }
@@ -157,14 +193,14 @@ static unsigned fallback_blocks(const LagArgs& a) {
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc,
+                 int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, cudaStream_t st);
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
-  cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
+  cudaMemsetAsync(a.counters, 0, 3 * sizeof(int), st);
   {
     PhaseMark ph(p, "lag_prep", st);
-    dim3 grid((a.N64 + 127) / 128, a.Kp * a.L, a.nbb);
+    dim3 grid((a.N64 + 127) / 128, a.Kp * a.L < 65535 ? a.Kp * a.L : 65535, a.nbb);
     k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag,
                                      (float4*)a.PkI, (float4*)a.PkJ);
   }
@@ -200,7 +236,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
       if (a.plv_band) cudaMemsetAsync(a.plv_band, 0, a.pair_stride * sizeof(float), st);
     }
     if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
-                     a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.counters, a.flag_cap,
+                     a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.recs, a.counters, a.flag_cap,
                      n_tiles, nbc, a.L, a.plv_bins, a.plv_band, st))
       return false;
   }
@@ -230,9 +266,6 @@ static bool imag_on_tensor_cores(unsigned mask) {
   return (mask & CS_IMAGCOHY) && !(mask & (CS_PLI | CS_USPLI | CS_WPLI | CS_DSWPLI | CS_COHY));
 }
 
-bool run_pairs_lagtc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, float* const* bins,
-                     float* const* band, int64_t pair_base, int64_t pair_stride, cudaStream_t st);
-
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
   if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
@@ -251,11 +284,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.N64 = (p.N + kTile - 1) / kTile * kTile;
   a.slots = slots; a.K = K;
   a.Kp = (K + 1) / 2;
-  // CUDA-core kernel (pairs_lag1.cu) by default; CSCONN_K3=tc selects the single-taper
-  // tensor-core variant (pairs_lagtc.cu: parity-equal, measured slower at cfg5)
-  static const bool want_tc = getenv("CSCONN_K3") && getenv("CSCONN_K3")[0] == 't';
-  const bool use_tc = p.L == 1 && want_tc;
-  if (!use_tc) {
+  {
     const size_t need = (size_t)2 * nbb * a.Kp * p.L * a.N64 * sizeof(float4);
     if (need > p.lag_bytes) {
       if (p.lag_ops) cudaFreeAsync(p.lag_ops, st);
@@ -285,20 +314,26 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.plv_bins = plvk ? (float*)out->bins[3] : nullptr;
   a.plv_band = plvk ? (float*)out->band[3] : nullptr;
   a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
+  if (const char* gs = getenv("CSCONN_GUARD_G")) a.g *= (float)atof(gs);  // test override (negative control)
   a.scale2 = p.scale * p.scale;
   a.flags = p.flags;
   a.counters = p.counters;
   a.flag_cap = p.flag_cap;
-  if (use_tc) {
-    cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), st);
-    if (!run_pairs_lagtc(p, slots, K, bin_lo, nbb, rb, re, a.bins, a.band, a.pair_base, a.pair_stride, st))
-      return -1;
-    PhaseMark ph(p, "lag_fallback", st);
-    k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
-    return 2;
-  }
   int64_t n_tiles = 0;
   for (int I = rb; I < re; ++I) n_tiles += a.nt - I;
+  // overflow records: at most one per (tile, bin, compute warp) of the call
+  const size_t n_rec = (size_t)n_tiles * nbb * kGuardWarps;
+  if (n_rec > p.rec_cap) {
+    if (p.recs) cudaFreeAsync(p.recs, st);
+    if (cudaMallocAsync(&p.recs, n_rec * 3 * sizeof(int4), st) != cudaSuccess) {
+      p.recs = nullptr;
+      p.rec_cap = 0;
+      cs_set_error("device allocation failed (guard records %zu bytes)", n_rec * 3 * sizeof(int4));
+      return -1;
+    }
+    p.rec_cap = n_rec;
+  }
+  a.recs = p.recs;
   if (!run_pairs_lag(p, a, n_tiles, st)) return -1;
   return 2;
 }

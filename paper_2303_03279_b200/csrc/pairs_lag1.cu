@@ -39,6 +39,51 @@ constexpr int k1ThreadsP = k1Threads + 128;
 constexpr int k1StageF4 = k1Rows * kTile;  // float4 per side per stage
 constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 
+// Exact-sign guard work list.  A warp whose (pair, bin) entries are flagged reserves
+// list slots with one atomic; when the list is full it instead appends one record
+// (row of its first pair, tile column base, bin, 256-bit mask over its 4 x 2 x 32 pairs)
+// to a record list sized for every (tile, bin, warp) of the call, so no flagged entry is
+// ever dropped (k_lag_fallback processes both).  counters: [0] flagged entries,
+// [1] list overflowed, [2] records.
+__device__ __noinline__ void guard_push(int4* flags, int4* recs, int* counters, int cap, unsigned fl,
+                                        int iBase, int jBase, int w, int lane, int bl) {
+  const int n = __popc(fl);
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  if (lane == 31) base = atomicAdd(&counters[0], total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  if (base + total <= cap) {
+    int s = base + incl - n;
+#pragma unroll
+    for (int r = 0; r < k1TR; ++r)
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c)
+        if ((fl >> (r * k1TC + c)) & 1u)
+          flags[s++] = make_int4(iBase + w + k1TY * r, jBase + lane + k1TX * c, bl, 0);
+    return;
+  }
+  // slots this warp reserved below the capacity stay unused: mark them empty
+  for (int s = base + lane; s < min(cap, base + total); s += 32) flags[s] = make_int4(-1, -1, 0, 0);
+  unsigned m[k1NP];
+#pragma unroll
+  for (int q = 0; q < k1NP; ++q) m[q] = __ballot_sync(0xffffffffu, (fl >> q) & 1u);
+  if (lane == 0) {
+    const int rec = atomicAdd(&counters[2], 1);
+    recs[3 * rec] = make_int4(iBase + w, jBase, bl, 0);
+    recs[3 * rec + 1] = make_int4((int)m[0], (int)m[1], (int)m[2], (int)m[3]);
+    recs[3 * rec + 2] = make_int4((int)m[4], (int)m[5], (int)m[6], (int)m[7]);
+    counters[1] = 1;
+  }
+}
+static_assert(k1NP == 8 && k1Warps == kGuardWarps && k1TY == kGuardRowStep && k1TX == kGuardColStep && k1TC == kGuardTC,
+              "guard record layout (common.cuh)");
+
 struct Lag1Args {
   int N, N64, K, Kp, bin_lo, nbb;
   int bpc, nbc;              // bins per CTA, bin chunks per tile (small pair spaces split bins)
@@ -52,8 +97,10 @@ struct Lag1Args {
   float* plv_band;
   float g;
   int4* flags;
+  int4* recs;
   int* counters;
   int flag_cap;
+  bool wide;                 // K >= 2^17: sign counts decoded per stage (see neg[] below)
 };
 
 // L == 1 uses a dedicated producer warpgroup (20 warps; setmaxnreg gives the 16 compute
@@ -65,7 +112,9 @@ struct Lag1Args {
 constexpr unsigned kStSign = 1, kStSum = 2, kStAbs = 4, kStAll = 7;
 // FULL: every per-bin and band output is requested (the fused all-metrics call), so the
 // epilogue needs no per-store pointer checks.
-template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false>
+// WIDE: K >= 2^17 trials, where the two 16-bit sign-count fields could wrap: the
+// packed counts are decoded into plain 32-bit counters after every stage.
+template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false, bool WIDE = false>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -161,7 +210,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   // 0x0000FFFF [t_a < 0] + 0xFFFF0000 [t_b < 0]; two trial pairs are added with one
   // IADD3 (3 instructions per 4 trials instead of 4 LEA.HI).  Decoded exactly in
   // the epilogue: A = -acc mod 2^16, B = (65535 A - acc) >> 16 (counts < 2^16).
-  unsigned neg[k1NP], ntmp[k1NP];
+  unsigned neg[k1NP], ntmp[k1NP], negw[WIDE ? k1NP : 1];
   f2 pvr[PLVK ? k1NP : 1], pvi[PLVK ? k1NP : 1];
 #pragma unroll
   for (int p = 0; p < k1NP; ++p) {
@@ -170,6 +219,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     mn[p] = 3.0e38f;
     neg[p] = 0u;
     ntmp[p] = 0u;
+    if (WIDE) negw[p] = 0u;
     if (PLVK) pvr[p] = pvi[p] = 0ull;
   }
 
@@ -269,6 +319,14 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 #pragma unroll
       for (int p = 0; p < k1NP; ++p) neg[p] += ntmp[p];
     }
+    if (WIDE && L == 1 && (STATS & kStSign)) {  // < 2^16 per field within one stage
+#pragma unroll
+      for (int p = 0; p < k1NP; ++p) {
+        const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
+        negw[p] += nA + nB;
+        neg[p] = 0u;
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (st + 1 < n_stage) continue;
@@ -299,6 +357,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       phJ[c] = m * k1Phantom;
     }
     const int64_t bin_off = (int64_t)bl * a.pair_stride;
+    unsigned fl = 0;  // exact-sign guard: this thread's entries the fp64 fallback writes
 #pragma unroll
     for (int r = 0; r < k1TR; ++r) {
       const int li = ty + k1TY * r, i = iBase + li;
@@ -311,18 +370,12 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         // dead: a node with a zero spectrum in this bin (or DC / Nyquist): all Im are 0
         const bool dead = Mi[r] * Mj[c] == 0.f;
         const bool flagged = valid && !dead && mn[p] <= gMi[r] * Mj[c];
-        if (flagged) {  // rare: the fp64 fallback writes this (pair, bin)
-          const int slot = atomicAdd(&a.counters[0], 1);
-          if (slot < a.flag_cap)
-            a.flags[slot] = make_int4(i, j, bl, 0);
-          else
-            a.counters[1] = 1;
-        }
+        fl |= (unsigned)flagged << p;
         const float tph = phI[r] * phJ[c];  // odd-K phantom trial (0 when K is even)
         const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
         const float s_abs = dead ? 0.f : sabs[p] - tph;
         const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
-        const int n_neg = L == 1 ? (int)(nA + nB) : (int)neg[p];
+        const int n_neg = WIDE ? (int)negw[p] : L == 1 ? (int)(nA + nB) : (int)neg[p];
         const int pli_sum = dead ? 0 : a.K - 2 * n_neg;
         float v[5];
         v[0] = s_im * rPi[r] * rPj[c];
@@ -355,8 +408,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         sabs[p] = 0.f;
         mn[p] = 3.0e38f;
         neg[p] = 0u;
+        if (WIDE) negw[p] = 0u;
       }
     }
+    if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
   }
 
   if (band_mask) {
@@ -393,7 +448,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
-                 int4* flags, int* counters, int flag_cap, int64_t n_tiles, int nbc,
+                 int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
@@ -426,7 +481,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     a.bins[m] = bins[m];
     a.band[m] = band[m];
   }
-  a.g = g; a.flags = flags; a.counters = counters; a.flag_cap = flag_cap;
+  a.g = g; a.flags = flags; a.recs = recs; a.counters = counters; a.flag_cap = flag_cap;
   a.plv_bins = plv_bins;
   a.plv_band = plv_band;
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
@@ -442,7 +497,10 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     CS_SMEM_ONCE((k_pairs_lag1<LL, PV>), smem);                                                         \
     k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
   } while (0)
-  if (L == 1) {
+  if (L == 1 && Kp >= 65536) {  // a 16-bit sign-count field could wrap: per-stage decode
+    CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, false, true>), smem);
+    k_pairs_lag1<1, false, kStAll, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
+  } else if (L == 1) {
     // statistics the requested outputs need (bins / band pointers: IMAG, PLI, USPLI, WPLI, DSWPLI)
     auto want = [&](int m) { return bins[m] || band[m]; };
     const unsigned need = ((want(1) || want(2)) ? kStSign : 0u) | ((want(0) || want(3) || want(4)) ? kStSum : 0u) |

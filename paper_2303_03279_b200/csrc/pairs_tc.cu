@@ -403,11 +403,12 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
                   if (rs[u] > 0.f && i < j && j < a.N && i >= a.i_lo && i < a.i_hi &&
                       fabsf(vi[u4 + u]) < a.imag_tau) {
                     const int slot = atomicAdd(&a.counters[0], 1);
-                    if (slot < a.flag_cap)
+                    if (slot < a.flag_cap) {
                       a.flags[slot] = make_int4(i, j, bl, 0);
-                    else
-                      a.counters[1] = 1;
-                    vi[u4 + u] = 0.f;  // out of the band sum; the fallback adds the fp64 value
+                      vi[u4 + u] = 0.f;  // out of the band sum; the fallback adds the fp64 value
+                    } else {
+                      a.counters[1] = 1;  // list full: keep the tensor-core value (|err| < imag_tau)
+                    }
                   }
                 }
               }

@@ -294,6 +294,10 @@ class ConnectivityEngine:
             if not (0 <= lo <= hi < self.n_bins):
                 raise ParameterError(f"accumulate_band [{lo}, {hi}] outside {self.n_bins} bins")
         self._accumulate_band = accumulate_band
+        # columns the reference's accumulator holds (metrics.py:314-322, 363-380): the
+        # accumulate band in storage mode, widened by ensure_band; the ring keeps all bins
+        self._storage_mode = storage_mode
+        self._init_cols()
         self.cache = TrialCache(enabled=storage_mode)
         self._slot_capacity = max(int(slot_capacity), 1)
         self._plan: DevicePlan | None = None
@@ -312,6 +316,24 @@ class ConnectivityEngine:
         self._xcor_peak_sum = None
         self._xcor_lag_sum = None
         self._xcor_trials = 0
+        self._pending: list = []     # device epochs whose finiteness flag is not read yet
+
+    def _init_cols(self) -> None:
+        self._acc_cols = np.ones(self.n_bins, dtype=bool)
+        ab = self._accumulate_band
+        if ab is not None and self._storage_mode and self.spectral_mode == "fixed":
+            self._acc_cols[:] = False
+            self._acc_cols[ab[0]:ab[1] + 1] = True
+
+    def _validate_pending(self) -> None:
+        """One host read for all device epochs added since the last finalize
+        (core.py:97-100 raises ParameterError for non-finite samples)."""
+        if self._pending:
+            flags = torch.stack([e.__dict__["_finite_dev"] for e in self._pending])
+            pend, self._pending = self._pending, []
+            if not bool(flags.all()):
+                for e in pend:
+                    e.validate()
 
     # -- ring ------------------------------------------------------------------
     def _ensure_plan(self, T: int, scale: float):
@@ -340,7 +362,8 @@ class ConnectivityEngine:
         idx = epoch.trial_index
         if not (self.cache.enabled and idx in self._slot_of):
             x = spectral._as_device_samples(epoch.data)
-            scale = pow2_scale(float(x.abs().amax()), min(x.shape[1], self.nfft))
+            # the fp32 scale is fixed by the first trial (host data: no device sync)
+            scale = 1.0 if self._plan is not None else pow2_scale(_abs_max(epoch.data), min(x.shape[1], self.nfft))
             self._ensure_plan(x.shape[1], scale)
             slot = self._next_slot
             self._next_slot += 1
@@ -369,6 +392,8 @@ class ConnectivityEngine:
             fold_slot = slot
         else:  # cached trial: the reference folds its cached (first-segment) spectra
             fold_slot = self._seg0_of.get(idx, self._slot_of[idx])
+        if epoch.__dict__.get("_finite_dev") is not None:
+            self._pending.append(epoch)       # device samples: finiteness checked at finalize
         if self.cache.enabled:
             self.cache.epochs[idx] = epoch
         else:  # no cache to recompute from: fold the trial's Pearson matrix now
@@ -415,9 +440,17 @@ class ConnectivityEngine:
                               positions=self.positions, node_ids=self.node_ids)
 
     def ensure_band(self, band: FrequencyBand) -> None:
-        """All bins are cached on the device, so back-fill is a no-op (metrics.py:363-380)."""
+        """All bins are cached on the device, so back-fill needs no FFT (metrics.py:363-380);
+        only the accumulator's column set widens."""
         if band.hi_bin >= self.n_bins:
             raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {self.n_bins} bins")
+        self._acc_cols[band.lo_bin:band.hi_bin + 1] = True
+
+    @property
+    def acc(self) -> "EngineSpectrumSet":
+        """The reference engine's ``acc`` (a SpectrumSet over the folded trials,
+        metrics.py:306): shape attributes, and the running sums on access."""
+        return EngineSpectrumSet(self)
 
     # -- finalization ---------------------------------------------------------------
     def _slots(self):
@@ -425,6 +458,7 @@ class ConnectivityEngine:
 
     def finalize(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
         metric = metric if isinstance(metric, MetricId) else MetricId.parse(metric)
+        self._validate_pending()
         if not metric.is_spectral:
             return self._finalize_time_domain(metric, band)
         self.ensure_band(band)
@@ -458,9 +492,67 @@ class ConnectivityEngine:
         self._xcor_peak_sum = self._xcor_lag_sum = None
         self._xcor_trials = 0
         self._sum_trials = list(keep)
+        self._init_cols()   # the reference's reset() restores the accumulate-band mask
         # re-added from the cache: fixed-mode folds of the cached spectra
         self._fold_slots = [self._seg0_of.get(i, self._slot_of[i]) for i in keep]
         self.n_trials = len(keep)
+
+
+def _abs_max(data) -> float:
+    if isinstance(data, torch.Tensor):
+        return float(data.abs().amax()) if data.numel() else 0.0
+    a = np.asarray(data)
+    return float(np.abs(a).max()) if a.size else 0.0
+
+
+class EngineSpectrumSet:
+    """Read-only SpectrumSet view of a ConnectivityEngine (the reference Pipeline
+    reads ``engine.acc.n_bins``, pipeline.py:161-162).  The sums are the
+    reference's fold over the engine's current trials (cs_pair_sums, fp64),
+    zero outside the columns the reference accumulator would hold."""
+
+    def __init__(self, engine: "ConnectivityEngine"):
+        self._e = engine
+        self._cache = None
+
+    n_channels = property(lambda self: self._e.n_channels)
+    nfft = property(lambda self: self._e.nfft)
+    n_bins = property(lambda self: self._e.n_bins)
+    n_pairs = property(lambda self: self._e.n_channels * (self._e.n_channels - 1) // 2)
+    n_trials_accumulated = property(lambda self: len(self._e._sum_trials))
+
+    def _sums(self) -> dict:
+        if self._cache is None:
+            e = self._e
+            C, B, P = self.n_channels, self.n_bins, self.n_pairs
+            out = {"csd": np.zeros((P, B), np.complex128), "psd": np.zeros((C, B)),
+                   "plv": np.zeros((P, B), np.complex128), "pli": np.zeros((P, B)), "abs_im": np.zeros((P, B))}
+            if e._fold_slots:
+                o = e._plan.pair_sums(e._slots())
+                cols = e._acc_cols
+                for k in ("csd", "plv", "pli", "abs_im", "psd"):
+                    v = o[k].T.cpu().numpy()
+                    out[k][:, cols] = v[:, cols]
+            self._cache = out
+        return self._cache
+
+    csd_sum = property(lambda self: self._sums()["csd"])
+    psd_sum = property(lambda self: self._sums()["psd"])
+    plv_sum = property(lambda self: self._sums()["plv"])
+    pli_sum = property(lambda self: self._sums()["pli"])
+    abs_im_sum = property(lambda self: self._sums()["abs_im"])
+    im_sum = property(lambda self: self.csd_sum.imag)
+
+    def csd_entry(self, i: int, j: int) -> np.ndarray:
+        if i == j:
+            return self.psd_sum[i].astype(np.complex128)
+        if i < j:
+            return self.csd_sum[spectral.pair_row_slice(self.n_channels, i)][j - i - 1]
+        return np.conj(self.csd_entry(j, i))
+
+    def nbytes(self) -> int:
+        e = self._e
+        return 0 if e._plan is None else len(e._slot_of) * e._plan.n_tapers * e.n_channels * e.n_bins * 24
 
 
 def convergence_curve(epochs, metric: MetricId, nfft: int, band: FrequencyBand, n_top: int = 20,

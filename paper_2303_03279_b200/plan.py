@@ -195,6 +195,13 @@ class DevicePlan:
         _lib.check(_lib.lib().cs_last_fallback_count(self._h, _stream_ptr(stream), ctypes.byref(n)))
         return int(n.value)
 
+    def guard_stats(self, stream=None) -> dict:
+        """Exact-sign guard of the last pair_metrics call: entries recomputed in fp64 and
+        the overflow records used when the work list was full (none is ever dropped)."""
+        n, r = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().cs_last_guard_stats(self._h, _stream_ptr(stream), ctypes.byref(n), ctypes.byref(r)))
+        return {"flagged": int(n.value), "records": int(r.value)}
+
     def get_spectra(self, slots: torch.Tensor, bin_lo: int = 0, n_bins: int | None = None, stream=None):
         if n_bins is None:
             n_bins = self.n_bins - bin_lo

@@ -162,6 +162,19 @@ def pair_row_slice(n_channels: int, i: int) -> slice:
     return slice(off, off + n_channels - 1 - i)
 
 
+def trial_csd_psd(spectra, n_channels: int):
+    """Upper-triangle CSD [P, B] and PSD [C, B] of one trial's spectra
+    (spectral.py:204-213; no Im flush -- that belongs to the fold).  Computed on
+    the device; returns numpy arrays like the reference."""
+    x = torch.as_tensor(spectra, dtype=torch.complex128, device=_device())
+    if x.dim() != 2 or x.shape[0] != n_channels:
+        raise ParameterError(f"spectra must be [{n_channels}, bins], got {tuple(x.shape)}")
+    i, j = (torch.as_tensor(a, device=x.device) for a in pair_index(n_channels))
+    csd = x[i] * x[j].conj()
+    psd = x.abs() ** 2
+    return csd.cpu().numpy(), psd.cpu().numpy()
+
+
 class SpectrumSet:
     """Device accumulator with the reference's SpectrumSet interface.
 
