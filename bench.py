@@ -582,9 +582,11 @@ def main():
         # pair kernels (row chunks, each downloaded while the next runs) -> pinned host band
         # means; consecutive steps are enqueued back to back, so step s+1's upload overlaps
         # step s's pair kernels and download.  Every step's copies are inside the timed region.
-        from paper_2303_03279_b200.plan import HostPipeline
+        from paper_2303_03279_b200.plan import HostPipeline, bind_host_to_gpu_numa, copy_ceilings
         del outs
         torch.cuda.empty_cache()
+        aff0 = os.sched_getaffinity(0)
+        numa = bind_host_to_gpu_numa(lr)   # pinned buffers below land on the GPU's NUMA node
         hp = HostPipeline(c.N, c.T, c.nfft, c.lo, c.hi, c.K, metrics=metrics, taper=c.taper, scale=scale,
                           device=dev, dtype=x.dtype)
         xh = x.cpu().pin_memory()
@@ -598,13 +600,22 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         t_ms = e0.elapsed_time(e1) / args.e2e_steps
+        d2h = sum(v.numel() * v.element_size() for v in hb.values())
+        del xh, hb
+        ceil = copy_ceilings(hp.h2d_bytes, d2h, dev)
+        copy_ms = max(hp.h2d_bytes / (ceil["h2d_gbs"] * 1e9), d2h / (ceil["d2h_gbs"] * 1e9), ceil["bidir_ms"] * 1e-3) * 1e3
         line["e2e"] = {"value": c.updates / (t_ms * 1e-3), "unit": "updates/s",
                        "h2d_bytes_per_step": hp.h2d_bytes,
-                       "d2h_bytes_per_step": sum(v.numel() * v.element_size() for v in hb.values()),
+                       "d2h_bytes_per_step": d2h,
                        "ms_per_step": t_ms, "steps": args.e2e_steps,
+                       "h2d_ceiling_gbs": ceil["h2d_gbs"], "d2h_ceiling_gbs": ceil["d2h_gbs"],
+                       "bidir_copy_ms": ceil["bidir_ms"],
+                       "copy_bound_ms": copy_ms, "frac_of_copy_bound": copy_ms / t_ms,
+                       "numa": None if numa is None else {"node": numa[0], "cpus": numa[1]},
                        "path": "HostPipeline.submit: pinned host samples -> H2D in trial chunks (overlapping K1) -> "
                                "pair kernels over row-tile chunks -> band means D2H per chunk; steps enqueued "
                                "back to back (step s+1 upload overlaps step s kernels + download)"}
+        os.sched_setaffinity(0, aff0)   # the CPU baseline below uses every host core again
     elif not args.no_e2e:
         # N > 1: every rank uploads its node block, runs K1, joins the all-gather, runs its
         # pair rows and downloads its band means; uploads and downloads run on copy streams

@@ -129,6 +129,16 @@ int cs_pair_metrics(cs_plan* plan, const int* slots_dev, int n_slots, unsigned m
                     int bin_lo, int n_bins, int row_tile_begin, int row_tile_end,
                     const cs_outputs* out, void* stream);
 
+/* cs_pair_metrics with flags.  CS_PM_REUSE_PREP: the node statistics and packed
+ * operands of the previous call on this plan (same slots pointer, trial count,
+ * bins and metric mask -- checked) are reused, so a caller that splits one
+ * step into row-tile chunks (e.g. to overlap each chunk's download) pays the
+ * per-call preparation once; the slots' contents must not have changed. */
+#define CS_PM_REUSE_PREP 1u
+int cs_pair_metrics_ex(cs_plan* plan, const int* slots_dev, int n_slots, unsigned metric_mask,
+                       int bin_lo, int n_bins, int row_tile_begin, int row_tile_end,
+                       const cs_outputs* out, unsigned flags, void* stream);
+
 /* SpectrumSet-compatible running sums over the same trial / bin selection, from
  * the fp64 ring with the reference's arithmetic (spectral.py:204-241: per-trial
  * CSD = sum over tapers / welch segments, Im flush at 1e-13 |Re|, unit phasor

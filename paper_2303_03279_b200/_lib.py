@@ -48,6 +48,7 @@ def lib():
     L.cs_plan_destroy.argtypes = [vp]
     L.cs_spectra.argtypes = [vp, vp, i32, i64, i64, i32, i32, vp]
     L.cs_pair_metrics.argtypes = [vp, vp, i32, u32, i32, i32, i32, i32, ctypes.POINTER(CsOutputs), vp]
+    L.cs_pair_metrics_ex.argtypes = [vp, vp, i32, u32, i32, i32, i32, i32, ctypes.POINTER(CsOutputs), u32, vp]
     L.cs_get_spectra.argtypes = [vp, vp, i32, i32, i32, vp, vp]
     L.cs_put_spectra.argtypes = [vp, vp, i32, i32, i32, i32, vp]
     L.cs_net_normalize.argtypes = [vp, vp, i64, vp]
@@ -79,8 +80,9 @@ def lib():
 
 
 CS_PLAN_WELCH = 1
+CS_PM_REUSE_PREP = 1
 
-EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_sums",
+EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_metrics_ex", "cs_pair_sums",
             "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count", "cs_last_guard_stats",
             "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
             "cs_launch_count", "cs_ring_view", "cs_probe_peaks", "cs_last_error", "cs_version")

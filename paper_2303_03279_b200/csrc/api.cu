@@ -382,7 +382,13 @@ int cs_spectra(cs_plan* p, const void* x, int dtype, int64_t ts, int64_t ns, int
 
 int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, void* stream) {
+  return cs_pair_metrics_ex(p, slots, K, mask, bin_lo, nbb, rb, re, out, 0u, stream);
+}
+
+int cs_pair_metrics_ex(cs_plan* p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
+                       int rb, int re, const cs_outputs* out, unsigned flags, void* stream) {
   if (!p || !out) { cs_set_error("cs_pair_metrics: null argument"); return CS_EPARAM; }
+  if (flags & ~CS_PM_REUSE_PREP) { cs_set_error("unknown pair-metrics flags 0x%x", flags); return CS_EPARAM; }
   if (mask == 0 || (mask >> CS_NUM_METRICS)) { cs_set_error("bad metric mask 0x%x", mask); return CS_EPARAM; }
   if (K < 1) { cs_set_error("no trials accumulated"); return CS_EDEGENERATE; }
   if ((mask & CS_USPLI) && K < 2) { cs_set_error("USPLI needs at least 2 trials"); return CS_EDEGENERATE; }
@@ -396,7 +402,16 @@ int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_
   if (p->N < 2 || rb == re) return CS_OK;
   DeviceGuard g(p->device);
   cudaStream_t st = (cudaStream_t)stream;
-  {
+  Plan::PrepKey key;
+  key.slots = slots; key.K = K; key.bin_lo = bin_lo; key.nbb = nbb; key.mask = mask;
+  const bool reuse = (flags & CS_PM_REUSE_PREP) != 0;
+  if (reuse && !(p->prep_valid && p->prep_key == key)) {
+    cs_set_error("CS_PM_REUSE_PREP: the previous call prepared other slots, bins or metrics");
+    return CS_EPARAM;
+  }
+  p->reuse_prep = reuse;
+  p->prep_valid = false;
+  if (!reuse) {
     cs::PhaseMark ph(*p, "node_stats", st);
     cs::run_node_stats(*p, slots, K, bin_lo, nbb, st);
   }
@@ -406,9 +421,13 @@ int cs_pair_metrics(cs_plan* p, const int* slots, int K, unsigned mask, int bin_
     if (!(mask & (1u << m))) o.bins[m] = o.band[m] = nullptr;
   // tensor-core family (COHY, COH, PLV; IMAGCOHY when no sign-based metric is asked),
   // then the phase-lag family
-  if (cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st) < 0) return CS_EPARAM;
-  if (cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st) < 0) return CS_EPARAM;
+  const int rc1 = cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
+  const int rc2 = rc1 < 0 ? -1 : cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
+  p->reuse_prep = false;
+  if (rc1 < 0 || rc2 < 0) return CS_EPARAM;
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_metrics");
+  p->prep_key = key;
+  p->prep_valid = true;
   return CS_OK;
 }
 

@@ -70,6 +70,19 @@ struct Plan {
   int4* recs = nullptr;          // guard overflow records (3 int4 each), grown on demand
   size_t rec_cap = 0;            // records
   int flag_cap = 0;
+  // node statistics + operand packing of the last cs_pair_metrics call, reusable by a
+  // following call over another row range (CS_PM_REUSE_PREP)
+  struct PrepKey {
+    const int* slots = nullptr;
+    int K = 0, bin_lo = 0, nbb = 0;
+    unsigned mask = 0;
+    bool operator==(const PrepKey& o) const {
+      return slots == o.slots && K == o.K && bin_lo == o.bin_lo && nbb == o.nbb && mask == o.mask;
+    }
+  };
+  PrepKey prep_key;
+  bool prep_valid = false;
+  bool reuse_prep = false;       // set for the duration of one call
   int64_t fft_calls = 0;
   int64_t launches = 0;          // kernels launched by this plan (bench evidence)
   bool profiling = false;        // record CUDA events around every kernel phase

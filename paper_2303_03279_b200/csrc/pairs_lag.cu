@@ -198,7 +198,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
   cudaMemsetAsync(a.counters, 0, 3 * sizeof(int), st);
-  {
+  if (!p.reuse_prep) {
     PhaseMark ph(p, "lag_prep", st);
     dim3 grid((a.N64 + 127) / 128, a.Kp * a.L < 65535 ? a.Kp * a.L : 65535, a.nbb);
     k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag,

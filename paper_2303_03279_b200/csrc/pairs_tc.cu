@@ -677,7 +677,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     p.tc_bytes = need;
   }
   __half* G = (__half*)p.tc_ops;
-  {
+  if (!p.reuse_prep) {
     PhaseMark ph(p, "tc_prep", st);
     dim3 grid((K_pad + 31) / 32, (p.N + 7) / 8, nbb);
     k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, Kc, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);

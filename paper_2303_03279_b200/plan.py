@@ -142,7 +142,9 @@ class DevicePlan:
 
     def pair_metrics(self, slots: torch.Tensor, metrics=SEVEN, bin_lo: int = 0, n_bins: int | None = None,
                      outputs=None, per_bin=True, band=True, row_tiles=(0, -1), pair_base: int = 0,
-                     pair_count: int | None = None, stream=None):
+                     pair_count: int | None = None, stream=None, reuse_prep: bool = False):
+        """reuse_prep: keep the node statistics and packed operands of the previous call
+        (same slots tensor, bins and metrics; cs_pair_metrics_ex CS_PM_REUSE_PREP)."""
         if n_bins is None:
             n_bins = self.n_bins - bin_lo
         metrics = tuple(m.upper() for m in metrics)
@@ -164,9 +166,10 @@ class DevicePlan:
         desc.pair_base = int(pair_base)
         desc.pair_stride = int(self.n_pairs if pair_count is None else pair_count)
         self._last_slots = slots
-        _lib.check(_lib.lib().cs_pair_metrics(self._h, ctypes.c_void_p(slots.data_ptr()), int(slots.numel()),
-                                              mask, int(bin_lo), int(n_bins), int(row_tiles[0]),
-                                              int(row_tiles[1]), ctypes.byref(desc), _stream_ptr(stream)))
+        _lib.check(_lib.lib().cs_pair_metrics_ex(self._h, ctypes.c_void_p(slots.data_ptr()), int(slots.numel()),
+                                                 mask, int(bin_lo), int(n_bins), int(row_tiles[0]),
+                                                 int(row_tiles[1]), ctypes.byref(desc),
+                                                 _lib.CS_PM_REUSE_PREP if reuse_prep else 0, _stream_ptr(stream)))
         return outputs
 
     def pair_sums(self, slots: torch.Tensor, bin_lo: int = 0, n_bins: int | None = None, stream=None) -> dict:
@@ -285,6 +288,83 @@ def probe_peaks(device_index: int = 0):
     return a.value, b.value
 
 
+def bind_host_to_gpu_numa(device_index: int = 0):
+    """Pin this process to the CPU cores local to the GPU's PCIe root (sysfs
+    local_cpulist), so pinned host buffers allocated afterwards land on the GPU's
+    NUMA node and host<->device copies do not cross the inter-socket link.
+    Returns (numa_node, n_cpus) or None when the topology is not visible."""
+    import os
+    try:
+        pr = torch.cuda.get_device_properties(device_index)
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        base = f"/sys/bus/pci/devices/{bdf}"
+        with open(f"{base}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            if "-" in part:
+                a, b = part.split("-")
+                cpus.update(range(int(a), int(b) + 1))
+            elif part:
+                cpus.add(int(part))
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        try:
+            with open(f"{base}/numa_node") as f:
+                node = int(f.read().strip())
+        except OSError:
+            node = -1
+        return node, len(cpus)
+    except (OSError, AttributeError, ValueError):
+        return None
+
+
+def copy_ceilings(nbytes_h2d: int, nbytes_d2h: int, device=None, reps: int = 3) -> dict:
+    """Measured pinned-host <-> device copy rates (GB/s, best of ``reps``) for buffers of
+    the given sizes on this box: the ceiling an end-to-end step that moves those
+    bytes cannot beat."""
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    out = {}
+    for name, nb, h2d in (("h2d_gbs", nbytes_h2d, True), ("d2h_gbs", nbytes_d2h, False)):
+        n = max(1, int(nb) // 4)
+        h = torch.empty(n, dtype=torch.float32).pin_memory()
+        d = torch.empty(n, dtype=torch.float32, device=dev)
+        best = 0.0
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            (d.copy_(h, non_blocking=True) if h2d else h.copy_(d, non_blocking=True))
+            e1.record()
+            e1.synchronize()
+            best = max(best, n * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = best
+        del h, d
+    # both directions at once (a pipelined step uploads and downloads concurrently)
+    nh, nd = max(1, int(nbytes_h2d) // 4), max(1, int(nbytes_d2h) // 4)
+    hh, dh = torch.empty(nh, dtype=torch.float32).pin_memory(), torch.empty(nh, dtype=torch.float32, device=dev)
+    hd, dd = torch.empty(nd, dtype=torch.float32).pin_memory(), torch.empty(nd, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize(dev)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        s1.wait_event(e0)
+        s2.wait_event(e0)
+        with torch.cuda.stream(s1):
+            dh.copy_(hh, non_blocking=True)
+            e1.record(s1)
+        with torch.cuda.stream(s2):
+            hd.copy_(dd, non_blocking=True)
+            e2.record(s2)
+        torch.cuda.synchronize(dev)
+        best = min(best, max(e0.elapsed_time(e1), e0.elapsed_time(e2)))
+    out["bidir_ms"] = best
+    return out
+
+
 def row_tile_range(n_nodes: int, n_shards: int, shard: int):
     L = _lib.lib()
     rb, re = ctypes.c_int(), ctypes.c_int()
@@ -379,10 +459,12 @@ class HostPipeline:
         self.ev_k1.record(self.s_comp)
         if self._armed:
             self.s_comp.wait_event(self.ev_out)   # the previous call's download has read the outputs
-        for ((rb, re), (p0, p1)), ev in zip(self.r_chunks, self.ev_rows):
+        for q, (((rb, re), (p0, p1)), ev) in enumerate(zip(self.r_chunks, self.ev_rows)):
             view = {m: {"bins": None, "band": t[p0:p1]} for m, t in self.out.items()}
+            # node statistics and operand packing once per step, not once per row chunk
             p.pair_metrics(self.slots, self.metrics, 0, p.n_bins, outputs=view, per_bin=False, band=True,
-                           row_tiles=(rb, re), pair_base=p0, pair_count=p1 - p0, stream=self.s_comp)
+                           row_tiles=(rb, re), pair_base=p0, pair_count=p1 - p0, stream=self.s_comp,
+                           reuse_prep=q > 0)
             ev.record(self.s_comp)
         for ((rb, re), (p0, p1)), ev in zip(self.r_chunks, self.ev_rows):
             self.s_out.wait_event(ev)
