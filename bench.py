@@ -10,10 +10,11 @@ band-averaged outputs) for the configured workload.  Default workload: config 5
 (N=10242, K=100, T=1000, Hann, 6 bins), the config BASELINE.json scales over
 1/2/4/8 GPUs.  Inputs (4.1 GB) exceed the 126 MB L2, so no explicit flush.
 
-N > 1 (torchrun): rank r owns node block r for K1, the fp32/fp64 spectrum ring
-is all-gathered over NCCL (the path's one exchange step), then rank r computes
-the pair row-tiles of its balanced shard (strong scaling; results stay
-sharded).  Timing: CUDA events on the launching stream, barrier + synchronize
+N > 1 (torchrun): rank r owns node block r for K1 and pushes that block of its
+fp32 spectrum ring into every peer's ring over NVLink peer memory (CUDA IPC +
+copy engines; the path's one exchange step), then computes the pair row-tiles
+of its balanced shard (strong scaling; results stay sharded; the fp64 fallback
+reads remote nodes' fp64 spectra from their owner by P2P loads).  Timing: CUDA events on the launching stream, barrier + synchronize
 on both sides, max over ranks.
 
 --impl reference times the reference's CPU path (the oracle port of
@@ -355,33 +356,39 @@ def main():
     metrics = tuple(args.metrics.split(",")) if args.metrics else c.metrics
 
     # ---- node block for K1, pair shard for the pair kernels ----
-    from paper_2303_03279_b200.shard import allgather_ring, node_block, shard_plan
+    from paper_2303_03279_b200.shard import RingExchange, node_block, shard_plan
     n0, n1, nloc = node_block(c.N, ws, rank)
     (rb, re), (p0, p1) = shard_plan(c.N, ws, rank)
     x = synth.generate(c, dev, nodes=slice(n0, n1))
-    if x.shape[1] < nloc:  # pad the last block so every rank gathers the same size
-        x = torch.cat([x, torch.zeros((c.K, nloc - x.shape[1], c.T), dtype=x.dtype, device=dev)], 1)
     amax = x.abs().amax()
     if dist is not None:
         dist.all_reduce(amax, op=dist.ReduceOp.MAX)
     scale = pow2_scale(float(amax), min(c.T, c.nfft))
-    full = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=c.K, device=dev, scale=scale)
-    local = full if ws == 1 else DevicePlan(nloc, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=c.K,
-                                            device=dev, scale=scale)
-    slots = torch.arange(c.K, dtype=torch.int32, device=dev)
+    # N > 1: the ring holds two steps (slots [0, K) and [K, 2K) alternate), so a step's K1
+    # and push never overwrite slots a peer's fallback of the previous step may still read
+    full = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=c.K * (2 if ws > 1 else 1),
+                      device=dev, scale=scale)
+    ex = RingExchange(full, dist) if ws > 1 else None
+    slot_sets = [torch.arange(h * c.K, (h + 1) * c.K, dtype=torch.int32, device=dev) for h in range(2 if ws > 1 else 1)]
     outs = full.alloc_outputs(metrics, c.n_bins, per_bin=True, band=True, pair_count=p1 - p0)
-    if ws > 1:
-        L64, L32 = local.ring()
-        F64, F32 = full.ring()
-        g64 = torch.empty((ws,) + tuple(L64.shape), dtype=L64.dtype, device=dev)
-        g32 = torch.empty((ws,) + tuple(L32.shape), dtype=L32.dtype, device=dev)
+    n_step = [0]
+
+    def exchange(h):
+        """K1 on this rank's node block, then the ring exchange (the path's one exchange step):
+        push the block into every peer's ring, wait for this rank's pushes, host barrier."""
+        if ex is None:
+            full.spectra(x, 0)
+            return
+        ex.spectra(x, h * c.K)
+        ex.push(h * c.K, c.K)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier()
 
     def step():
-        local.spectra(x, 0)
-        if ws > 1:  # the exchange step: all-gather node-block spectra over NVLink
-            allgather_ring(L32, F32, dist, g32)
-            allgather_ring(L64, F64, dist, g64)
-        full.pair_metrics(slots, metrics, 0, c.n_bins, outputs=outs, row_tiles=(rb, re), pair_base=p0,
+        h = n_step[0] % len(slot_sets)
+        n_step[0] += 1
+        exchange(h)
+        full.pair_metrics(slot_sets[h], metrics, 0, c.n_bins, outputs=outs, row_tiles=(rb, re), pair_base=p0,
                           pair_count=p1 - p0)
 
     def barrier():
@@ -394,10 +401,8 @@ def main():
     barrier()
     n_fallback = full.fallback_count()
     full.set_profiling(True)
-    if local is not full:
-        local.set_profiling(True)
     full.profile()
-    launches0 = full.launch_count() + (local.launch_count() if local is not full else 0)
+    launches0 = full.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(lr) as clk:
         barrier()
@@ -408,9 +413,7 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1)
     prof = full.profile()
-    if local is not full:
-        prof.update({("local_" + k): v for k, v in local.profile().items()})
-    launches = full.launch_count() + (local.launch_count() if local is not full else 0) - launches0
+    launches = full.launch_count() - launches0
     ms_t = torch.tensor([ms], device=dev)
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -424,7 +427,7 @@ def main():
     per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}  # ms per launch
     dom = max(per, key=per.get)
     lag_ms = per.get("pairs_lag", 0.0)
-    spec_key = "local_spectra" if "local_spectra" in per else "spectra"
+    spec_key = "spectra"
     roof = roof_k3 = roof_k1 = None
     if lag_ms > 0:
         # algorithmic FP32-pipe work per update (trial): t = sum over L tapers of FMUL+FFMA (2L),
@@ -444,7 +447,7 @@ def main():
     if per.get(spec_key, 0.0) > 0:
         k1_ms = per[spec_key]
         L_ = 1 if not isinstance(c.taper, tuple) else c.taper[2]
-        kind = local.k1_kind
+        kind = full.k1_kind
         if kind.startswith("fft"):   # 5 M log2 M + 16 M fp64 flops per signal-taper, M = nfft / 2 (2 flops per DFMA)
             M_ = c.nfft // 2
             fma = c.K * nloc * L_ * (5 * M_ * math.log2(M_) + 16 * M_) / 2
@@ -529,19 +532,16 @@ def main():
     per_metric = None
     if not args.no_per_metric and len(metrics) > 1:
         full.set_profiling(False)
-        if local is not full:
-            local.set_profiling(False)
         per_metric = {}
         n_pm = max(3, min(args.steps, 10))
         for m in metrics:
             om = full.alloc_outputs((m,), c.n_bins, per_bin=True, band=True, pair_count=p1 - p0)
 
             def step_m():
-                local.spectra(x, 0)
-                if ws > 1:
-                    allgather_ring(L32, F32, dist, g32)
-                    allgather_ring(L64, F64, dist, g64)
-                full.pair_metrics(slots, (m,), 0, c.n_bins, outputs=om, row_tiles=(rb, re), pair_base=p0,
+                h = n_step[0] % len(slot_sets)
+                n_step[0] += 1
+                exchange(h)
+                full.pair_metrics(slot_sets[h], (m,), 0, c.n_bins, outputs=om, row_tiles=(rb, re), pair_base=p0,
                                   pair_count=p1 - p0)
             for _ in range(2):
                 step_m()
@@ -617,9 +617,9 @@ def main():
                                "back to back (step s+1 upload overlaps step s kernels + download)"}
         os.sched_setaffinity(0, aff0)   # the CPU baseline below uses every host core again
     elif not args.no_e2e:
-        # N > 1: every rank uploads its node block, runs K1, joins the all-gather, runs its
-        # pair rows and downloads its band means; uploads and downloads run on copy streams
-        # so step s+1's upload overlaps step s's kernels and download (event-ordered)
+        # N > 1: every rank uploads its node block, runs K1, pushes it into the peers' rings,
+        # runs its pair rows and downloads its band means; uploads and downloads run on copy
+        # streams so step s+1's upload overlaps step s's kernels and download (event-ordered)
         xh = x.cpu().pin_memory()
         hb = {m: torch.empty(p1 - p0, dtype=torch.float32).pin_memory() for m in metrics}
         xd = torch.empty_like(x)
@@ -630,18 +630,21 @@ def main():
             ev.record(cur)
 
         def e2e_step():
+            h = n_step[0] % len(slot_sets)
+            n_step[0] += 1
             s_in.wait_event(ev_k1)                 # the previous K1 has consumed xd
             with torch.cuda.stream(s_in):
                 xd.copy_(xh, non_blocking=True)
                 ev_in.record(s_in)
             cur.wait_event(ev_in)
-            local.spectra(xd, 0)
+            ex.spectra(xd, h * c.K)
             ev_k1.record(cur)
-            allgather_ring(L32, F32, dist, g32)
-            allgather_ring(L64, F64, dist, g64)
+            ex.push(h * c.K, c.K)
+            cur.synchronize()
+            dist.barrier()
             cur.wait_event(ev_out)                 # the previous download has read the outputs
-            o = full.pair_metrics(slots, metrics, 0, c.n_bins, per_bin=False, band=True, row_tiles=(rb, re),
-                                  pair_base=p0, pair_count=p1 - p0)
+            o = full.pair_metrics(slot_sets[h], metrics, 0, c.n_bins, per_bin=False, band=True,
+                                  row_tiles=(rb, re), pair_base=p0, pair_count=p1 - p0)
             ev_pm.record(cur)
             s_out.wait_event(ev_pm)
             with torch.cuda.stream(s_out):
@@ -651,7 +654,6 @@ def main():
         e2e_step()
         barrier()
         full.set_profiling(False)
-        local.set_profiling(False)
         barrier()
         e0.record()
         for _ in range(args.e2e_steps):
@@ -665,8 +667,8 @@ def main():
                        "h2d_bytes_per_step": xh.numel() * xh.element_size() * ws,
                        "d2h_bytes_per_step": sum(v.numel() * 4 for v in hb.values()) * ws,
                        "ms_per_step": float(t), "steps": args.e2e_steps,
-                       "path": "per rank: pinned host node block -> H2D (copy stream) -> K1 -> all-gather -> pair "
-                               "rows -> band means D2H (copy stream); steps back to back"}
+                       "path": "per rank: pinned host node block -> H2D (copy stream) -> K1 -> ring push to the "
+                               "peers + barrier -> pair rows -> band means D2H (copy stream); steps back to back"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -223,6 +223,33 @@ int64_t cs_launch_count(const cs_plan* plan);
  * complex) and its element count: used to all-gather node blocks across GPUs. */
 int cs_ring_view(cs_plan* plan, void** x64, void** x32, int64_t* n_elems);
 
+/* ---- multi-GPU: the spectrum ring exchanged over NVLink peer memory (shard.cu) ----
+ * Every rank holds a plan over all N nodes; rank r computes K1 for its node block
+ * [r*node_block, (r+1)*node_block) with cs_spectra_nodes, then cs_ring_push copies
+ * that block of its fp32 ring into every attached peer's ring (strided copy-engine
+ * copies, no staging).  The fp64 ring is not exchanged: the exact-sign fallback
+ * reads a node's fp64 spectra from the rank owning it (P2P loads).  After the push
+ * the caller synchronises the ranks (all pushes into this rank's ring complete)
+ * before cs_pair_metrics over its row tiles (cs_row_tile_range).  The reference
+ * has no multi-process path; this replaces the NCCL all-gather proposed in
+ * SURVEY.md 8(b) (in place, no layout constraint on the ring). */
+typedef struct cs_ring_handle {
+  unsigned char x64[64];  /* cudaIpcMemHandle_t of the fp64 ring */
+  unsigned char x32[64];  /* cudaIpcMemHandle_t of the fp32 ring */
+  int32_t n_nodes, slot_capacity, n_tapers, n_bins;  /* geometry, checked on attach */
+} cs_ring_handle;
+/* K1 for the node range [node0, node0 + n_nodes) only; x_dev holds those nodes. */
+int cs_spectra_nodes(cs_plan* plan, const void* x_dev, int dtype, int64_t trial_stride, int64_t node_stride,
+                     int node0, int n_nodes, int slot0, int k_count, void* stream);
+int cs_ring_export(cs_plan* plan, cs_ring_handle* out);
+/* handles[r] of every rank (own included, not opened); node n is owned by rank n / node_block */
+int cs_ring_attach(cs_plan* plan, const cs_ring_handle* handles, int n_ranks, int self, int node_block);
+/* the same with device pointers of rings in this process (tests, one process driving several plans) */
+int cs_ring_attach_ptrs(cs_plan* plan, void* const* x64, void* const* x32, int n_ranks, int self, int node_block);
+/* push nodes [node0, node0 + n_nodes) of slots slot0 .. slot0 + k_count - 1 (mod capacity) of the
+ * fp32 ring into every attached peer's ring, on stream */
+int cs_ring_push(cs_plan* plan, int node0, int n_nodes, int slot0, int k_count, void* stream);
+
 /* Measure this device's FP32 FMA-pipe lane-op rate and FP64 DFMA rate (a few
  * ms of dependent-chain FMA loops; the roofline denominators for K3 and K1). */
 int cs_probe_peaks(int device, double* fp32_lane_ops_per_s, double* fp64_fma_per_s);

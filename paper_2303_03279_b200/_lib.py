@@ -31,6 +31,11 @@ class CsSums(ctypes.Structure):
                 ("pair_base", ctypes.c_int64), ("pair_stride", ctypes.c_int64)]
 
 
+class CsRingHandle(ctypes.Structure):
+    _fields_ = [("x64", ctypes.c_ubyte * 64), ("x32", ctypes.c_ubyte * 64), ("n_nodes", ctypes.c_int32),
+                ("slot_capacity", ctypes.c_int32), ("n_tapers", ctypes.c_int32), ("n_bins", ctypes.c_int32)]
+
+
 _lib = None
 
 
@@ -72,6 +77,11 @@ def lib():
     L.cs_launch_count.argtypes = [vp]
     L.cs_launch_count.restype = i64
     L.cs_ring_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.cs_spectra_nodes.argtypes = [vp, vp, i32, i64, i64, i32, i32, i32, i32, vp]
+    L.cs_ring_export.argtypes = [vp, ctypes.POINTER(CsRingHandle)]
+    L.cs_ring_attach.argtypes = [vp, ctypes.POINTER(CsRingHandle), i32, i32, i32]
+    L.cs_ring_attach_ptrs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i32, i32]
+    L.cs_ring_push.argtypes = [vp, i32, i32, i32, i32, vp]
     L.cs_probe_peaks.argtypes = [i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
     L.cs_last_error.restype = ctypes.c_char_p
     L.cs_version.restype = ctypes.c_char_p
@@ -85,7 +95,8 @@ CS_PM_REUSE_PREP = 1
 EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_metrics_ex", "cs_pair_sums",
             "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_accumulate", "cs_xcor_peaks", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count", "cs_last_guard_stats",
             "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
-            "cs_launch_count", "cs_ring_view", "cs_probe_peaks", "cs_last_error", "cs_version")
+            "cs_launch_count", "cs_ring_view", "cs_spectra_nodes", "cs_ring_export", "cs_ring_attach",
+            "cs_ring_attach_ptrs", "cs_ring_push", "cs_probe_peaks", "cs_last_error", "cs_version")
 
 
 def check(status: int) -> None:

@@ -195,7 +195,7 @@ int cs_plan_create(cs_plan** out, int device, int N, int T, int nfft, int lo, in
   DeviceGuard g(device);
   cs_plan* p = new cs_plan();
   p->device = device;
-  p->N = N; p->T = T; p->nfft = nfft; p->lo = lo; p->hi = hi; p->nb = hi - lo + 1; p->L = L;
+  p->N = N; p->ldn = N; p->T = T; p->nfft = nfft; p->lo = lo; p->hi = hi; p->nb = hi - lo + 1; p->L = L;
   p->T_eff = T < nfft ? T : nfft;
   p->seg_stride = seg_stride;
   p->slot_cap = slot_cap;
@@ -348,6 +348,8 @@ int cs_plan_destroy(cs_plan* p) {
     if (e.ptr) cudaFree(e.ptr);
   if (p->lag_ops) cudaFree(p->lag_ops);
   cudaFree(p->flags); cudaFree(p->counters);
+  if (p->peer_x64) cudaFree(p->peer_x64);
+  for (void* m : p->ipc_opened) cudaIpcCloseMemHandle(m);
   if (p->recs) cudaFree(p->recs);
   if (p->prof) {
     auto* ps = (ProfState*)p->prof;

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <vector>
 
 #include "../../include/csconn.h"
 
@@ -48,6 +49,7 @@ struct Plan {
   bool use_fft = false;          // power-of-two nfft and a band wide enough to prefer the FFT
   int seg_stride = 0;            // welch: sample offset between segments (= nfft), else 0
   double* dft_tf = nullptr;      // [L][ceil(T_eff/4)][NT][32] fp64 DFT B fragments (tensor-core DFT), or null
+  int ldn = 0;                   // ring row stride in nodes (N; a node-range view of K1 keeps the full plan's)
   double2* X64 = nullptr;        // [slot][L][nb][N]  fp64 spectra (fp64 guard / fallback)
   float2* X32 = nullptr;         // [slot][L][nb][N]  fp32 scaled spectra
   float* psd = nullptr;          // [nb][N] per-call node statistics
@@ -83,6 +85,11 @@ struct Plan {
   PrepKey prep_key;
   bool prep_valid = false;
   bool reuse_prep = false;       // set for the duration of one call
+  // multi-GPU (shard.cu): peers' rings attached by cs_ring_attach[_ptrs]
+  int n_ranks = 0, rank = 0, node_block = 0;  // node n's fp64 spectra live on rank n / node_block
+  double2** peer_x64 = nullptr;  // device [n_ranks] fp64 ring of every rank (own included)
+  std::vector<float2*> peers32;  // fp32 rings of the peers (push targets; own = null)
+  std::vector<void*> ipc_opened; // IPC mappings to close on destroy
   int64_t fft_calls = 0;
   int64_t launches = 0;          // kernels launched by this plan (bench evidence)
   bool profiling = false;        // record CUDA events around every kernel phase

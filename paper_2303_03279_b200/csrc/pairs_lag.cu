@@ -52,6 +52,8 @@ struct LagArgs {
   int4* recs;        // guard overflow records (pairs_lag1.cu guard_push), or null
   int* counters;
   int flag_cap;
+  double2* const* x64_of;  // sharded plan: fp64 ring of the rank owning node n / node_block (else null)
+  int node_block;
 };
 
 // Trial-pair packing of the selected trials (k = 2 kp, 2 kp + 1) into the layouts the
@@ -96,13 +98,17 @@ __device__ __forceinline__ void fallback_entry(const LagArgs& a, int i, int j, i
   const int b = a.bin_lo + bl;
   double s_im = 0.0, s_abs = 0.0;
   int s_sign = 0;
+  // a sharded plan reads each node's fp64 spectra from the rank that computed them
+  // (P2P loads over NVLink); otherwise from this plan's ring
+  const double2* Xi = a.x64_of ? a.x64_of[i / a.node_block] : a.X64;
+  const double2* Xj = a.x64_of ? a.x64_of[j / a.node_block] : a.X64;
 #pragma unroll 4
   for (int k = lane; k < (live ? a.K : 0); k += 8) {  // unrolled: the trials' loads are independent
     const int slot = a.slots[k];
     double re = 0.0, im = 0.0;
     for (int l = 0; l < a.L; ++l) {
-      const double2 xi = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + i];
-      const double2 xj = a.X64[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + j];
+      const double2 xi = Xi[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + i];
+      const double2 xj = Xj[slot * slot_stride + ((int64_t)l * a.nb + b) * a.N + j];
       // (xi.x + i xi.y) * (xj.x - i xj.y)
       re += xi.x * xj.x + xi.y * xj.y;
       im += xi.y * xj.x - xi.x * xj.y;
@@ -314,6 +320,8 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.plv_bins = plvk ? (float*)out->bins[3] : nullptr;
   a.plv_band = plvk ? (float*)out->band[3] : nullptr;
   a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
+  a.x64_of = p.n_ranks > 1 ? p.peer_x64 : nullptr;
+  a.node_block = p.node_block;
   if (const char* gs = getenv("CSCONN_GUARD_G")) a.g *= (float)atof(gs);  // test override (negative control)
   a.scale2 = p.scale * p.scale;
   a.flags = p.flags;
@@ -364,6 +372,8 @@ int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     a.flags = p.flags;
     a.counters = p.counters;
     a.flag_cap = p.flag_cap;
+    a.x64_of = p.n_ranks > 1 ? p.peer_x64 : nullptr;
+    a.node_block = p.node_block;
     PhaseMark ph(p, "lag_fallback", st);
     k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
   }

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kSpecNodes)
 k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N,
           int T_eff, int nb, int L, const double2* __restrict__ tww, const double2* __restrict__ wsum,
           int slot0, int slot_cap, double2* __restrict__ X64, float2* __restrict__ X32, float scale,
-          int dc_local, int nyq_local, int vec16, int seg_stride) {
+          int dc_local, int nyq_local, int vec16, int seg_stride, int ldn) {
   using Sh = SpecShape<Tin, NBT, NS>;
   constexpr int ROWS = Sh::ROWS, TC = Sh::TC, RS = Sh::RS;
   extern __shared__ __align__(16) unsigned char spec_smem[];
@@ -199,7 +199,7 @@ k_spectra(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, 
       double re = fma(-mean, W.x, are[q][j]), im = fma(-mean, W.y, aim[q][j]);
       if (b == dc_local) re = im = 0.0;       // spectral.py:96: DC is exactly zero
       if (b == nyq_local) im = 0.0;           // Nyquist of a real signal is real
-      const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
+      const int64_t o = (((int64_t)slot * L + l) * nb + b) * ldn + n;  // ring rows of ldn nodes
       X64[o] = make_double2(re, im);
       X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
     }
@@ -219,7 +219,7 @@ static void launch_spectra(const Plan& p, const void* x, int64_t ts, int64_t ns,
   k_spectra<Tin, NBT, NS><<<grid, kSpecNodes, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb,
                                                            p.L, p.tww, p.wsum, slot0, p.slot_cap, p.X64,
                                                            p.X32, p.scale, p.dc_local, p.nyq_local, vec16,
-                                                           p.seg_stride);
+                                                           p.seg_stride, p.ldn);
 }
 
 // ---------------------------------------------------------------------------
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kDW * 32)
 k_spectra_dmma(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N, int T_eff, int nb,
                int L, const double* __restrict__ tf, const double2* __restrict__ wsum, int slot0, int slot_cap,
                double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local, int nyq_local,
-               int vec16, int seg_stride) {
+               int vec16, int seg_stride, int ldn) {
   constexpr int RS = kDTC + 16 / (int)sizeof(Tin);        // padded row (conflict-free A-fragment reads)
   constexpr int KS = kDTC / 4;                             // k-steps per chunk
   extern __shared__ __align__(16) unsigned char dm_smem[];
@@ -337,7 +337,7 @@ k_spectra_dmma(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
     double re = fma(-mean, W.x, acc[nt][0]), im = fma(-mean, W.y, acc[nt][1]);
     if (b == dc_local) re = im = 0.0;       // spectral.py:96
     if (b == nyq_local) im = 0.0;
-    const int64_t o = (((int64_t)slot * L + l) * nb + b) * N + n;
+    const int64_t o = (((int64_t)slot * L + l) * nb + b) * ldn + n;  // ring rows of ldn nodes
     X64[o] = make_double2(re, im);
     X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
   }
@@ -353,7 +353,7 @@ static void launch_dmma(const Plan& p, const void* x, int64_t ts, int64_t ns, in
   dim3 grid((p.N + kDRows - 1) / kDRows, kc * p.L);
   k_spectra_dmma<Tin, NT><<<grid, kDW * 32, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff, p.nb, p.L, p.dft_tf,
                                                          p.wsum, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local,
-                                                         p.nyq_local, vec16, p.seg_stride);
+                                                         p.nyq_local, vec16, p.seg_stride, p.ldn);
 }
 
 template <typename Tin>
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kFftWarps * 32)
 k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stride, int N, int T_eff, int nfft,
               int log2M, int lo, int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw,
               const double2* __restrict__ post_tw, int slot0, int slot_cap, double2* __restrict__ X64,
-              float2* __restrict__ X32, float scale, int dc_local, int nyq_local, int seg_stride) {
+              float2* __restrict__ X32, float scale, int dc_local, int nyq_local, int seg_stride, int ldn) {
   extern __shared__ double2 fft_smem[];
   const int M = nfft >> 1;
   double2* stw = fft_smem;                                  // [M/2] twiddles, shared by the CTA
@@ -649,7 +649,7 @@ k_spectra_fft(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_stri
       double im = ei + (wk.x * oi + wk.y * orr);
       if (b == dc_local) re = im = 0.0;
       if (b == nyq_local) im = 0.0;
-      const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * N + n;
+      const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * ldn + n;  // ring rows of ldn nodes
       X64[o] = make_double2(re, im);
       X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
     }
@@ -730,7 +730,7 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
                int nb, int L, const double* __restrict__ taper, const double2* __restrict__ tw4,
                const double2* __restrict__ post_tw, const double2* __restrict__ wsum, int slot0, int slot_cap,
                double2* __restrict__ X64, float2* __restrict__ X32, float scale, int dc_local, int nyq_local,
-               int n_trials, int vec16, int seg_stride) {
+               int n_trials, int vec16, int seg_stride, int ldn) {
   constexpr int R = 32 / A, M = 32 * A, S = 32 + R, PAD = 8 / R;
   constexpr int BUF = (A * S > M + PAD * R) ? A * S : M + PAD * R;
   extern __shared__ double2 f4_smem[];
@@ -849,7 +849,7 @@ k_spectra_fft4(const Tin* __restrict__ x, int64_t trial_stride, int64_t node_str
         double im = ei + (wk.x * oi + wk.y * orr) - mean_d * ws.y;
         if (b == dc_local) re = im = 0.0;
         if (b == nyq_local) im = 0.0;
-        const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * N + n;
+        const int64_t o = (((int64_t)slot * L + l) * (int64_t)nb + b) * ldn + n;  // ring rows of ldn nodes
         X64[o] = make_double2(re, im);
         X32[o] = make_float2((float)(re * (double)scale), (float)(im * (double)scale));
       }
@@ -885,7 +885,7 @@ void launch_fft4(const Plan& p, const void* x, int64_t ts, int64_t ns, int slot0
                     ((p.seg_stride * (int64_t)sizeof(Tin)) % 16 == 0);
   k_spectra_fft4<Tin, A><<<(unsigned)grid, kFft4Warps * 32, smem, st>>>((const Tin*)x, ts, ns, p.N, p.T_eff,
       p.lo, p.nb, p.L, p.taper, p.fft4_tw, p.post_tw, p.wsum, slot0, p.slot_cap, p.X64, p.X32, p.scale,
-      p.dc_local, p.nyq_local, kc, vec16, p.seg_stride);
+      p.dc_local, p.nyq_local, kc, vec16, p.seg_stride, p.ldn);
 }
 
 bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_t ns, int slot0, int kc,
@@ -909,12 +909,12 @@ bool run_spectra_fft(const Plan& p, const void* x, int dtype, int64_t ts, int64_
     CS_SMEM_ONCE(k_spectra_fft<double>, 200 * 1024);
     k_spectra_fft<double><<<grid, kFftWarps * 32, smem, st>>>((const double*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
         p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
-        p.seg_stride);
+        p.seg_stride, p.ldn);
   } else {
     CS_SMEM_ONCE(k_spectra_fft<float>, 200 * 1024);
     k_spectra_fft<float><<<grid, kFftWarps * 32, smem, st>>>((const float*)x, ts, ns, p.N, p.T_eff, p.nfft, log2M,
         p.lo, p.nb, p.L, p.taper, p.fft_tw, p.post_tw, slot0, p.slot_cap, p.X64, p.X32, p.scale, p.dc_local, p.nyq_local,
-        p.seg_stride);
+        p.seg_stride, p.ldn);
   }
   return true;
 }

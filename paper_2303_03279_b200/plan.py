@@ -129,6 +129,24 @@ class DevicePlan:
         _lib.check(_lib.lib().cs_spectra(self._h, ctypes.c_void_p(x.data_ptr()), dt, x.stride(0), x.stride(1),
                                          int(slot0), int(x.shape[0]), _stream_ptr(stream)))
 
+    def spectra_nodes(self, x: torch.Tensor, node0: int, slot0: int = 0, stream=None) -> None:
+        """K1 for the node range [node0, node0 + x.shape[1]) only (multi-GPU: a rank's
+        node block, csconn cs_spectra_nodes); x: device [k, n, T]."""
+        if x.device != self.device:
+            raise ParameterError("input must live on the plan's device")
+        if x.dim() != 3 or x.shape[2] != self.n_samples or node0 < 0 or node0 + x.shape[1] > self.n_nodes:
+            raise ParameterError(f"expected [k, n <= {self.n_nodes - node0}, {self.n_samples}] samples, "
+                                 f"got {tuple(x.shape)}")
+        if x.stride(2) != 1:
+            x = x.contiguous()
+        dt = {torch.float64: _lib.CS_F64, torch.float32: _lib.CS_F32}.get(x.dtype)
+        if dt is None:
+            raise ParameterError(f"unsupported sample dtype {x.dtype}")
+        self._last_x = x
+        _lib.check(_lib.lib().cs_spectra_nodes(self._h, ctypes.c_void_p(x.data_ptr()), dt, x.stride(0),
+                                               x.stride(1), int(node0), int(x.shape[1]), int(slot0),
+                                               int(x.shape[0]), _stream_ptr(stream)))
+
     # -- pair kernels -------------------------------------------------------
     def alloc_outputs(self, metrics, n_bins: int, per_bin=True, band=True, pair_count=None):
         P = self.n_pairs if pair_count is None else int(pair_count)

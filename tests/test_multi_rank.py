@@ -1,11 +1,11 @@
 """World-size-2 gloo tests of the multi-GPU host logic (CPU): node-block
-ownership, the spectrum-ring all-gather/reassembly used by bench.py, and the
+ownership (node n lives on rank n // nloc, the table the fp64 fallback reads
+through), the ring-handle exchange used by shard.RingExchange, and the
 pair-range sharding covering every pair exactly once."""
 import os
 import socket
 
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -23,31 +23,21 @@ def _worker(rank, world, port, n_nodes, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2303_03279_b200.shard import allgather_ring, node_block, shard_plan
-        S, L, nb = 3, 2, 4
+        from paper_2303_03279_b200.shard import exchange_handles, node_block, shard_plan
         n0, n1, nloc = node_block(n_nodes, world, rank)
-        local = torch.zeros((S, L, nb, nloc), dtype=torch.complex128)
-        ids = torch.arange(n0, n1, dtype=torch.float64)
-        for s in range(S):
-            for l in range(L):
-                for b in range(nb):
-                    local[s, l, b, : n1 - n0] = ids + 1j * (1000 * s + 100 * l + 10 * b)
-        full = torch.empty((S, L, nb, n_nodes), dtype=torch.complex128)
-        allgather_ring(local, full, dist)
-        want = torch.arange(n_nodes, dtype=torch.float64)
-        ok = all(torch.equal(full[s, l, b], want + 1j * (1000 * s + 100 * l + 10 * b))
-                 for s in range(S) for l in range(L) for b in range(nb))
+        owner_ok = all(n // nloc == rank for n in range(n0, n1))
+        # handle bytes of the size of a csconn ring handle (2 x 64 B IPC + geometry)
+        mine = bytes([rank]) * 144
+        allh = exchange_handles(dist, mine)
+        ex_ok = [h[0] for h in allh] == list(range(world))
         (rb, re_), (p0, p1) = shard_plan(n_nodes, world, rank)
-        rng = torch.tensor([p0, p1, rb, re_], dtype=torch.int64)
-        allr = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(allr, rng)
-        q.put((rank, ok, [r.tolist() for r in allr]))
+        q.put((rank, owner_ok and ex_ok, (n0, n1), (p0, p1, rb, re_)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_nodes", [130, 1000])
-def test_two_rank_ring_gather_and_pair_sharding(n_nodes):
+@pytest.mark.parametrize("n_nodes", [130, 1000, 10242])
+def test_two_rank_blocks_handles_and_pair_sharding(n_nodes):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -55,13 +45,16 @@ def test_two_rank_ring_gather_and_pair_sharding(n_nodes):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_nodes, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = sorted(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     P = n_nodes * (n_nodes - 1) // 2
-    for rank, ok, ranges in res:
-        assert ok, f"rank {rank}: reassembled ring mismatch"
-        assert ranges[0][0] == 0 and ranges[-1][1] == P
-        for a, b in zip(ranges, ranges[1:]):
-            assert a[1] == b[0] and a[3] == b[2]
+    assert all(ok for _, ok, _, _ in res)
+    blocks = [b for _, _, b, _ in res]
+    assert blocks[0][0] == 0 and blocks[-1][1] == n_nodes
+    assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+    ranges = [r for _, _, _, r in res]
+    assert ranges[0][0] == 0 and ranges[-1][1] == P
+    for a, b in zip(ranges, ranges[1:]):
+        assert a[1] == b[0] and a[3] == b[2]
