@@ -175,20 +175,19 @@ int cs_put_taper_spectra(cs_plan* plan, const void* src_dev, int n, int bin_lo, 
 int cs_net_normalize(float* w_dev, void* cw_dev, int64_t n, void* stream);
 int cs_net_threshold(const float* w_dev, int64_t n, int64_t keep, int64_t* out_idx_dev, void* stream);
 
-/* Time-domain metrics (metrics.py:140-260).  The Gram product and the FFTs are
- * library calls (cuBLAS, cuFFT); these are their epilogues.
- *  cs_cor_accumulate  total[p - pair_base] += clip(G[i][j], -1, 1) for pairs p in
- *                     [pair_base, pair_base + n_pairs) (G: fp64 [C][C] Pearson matrix).
- *  cs_xcor_peaks      per pair (pi[k], pj[k]): the first maximum over lags
- *                     [-max_lag, max_lag] of r[tau] / sqrt(ex(tau) ey), r from
- *                     cc[k][nfft] (circular, nfft >= 2 n - 1), ex from the prefix sums
- *                     csq[C][n + 1] of dx^2, ey = csq[j][n]; (0, 0) when ey == 0 or
- *                     xzero[i]; adds the value and the lag to peak_sum[k], lag_sum[k]. */
-int cs_cor_accumulate(const double* G_dev, int n_channels, int64_t pair_base, int64_t n_pairs,
-                      double* total_dev, void* stream);
-int cs_xcor_peaks(const double* cc_dev, int64_t n_pairs, int nfft, int n_samples, int max_lag,
-                  const int64_t* pi_dev, const int64_t* pj_dev, const double* csq_dev,
-                  const unsigned char* xzero_dev, double* peak_sum_dev, double* lag_sum_dev, void* stream);
+/* Time-domain metrics (metrics.py:140-260) on the fp64 tensor cores, every trial of
+ * a call in one launch.  x_dev: fp64 samples [n_trials][n_channels][n_samples].
+ *  cs_cor_sums   total[p] += clip(Pearson_k(i, j), -1, 1) over trials k (upper-triangle
+ *                pair order); dead (optional, [n_trials][n_channels]) = 1 for a
+ *                zero-variance channel (its edges are 0, the reference warns).
+ *  cs_xcor_sums  per pair the first maximum over lags [-max_lag, max_lag] of the
+ *                overlap-normalised cross-correlation, peak_sum[p] += value and
+ *                lag_sum[p] += lag over trials (negative lag: x = channel i leads);
+ *                a constant x or y gives (0, 0). */
+int cs_cor_sums(const double* x_dev, int n_trials, int n_channels, int n_samples, double* total,
+                unsigned char* dead, void* stream);
+int cs_xcor_sums(const double* x_dev, int n_trials, int n_channels, int n_samples, int max_lag,
+                 double* peak_sum, double* lag_sum, unsigned char* dead, void* stream);
 
 /* Which K1 kernel the plan runs (for rooflines / reports): 0 direct DFT on the
  * FP64 pipe, 1 direct DFT on the fp64 tensor cores, 2 four-step register FFT,
@@ -222,6 +221,22 @@ int64_t cs_launch_count(const cs_plan* plan);
 /* Device pointers of the spectrum ring (fp64 and fp32 copies, [slot][L][nb][N]
  * complex) and its element count: used to all-gather node blocks across GPUs. */
 int cs_ring_view(cs_plan* plan, void** x64, void** x32, int64_t* n_elems);
+
+/* ---- upstream of the spectra (upstream.cu; fp64, hand-written DMMA GEMM / FIR) ----
+ *  cs_apply_inverse  y[n_src][T] = M[n_src][n_sens] x[n_sens][T]   (inverse.py:147-154)
+ *  cs_project_ring   the source plan's rings (fp64 + scaled fp32) for slots slot0 ..
+ *                    slot0 + k_count - 1 = M[dst N][src N] times the sensor plan's
+ *                    fp64 spectra (same slots / tapers / bins): source connectivity
+ *                    without transforming the source time series
+ *  cs_fir_apply      streaming causal FIR of a block x[C][S] (preprocess.py:109-142):
+ *                    y = (taps * [hist, x])[:S]; hist / hist_out [C][n_taps - 1]
+ *                    (the previous / new last input samples; distinct buffers) */
+int cs_apply_inverse(const double* M_dev, int n_src, int n_sens, const double* x_dev, int n_samples,
+                     double* y_dev, void* stream);
+int cs_project_ring(cs_plan* dst_plan, const cs_plan* src_plan, const double* M_dev, int slot0, int k_count,
+                    void* stream);
+int cs_fir_apply(const double* taps_dev, int n_taps, const double* x_dev, int n_channels, int n_samples,
+                 const double* hist_dev, double* hist_out_dev, double* y_dev, void* stream);
 
 /* ---- multi-GPU: the spectrum ring exchanged over NVLink peer memory (shard.cu) ----
  * Every rank holds a plan over all N nodes; rank r computes K1 for its node block

@@ -1,14 +1,12 @@
 """Time-domain metrics COR and XCOR on the device (reference metrics.py:137-260).
 
-COR: per trial the Pearson matrix of the demeaned, normalised channels is one
-Gram product (cuBLAS DGEMM, fp64 like the reference); the clipped upper
-triangle is accumulated by ``cs_cor_accumulate``.  XCOR: per trial one real FFT
-per channel (cuFFT, fp64), an inverse FFT per pair of X_i conj X_j gives every
-lag's numerator at once, and ``cs_xcor_peaks`` normalises by the overlap
-energies and takes the first maximum over [-max_lag, max_lag] (one warp per
-pair).  Both keep the reference's edge cases: zero-variance channels give
-zero-weight COR edges and a warning; an XCOR pair with a constant x or y gives
-(0, lag 0).
+Both run in the hand-written kernels of csrc/timedomain.cu on the fp64 tensor
+cores (DMMA): COR as the Gram product of the demeaned unit-norm channels with the
+clip fused in (``cs_cor_sums``), XCOR as per-lag "shifted Gram" products of the
+demeaned channels with the overlap normalisation and the first-maximum argmax
+fused in (``cs_xcor_sums``), every trial of a call in one launch.  Both keep the
+reference's edge cases: zero-variance channels give zero-weight COR edges and a
+warning; an XCOR pair with a constant x or y gives (0, lag 0).
 """
 from __future__ import annotations
 
@@ -31,6 +29,26 @@ def _dev_f64(data) -> torch.Tensor:
     return t.to(device=_device(), dtype=torch.float64)
 
 
+def _groups(epochs_data, C: int):
+    """Device fp64 stacks [k, C, T] of consecutive epochs sharing n_samples (the
+    reference allows epochs of different lengths; each stack is one launch)."""
+    out, cur = [], []
+    for data in epochs_data:
+        x = _dev_f64(data)
+        if x.dim() != 2 or x.shape[0] != C:
+            raise ParameterError("epochs must have equal channel counts")
+        if cur and x.shape[1] != cur[0].shape[1]:
+            out.append(torch.stack(cur))
+            cur = []
+        cur.append(x)
+        if len(cur) == 65535:
+            out.append(torch.stack(cur))
+            cur = []
+    if cur:
+        out.append(torch.stack(cur))
+    return out
+
+
 def cor_sums(epochs_data, n_channels: int):
     """(sum over epochs of the clipped Pearson upper triangle [P] fp64 device,
     sorted zero-variance channels) -- metrics.py:140-177."""
@@ -38,59 +56,40 @@ def cor_sums(epochs_data, n_channels: int):
     P = C * (C - 1) // 2
     total = None
     dead = set()
-    for data in epochs_data:
-        x = _dev_f64(data)
-        if x.shape[0] != C:
-            raise ParameterError("epochs must have equal channel counts")
+    for xs in _groups(epochs_data, C):
+        K, _, T = xs.shape
         if total is None:
-            total = torch.zeros(P, dtype=torch.float64, device=x.device)
-        d = x - x.mean(dim=1, keepdim=True)
-        norms = torch.sqrt((d * d).sum(dim=1))
-        z = norms == 0.0
-        if bool(z.any()):
-            dead.update(torch.nonzero(z).flatten().tolist())
-        u = d / torch.where(z, torch.ones_like(norms), norms)[:, None]
-        G = (u @ u.T).contiguous()                       # cuBLAS DGEMM
-        if P:
-            _lib.check(_lib.lib().cs_cor_accumulate(ctypes.c_void_p(G.data_ptr()), C, 0, P,
-                                                    ctypes.c_void_p(total.data_ptr()), _sp()))
+            total = torch.zeros(P, dtype=torch.float64, device=xs.device)
+        if P == 0:  # one channel: no pairs, only the zero-variance warning
+            flags = (xs == xs[..., :1]).all(dim=-1)
+        else:
+            flags = torch.zeros((K, C), dtype=torch.uint8, device=xs.device)
+            _lib.check(_lib.lib().cs_cor_sums(ctypes.c_void_p(xs.data_ptr()), K, C, T,
+                                              ctypes.c_void_p(total.data_ptr()), ctypes.c_void_p(flags.data_ptr()),
+                                              _sp()))
+        dead.update(torch.nonzero(flags.any(dim=0)).flatten().tolist())
     return total, sorted(dead)
 
 
-def xcor_sums(epochs_data, n_channels: int, max_lag: int, pair_chunk: int | None = None):
-    """(sum of per-epoch peak values [P], sum of peak lags [P], n_epochs), fp64
-    device -- metrics.py:180-260 (peak of the overlap-normalised
-    cross-correlation, negative lag = x leads y)."""
+def xcor_sums(epochs_data, n_channels: int, max_lag: int):
+    """(sum of per-epoch peak values [P], sum of peak lags [P]), fp64 device --
+    metrics.py:180-260 (peak of the overlap-normalised cross-correlation,
+    negative lag = x leads y)."""
     C = int(n_channels)
     P = C * (C - 1) // 2
     peak = lag = None
-    pi = pj = None
-    for data in epochs_data:
-        x = _dev_f64(data)
-        n = x.shape[1]
-        if max_lag >= n:
+    for xs in _groups(epochs_data, C):
+        K, _, T = xs.shape
+        if max_lag >= T:
             raise ParameterError("max_lag must be < n_samples")
         if peak is None:
-            peak = torch.zeros(P, dtype=torch.float64, device=x.device)
-            lag = torch.zeros(P, dtype=torch.float64, device=x.device)
-            a, b = np.triu_indices(C, 1)
-            pi = torch.as_tensor(a, dtype=torch.int64, device=x.device)
-            pj = torch.as_tensor(b, dtype=torch.int64, device=x.device)
-        nfft = 1 << max(1, (2 * n - 1 - 1).bit_length())      # >= 2 n - 1: no circular wrap
-        d = x - x.mean(dim=1, keepdim=True)
-        xz = (d == 0).all(dim=1).to(torch.uint8).contiguous()
-        csq = torch.cat([torch.zeros((C, 1), dtype=torch.float64, device=x.device), torch.cumsum(d * d, 1)], 1)
-        csq = csq.contiguous()
-        X = torch.fft.rfft(d, n=nfft, dim=1)                  # cuFFT, fp64
-        chunk = pair_chunk or max(1, min(P, (1 << 28) // (8 * nfft)))
-        for p0 in range(0, P, chunk):
-            a, b = pi[p0:p0 + chunk], pj[p0:p0 + chunk]
-            cc = torch.fft.irfft(X[a] * torch.conj(X[b]), n=nfft, dim=1).contiguous()
-            _lib.check(_lib.lib().cs_xcor_peaks(
-                ctypes.c_void_p(cc.data_ptr()), int(a.numel()), nfft, n, int(max_lag),
-                ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(csq.data_ptr()),
-                ctypes.c_void_p(xz.data_ptr()), ctypes.c_void_p(peak[p0:].data_ptr()),
-                ctypes.c_void_p(lag[p0:].data_ptr()), _sp()))
+            peak = torch.zeros(P, dtype=torch.float64, device=xs.device)
+            lag = torch.zeros(P, dtype=torch.float64, device=xs.device)
+        if P == 0:
+            continue
+        _lib.check(_lib.lib().cs_xcor_sums(ctypes.c_void_p(xs.data_ptr()), K, C, T, int(max_lag),
+                                           ctypes.c_void_p(peak.data_ptr()), ctypes.c_void_p(lag.data_ptr()), None,
+                                           _sp()))
     return peak, lag
 
 
