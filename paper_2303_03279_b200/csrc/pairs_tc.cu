@@ -209,9 +209,9 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   int64_t* rowoff_s = (int64_t*)(colfac + kTcTileJ);                   // [128] output row offsets
   uint64_t* full = (uint64_t*)(rowoff_s + kTcTile);
   uint64_t* empty = full + kTcStages;
-  uint64_t* tfull = empty + kTcStages;   // [2] per pass region
-  uint64_t* tempty = tfull + 2;          // [2]
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* tfull = empty + kTcStages;   // [3] per accumulator region
+  uint64_t* tempty = tfull + 3;          // [3]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // persistent CTAs: work unit u = (tile u / nbc, bin chunk u % nbc), strided by the grid;
@@ -225,7 +225,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 3; ++r) {
       mbar_init(&tfull[r], 1);
       mbar_init(&tempty[r], kTcEpiWarps);  // one arrive per epilogue warp
     }
@@ -243,6 +243,10 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   const int n_chunk = (a.K_pad + kTcChunk - 1) / kTcChunk;
   const int npass = a.do_x + a.do_u;
   const int pass0 = a.do_x ? 0 : 1;
+  // accumulator regions of 128 TMEM columns, used round-robin by the (bin, pass) sequence
+  // so the MMAs can run ahead of the epilogue: [0,128), [128,256) and, when the band sums
+  // need only [256,384) (no COHY / IMAGCOHY band), a third at [384,512)
+  const int nreg = (a.cohy_band || a.imag_band) ? 2 : 3;
 
   // register budgets: warps 0-3 (TMA, MMA, TMEM allocator, spare) drop to 32, the
   // epilogue warps rise to 112 (launch pool 640 x 96 = 128 x 32 + 512 x 112)
@@ -291,16 +295,18 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     int stage = 0;
     uint32_t phase = 0;
     uint32_t tuse = 0;  // bit r: phase of TMEM region r
+    int seq = 0;        // (bin, pass) counter -> region seq % nreg
     const uint64_t desc0 = umma_desc_sw64(smem_u32(smem));
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
       for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
-          const int reg = ps;
+          const int reg = seq % nreg;
+          ++seq;
           mbar_wait(&tempty[reg], ((tuse >> reg) & 1) ^ 1);
           tuse ^= 1u << reg;
           tc_fence_after();
-          const uint32_t d_re = tmem + reg * 128, d_im = d_re + 64;
+          const uint32_t d_re = tmem + (reg == 2 ? 384 : reg * 128), d_im = d_re + 64;
           for (int c = 0; c < n_chunk; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
@@ -339,6 +345,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     const uint32_t xrow = xb + (uint32_t)(r * kTcXStride) * 8u;  // this thread's transpose row
     const bool cohy = a.cohy_bins || a.cohy_band;
     uint32_t tuse = 0;  // bit r: phase of TMEM region r
+    int seq = 0;        // (bin, pass) counter, as in the MMA warp
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
     const int2 tij = a.tiles[u / a.nbc];
     const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
@@ -375,11 +382,12 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       epi_bar();
       for (int ps = 0; ps < npass; ++ps) {
         const int pass = pass0 + ps;
-        const int reg = ps;
+        const int reg = seq % nreg;
+        ++seq;
         mbar_wait(&tfull[reg], (tuse >> reg) & 1);
         tuse ^= 1u << reg;
         tc_fence_after();
-        const uint32_t t_acc = tmem + lane_addr + reg * 128;
+        const uint32_t t_acc = tmem + lane_addr + (reg == 2 ? 384 : reg * 128);
 #pragma unroll
         for (int c1 = 0; c1 < kTcColsPerWarp; c1 += 8) {
           const int c0 = cb + c1;
