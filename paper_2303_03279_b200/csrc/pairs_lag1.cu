@@ -400,7 +400,12 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           float* bs = band_s + li * kTile + lj;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
-            if (bin_mask & (1u << m)) __stcs(&a.bins[m][rowoff + j], v[m]);
+            if (bin_mask & (1u << m)) {
+              if (FULL)  // host-checked: every per-bin index < 2^32 -> one IMAD.WIDE.U32 per address
+                __stcs(&a.bins[m][(uint32_t)(rowoff + j)], v[m]);
+              else
+                __stcs(&a.bins[m][rowoff + j], v[m]);
+            }
             if (band_mask & (1u << m)) bs[m * kTile * kTile] += v[m];
           }
         }
@@ -511,7 +516,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
       case kStSign | kStSum: CS_LAG1S(1, false, kStSign | kStSum); break;
       case kStSum | kStAbs: CS_LAG1S(1, false, kStSum | kStAbs); break;
       default: {
-        bool full = true;
+        bool full = (uint64_t)nbb * (uint64_t)pair_stride < (1ull << 32);  // 32-bit per-bin offsets
         for (int m = 0; m < 5; ++m) full = full && bins[m] && band[m];
         if (full) {
           CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, true>), smem);
