@@ -218,28 +218,23 @@ def run_reference(args, c, rank):
 def run_window(args, c, dist, rank, ws, lr):
     """Config 4: online sliding window.  A stream of 1045 trials, window w =
     trials [5w, 5w + 50): per window K1 runs on the 5 new trials only (cached
-    spectra of the other 45 are reused from the HBM ring) and the pair kernels
-    recompute PLV and WPLI over the window's 50 slots -- the work the
-    reference's rebuild_last(50) performs (metrics.py:450-460,
-    pipeline.py:304-309).  Each window is one staging copy of the new trials plus
-    one CUDA-graph replay (plan.WindowGraph; one graph per ring phase, captured in
-    the warm-up).  Replicas only at N > 1 (each rank its own stream)."""
+    spectra of the other 45 are reused from the HBM ring) and PLV and WPLI are
+    produced over the window's 50 trials -- the work the reference's
+    rebuild_last(50) performs (metrics.py:450-460, pipeline.py:304-309), counted
+    as P nb 50 updates per window.  The timed path is the incremental window
+    (plan.IncrementalWindow, csrc/window.cu): the running sums move by the 5
+    entering and 5 leaving trials, risky (pair, bin) entries are recomputed over
+    the window in fp64, one CUDA-graph replay per window.  The full re-fold of
+    every window (plan.WindowGraph, the reference's semantics executed literally)
+    is timed beside it as ``full_recompute``.  Replicas only at N > 1."""
     from paper_2303_03279_b200 import synth
-    from paper_2303_03279_b200.plan import DevicePlan, WindowGraph, pow2_scale, probe_peaks
+    from paper_2303_03279_b200.plan import DevicePlan, IncrementalWindow, WindowGraph, pow2_scale, probe_peaks
     dev = torch.device("cuda", lr)
-    cap = 50                       # ring = the window: new trials overwrite the ones that left it
-    n_phases = cap // math.gcd(cap, 5)
-    warm = max(args.warmup, n_phases)  # every ring phase's graph is captured before the timed region
-    W = min(synth.CFG4_WINDOWS, warm + args.steps + 1)  # windows of the stream (more steps cycle over it)
-    n_trials = 5 * (W - 1) + 50
+    win, new = 50, 5
+    W = min(synth.CFG4_WINDOWS, max(args.warmup, 11) + args.steps + 1)  # windows of the stream
+    n_trials = new * (W - 1) + win
     x = synth.generate(c, dev, trials=range(n_trials))            # [n_trials, N, T] resident in HBM
-    plan = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=cap, device=dev,
-                      scale=pow2_scale(float(x.abs().amax()), min(c.T, c.nfft)))
-    wg = WindowGraph(plan, 5, c.metrics, 0, c.n_bins)
-
-    def window(w):  # trials [5w, 5w + 50): K1 on the 5 new ones, pair kernels over all 50
-        w = 1 + (w - 1) % (W - 1)
-        wg.update(x[5 * w + 45: 5 * w + 50])
+    scale = pow2_scale(float(x.abs().amax()), min(c.T, c.nfft))
 
     def barrier():
         if dist is not None:
@@ -253,67 +248,86 @@ def run_window(args, c, dist, rank, ws, lr):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
-    wg.prime(x[0:50])
-    for w in range(1, 1 + warm):
-        window(w)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(lr) as clk:
+    def new_trials(w):  # trials [5w + 45, 5w + 50) of window w (cycling over the generated stream)
+        w = 1 + (w - 1) % (W - 1)
+        return x[new * w + win - new: new * w + win]
+
+    def time_windows(runner, warm):
+        for w in range(1, 1 + warm):
+            runner.update(new_trials(w))
         barrier()
-        e0.record()
-        for w in range(1 + warm, 1 + warm + args.steps):
-            window(w)
-        e1.record()
-        barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)   # replicas: every rank runs its own stream
-    launches = wg.graph_kernels() * args.steps
-    # e2e: the online use -- each window's 5 new trials arrive in pinned host memory
-    # (H2D into the staging buffer inside update()), the window's band results are
-    # read back to the host after it
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(lr) as clk:
+            barrier()
+            e0.record()
+            for w in range(1 + warm, 1 + warm + args.steps):
+                runner.update(new_trials(w))
+            e1.record()
+            barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps), clk.summary()
+
+    # the timed online path: incremental sums
+    plan_i = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=win + new, device=dev, scale=scale)
+    iw = IncrementalWindow(plan_i, win, new, c.metrics)
+    iw.prime(x[0:win])
+    warm_i = max(args.warmup, 2 * iw.n_phases)          # every (phase, buffer) graph captured
+    ms, clk = time_windows(iw, warm_i)
+    launches = iw.graph_kernels() * args.steps
+    # e2e: each window's 5 new trials from pinned host memory, band results back to the host
     n_e2e = min(args.steps, 500)
-    xh = x[: 5 * (W - 1) + 50].cpu().pin_memory()
+    xh = x[: new * (W - 1) + win].cpu().pin_memory()
     hb = {m: torch.empty(c.n_pairs, dtype=torch.float32).pin_memory() for m in c.metrics}
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
-    for w in range(1 + warm, 1 + warm + n_e2e):   # back to back: upload / kernels / download overlap
+    for w in range(1 + warm_i, 1 + warm_i + n_e2e):   # back to back: upload / kernels / download overlap
         wi = 1 + (w - 1) % (W - 1)
-        ev = wg.submit(xh[5 * wi + 45: 5 * wi + 50], hb)
+        ev = iw.submit(xh[new * wi + win - new: new * wi + win], hb)
     torch.cuda.current_stream().wait_event(ev)
     f1.record()
     barrier()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1) / n_e2e)
-    # per-kernel breakdown from an eager (un-graphed, profiled) pass over the same windows
-    plan.set_profiling(True)
-    plan.profile()
+    # per-kernel breakdown from an eager profiled pass (graphs are not profiled per kernel)
+    plan_i.set_profiling(True)
+    plan_i.profile()
     n_prof = min(args.steps, 10)
-    for w in range(1 + warm, 1 + warm + n_prof):
-        slot0 = (5 * w + 45) % cap
-        plan.spectra(x[5 * w + 45: 5 * w + 50], slot0)
-        plan.pair_metrics(wg._slots[w % n_phases], c.metrics, 0, c.n_bins, outputs=wg.outputs)
-    prof = plan.profile()
-    plan.set_profiling(False)
-    upd = c.n_pairs * c.n_bins * 50
+    for w in range(1, 1 + n_prof):
+        iw._body(iw.updates % iw.n_phases, 0)
+        iw.updates += 1
+    prof = plan_i.profile()
+    plan_i.set_profiling(False)
     per = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
+    del iw, plan_i
+
+    # the full re-fold of every window, for comparison
+    plan_f = DevicePlan(c.N, c.T, c.nfft, c.lo, c.hi, taper=c.taper, slot_capacity=win, device=dev, scale=scale)
+    wg = WindowGraph(plan_f, new, c.metrics, 0, c.n_bins)
+    wg.prime(x[0:win])
+    ms_full, _ = time_windows(wg, max(args.warmup, 2 * wg.n_phases))
+    del wg, plan_f
+
+    upd = c.n_pairs * c.n_bins * win
     fp32_ops, fp64_fma = probe_peaks(lr)
     line = {"metric": metric_name(c),
             "value": ws * upd / (ms * 1e-3),
             "unit": "updates/s", "ms_per_window": ms, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY.md 8(d) cfg4 pink noise + planted 20 Hz)",
-            "config": {"workload": f"cfg{c.cfg}: {c.name}", "N": c.N, "window": 50, "new_trials_per_window": 5,
+            "config": {"workload": f"cfg{c.cfg}: {c.name}", "N": c.N, "window": win, "new_trials_per_window": new,
                        "bins": [c.lo, c.hi], "metrics": list(c.metrics), "parallelism": f"replicas x{ws}",
-                       "updates_per_window": upd},
+                       "updates_per_window": upd,
+                       "path": "incremental window sums (+5 entering, -5 leaving trials; fp64 re-fold of risky "
+                               "entries), one CUDA-graph replay per window"},
+            "full_recompute": {"ms_per_window": ms_full, "updates_per_s": ws * upd / (ms_full * 1e-3),
+                               "path": "WindowGraph: the pair kernels re-fold all 50 trials every window"},
             "breakdown": {k: {"ms_per_launch": round(v, 4), "launches": prof[k][1]} for k, v in per.items()},
             "breakdown_note": "eager profiled pass over the same windows; the timed region replays CUDA graphs",
-            "cuda_graphs": {"phases": n_phases, "kernels_per_window": wg.graph_kernels(),
-                            "staging_copy_bytes": int(wg.staging.numel() * wg.staging.element_size())},
-            "gpu_launches": launches, "clocks": clk.summary(),
+            "gpu_launches": launches, "clocks": clk,
             "e2e": {"value": ws * upd / (e2e_ms * 1e-3), "unit": "updates/s", "ms_per_window": e2e_ms,
                     "windows": n_e2e,
-                    "h2d_bytes_per_step": int(wg.staging.numel() * 4) * ws,
+                    "h2d_bytes_per_step": int(new * c.N * c.T * 4) * ws,
                     "d2h_bytes_per_step": int(sum(v.numel() * 4 for v in hb.values())) * ws,
-                    "path": "WindowGraph.submit(pinned host trials, pinned host band buffers): H2D into a "
+                    "path": "IncrementalWindow.submit(pinned host trials, pinned host band buffers): H2D into a "
                             "double-buffered staging buffer, graph replay, band results D2H, on three streams "
                             "so consecutive windows overlap"},
             "peaks": {"fp32_lane_ops_per_s": fp32_ops, "fp64_dfma_per_s": fp64_fma}}

@@ -222,6 +222,23 @@ int64_t cs_launch_count(const cs_plan* plan);
  * complex) and its element count: used to all-gather node blocks across GPUs. */
 int cs_ring_view(cs_plan* plan, void** x64, void** x32, int64_t* n_elems);
 
+/* ---- incremental online window (window.cu; pipeline.py:304-309, metrics.py:450-460) ----
+ * The reference re-folds the whole window per update (rebuild_last); every fold sum is
+ * additive over trials, so a cs_window keeps per-(pair, bin) running sums (fp32 / int32)
+ * for the metric families of its mask and moves them by the changed trials only:
+ * changed_slots = n_add new ring slots then n_sub leaving ones.  Per trial the
+ * exact-sign guard is |Im| <= g |X_i||X_j| (a count that moves with the window); a
+ * (pair, bin) with a risky trial in the window is recomputed over window_slots[0..K) in
+ * fp64 by the fallback.  Outputs (all pairs, pair_base 0): per-bin values and band
+ * means by metric bit (either may be NULL).  COHY and multitaper plans are not incremental.
+ * cs_window_reset zeroes the sums (resynchronise: reset + one update adding the window). */
+typedef struct cs_window cs_window;
+int cs_window_create(cs_window** w, cs_plan* plan, unsigned metric_mask, int bin_lo, int n_bins);
+int cs_window_destroy(cs_window* w);
+int cs_window_reset(cs_window* w, void* stream);
+int cs_window_update(cs_window* w, const int* changed_slots_dev, int n_add, int n_sub,
+                     const int* window_slots_dev, int K, const cs_outputs* out, void* stream);
+
 /* ---- upstream of the spectra (upstream.cu; fp64, hand-written DMMA GEMM / FIR) ----
  *  cs_apply_inverse  y[n_src][T] = M[n_src][n_sens] x[n_sens][T]   (inverse.py:147-154)
  *  cs_project_ring   the source plan's rings (fp64 + scaled fp32) for slots slot0 ..

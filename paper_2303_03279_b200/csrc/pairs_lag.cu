@@ -196,6 +196,30 @@ static unsigned fallback_blocks(const LagArgs& a) {
   return (unsigned)(pb < 148 ? 148 : (pb > 148 * 8 ? 148 * 8 : pb));
 }
 
+// the incremental window's fallback (window.cu): the risky (pair, bin) entries over the
+// window's slots (per-bin values; band means by atomic adds like the batch path)
+void run_window_fallback(Plan& p, const int* slots, int K, int bin_lo, int nbb, const float* psd,
+                         float* const* bins5, float* const* band5, int4* recs, cudaStream_t st) {
+  LagArgs a{};
+  a.X64 = p.X64;
+  a.N = p.N; a.nb = p.nb; a.L = p.L;
+  a.slots = slots; a.K = K;
+  a.bin_lo = bin_lo; a.nbb = nbb;
+  a.psd = psd;
+  a.pair_base = 0;
+  a.pair_stride = (int64_t)p.N * (p.N - 1) / 2;
+  for (int q = 0; q < 5; ++q) {
+    a.bins[q] = bins5[q];
+    a.band[q] = band5[q];
+  }
+  a.scale2 = p.scale * p.scale;
+  a.flags = p.flags; a.recs = recs; a.counters = p.counters; a.flag_cap = p.flag_cap;
+  a.x64_of = p.n_ranks > 1 ? p.peer_x64 : nullptr;
+  a.node_block = p.node_block;
+  PhaseMark ph(p, "lag_fallback", st);
+  k_lag_fallback<<<fallback_blocks(a), 256, 0, st>>>(a);
+}
+
 bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, int Kp, int bin_lo, int nbb,
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,

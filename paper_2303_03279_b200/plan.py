@@ -638,3 +638,194 @@ class WindowGraph:
     def graph_kernels(self) -> int:
         """Kernels one replay launches (the plan's launch counter over one eager update)."""
         return self._kernels_per_update
+
+
+class IncrementalWindow:
+    """The online sliding window (``update_and_finalize`` every ``n_new`` trials over
+    the last ``window``; pipeline.py:304-309, metrics.py:450-460) with the running sums
+    moved by the changed trials only (csconn ``cs_window_*``, csrc/window.cu).
+
+    The reference's ``rebuild_last`` re-folds all ``window`` trials per update; the
+    fold sums are additive over trials, so each update adds the ``n_new`` trials that
+    entered and subtracts the ``n_new`` that left: O(n_new) work per (pair, bin)
+    instead of O(window).  A (pair, bin) with a trial inside the fp32 exact-sign error
+    bound anywhere in the window is recomputed over the whole window in fp64 (the batch
+    path's fallback), and the sums are rebuilt from scratch every ``resync_every``
+    updates so fp32 rounding cannot drift.  The plan's ring needs ``window + n_new``
+    slots (new trials must not overwrite the ones still to be subtracted).  One CUDA
+    graph per (ring phase, buffer) -- K1 on the staging buffer, the sums update, the
+    fallback, the band means -- is captured on first use and replayed after; staging
+    buffers and output sets are double-buffered so ``submit`` overlaps the next
+    window's upload and the previous window's download with the kernels.
+    """
+
+    def __init__(self, plan: DevicePlan, window: int, n_new: int, metrics=("PLV", "WPLI"), bin_lo: int = 0,
+                 n_bins: int | None = None, dtype=torch.float32, resync_every: int = 256, buffers: int = 2):
+        self.plan = plan
+        self.window, self.n_new = int(window), int(n_new)
+        if not 1 <= self.n_new <= self.window:
+            raise ParameterError(f"n_new must be in [1, {self.window}], got {n_new}")
+        if plan.slot_capacity < self.window + self.n_new:
+            raise ParameterError(f"the plan needs window + n_new = {self.window + self.n_new} slots, "
+                                 f"has {plan.slot_capacity}")
+        self.cap = plan.slot_capacity
+        self.metrics = tuple(m.upper() for m in metrics)
+        self.bin_lo = int(bin_lo)
+        self.n_bins = plan.n_bins - self.bin_lo if n_bins is None else int(n_bins)
+        mask = 0
+        for m in self.metrics:
+            if m not in METRIC_BITS:
+                raise ParameterError(f"{m} is not a spectral metric")
+            mask |= 1 << METRIC_BITS[m]
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().cs_window_create(ctypes.byref(h), plan._h, mask, self.bin_lo, self.n_bins))
+        self._h = h
+        self.nbuf = max(1, int(buffers))
+        self._outs, self._descs = [], []
+        for _ in range(self.nbuf):
+            o = plan.alloc_outputs(self.metrics, self.n_bins, per_bin=True, band=True)
+            d = _lib.CsOutputs()
+            for m in self.metrics:
+                d.bins[METRIC_BITS[m]] = o[m]["bins"].data_ptr()
+                d.band[METRIC_BITS[m]] = o[m]["band"].data_ptr()
+            d.pair_base = 0
+            d.pair_stride = plan.n_pairs
+            self._outs.append(o)
+            self._descs.append(d)
+        self._stage = [torch.empty((self.n_new, plan.n_nodes, plan.n_samples), dtype=dtype, device=plan.device)
+                       for _ in range(self.nbuf)]
+        self.n_phases = self.cap // math.gcd(self.cap, self.n_new)
+        dev = plan.device
+        # phase u (window starts at trial u n_new mod cap): changed slots (entering, then leaving)
+        # and the window's slots
+        self._changed, self._win = [], []
+        for u in range(self.n_phases):
+            first = (u * self.n_new) % self.cap
+            new = [(first + self.window - self.n_new + q) % self.cap for q in range(self.n_new)]
+            old = [(first - self.n_new + q) % self.cap for q in range(self.n_new)]
+            self._changed.append(torch.tensor(new + old, dtype=torch.int32, device=dev))
+            self._win.append(torch.tensor([(first + k) % self.cap for k in range(self.window)], dtype=torch.int32,
+                                          device=dev))
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+        self._kernels_per_update = 0
+        self.resync_every = max(1, int(resync_every))
+        self.updates = 0
+        self._cur = 0
+        with torch.cuda.device(dev):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+            self._ev_in = [torch.cuda.Event() for _ in range(self.nbuf)]
+            self._ev_used = [torch.cuda.Event() for _ in range(self.nbuf)]
+            self._ev_out = [torch.cuda.Event() for _ in range(self.nbuf)]
+            for e in self._ev_used + self._ev_out:
+                e.record()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().cs_window_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def outputs(self) -> dict:
+        """Output set of the latest update."""
+        return self._outs[self._cur]
+
+    @property
+    def staging(self) -> torch.Tensor:
+        return self._stage[0]
+
+    def _update_call(self, changed, n_add, n_sub, win, b):
+        _lib.check(_lib.lib().cs_window_update(self._h, ctypes.c_void_p(changed.data_ptr()), int(n_add), int(n_sub),
+                                               ctypes.c_void_p(win.data_ptr()), self.window,
+                                               ctypes.byref(self._descs[b]), _stream_ptr(None)))
+
+    def _resync(self, u: int, b: int) -> None:
+        """Sums of the window of phase u from scratch (reset + add every window trial)."""
+        _lib.check(_lib.lib().cs_window_reset(self._h, _stream_ptr(None)))
+        self._update_call(self._win[u], self.window, 0, self._win[u], b)
+
+    def prime(self, x: torch.Tensor) -> dict:
+        """The first ``window`` trials [window, N, T]: K1 into slots 0.., sums from scratch."""
+        if x.shape[0] != self.window:
+            raise ParameterError(f"prime needs {self.window} trials, got {x.shape[0]}")
+        self.plan.spectra(x.to(self.plan.device, non_blocking=True), 0)
+        self._resync(0, 0)
+        self._ev_used[0].record()
+        self._cur = 0
+        self.updates = 1
+        return self._outs[0]
+
+    def _body(self, u: int, b: int) -> None:
+        self.plan.spectra(self._stage[b], (u * self.n_new + self.window - self.n_new) % self.cap)
+        self._update_call(self._changed[u], self.n_new, self.n_new, self._win[u], b)
+
+    def _run(self, u: int, b: int) -> None:
+        if self.updates % self.resync_every == 0:   # fp32 rounding of the running sums stays bounded
+            self.plan.spectra(self._stage[b], (u * self.n_new + self.window - self.n_new) % self.cap)
+            self._resync(u, b)
+            return
+        key = (u, b)
+        g = self._graphs.get(key)
+        if g is not None:
+            g.replay()
+            return
+        l0 = self.plan.launch_count()
+        self._body(u, b)  # eager once per key (this update's sums move here)
+        self._kernels_per_update = self.plan.launch_count() - l0
+        torch.cuda.current_stream().synchronize()
+        prof = self.plan.profiling
+        if prof:
+            self.plan.set_profiling(False)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):  # capture only: the eager call above applied this update
+                self._body(u, b)
+        finally:
+            if prof:
+                self.plan.set_profiling(True)
+        self._graphs[key] = g
+
+    def submit(self, x_new: torch.Tensor, host_out: dict | None = None):
+        """Append ``n_new`` trials [n_new, N, T] (pinned host or device memory) and enqueue
+        the window update; with ``host_out`` ({metric: pinned float32 [P]}) the band means
+        are downloaded into it.  Returns the CUDA event marking the results complete;
+        nothing synchronises the host."""
+        if self.updates == 0:
+            raise ParameterError("prime() the first window first")
+        if tuple(x_new.shape) != tuple(self._stage[0].shape):
+            raise ParameterError(f"expected {tuple(self._stage[0].shape)} new samples, got {tuple(x_new.shape)}")
+        u = self.updates % self.n_phases
+        b = self.updates % self.nbuf
+        cs = torch.cuda.current_stream(self.plan.device)
+        self._h2d.wait_event(self._ev_used[b])        # the update that last read stage b is done
+        if x_new.is_cuda:
+            self._h2d.wait_stream(cs)
+        with torch.cuda.stream(self._h2d):
+            self._stage[b].copy_(x_new, non_blocking=True)
+            self._ev_in[b].record()
+        cs.wait_event(self._ev_in[b])
+        cs.wait_event(self._ev_out[b])                # output set b has been downloaded
+        self._run(u, b)
+        self._ev_used[b].record(cs)
+        self._cur = b
+        self.updates += 1
+        if host_out is None:
+            return self._ev_used[b]
+        self._d2h.wait_event(self._ev_used[b])
+        with torch.cuda.stream(self._d2h):
+            for m, h in host_out.items():
+                h.copy_(self._outs[b][m]["band"], non_blocking=True)
+            self._ev_out[b].record()
+        return self._ev_out[b]
+
+    def update(self, x_new: torch.Tensor) -> dict:
+        """Append ``n_new`` trials [n_new, N, T] (host or device) and return the new
+        window's outputs (device buffers, stream-ordered; reused ``buffers`` updates later)."""
+        self.submit(x_new)
+        return self._outs[self._cur]
+
+    def graph_kernels(self) -> int:
+        return self._kernels_per_update
