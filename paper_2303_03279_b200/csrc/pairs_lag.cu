@@ -54,6 +54,8 @@ struct LagArgs {
   int flag_cap;
   double2* const* x64_of;  // sharded plan: fp64 ring of the rank owning node n / node_block (else null)
   int node_block;
+  const float* imag_in;    // hand-off: IMAGCOHY per bin from the tensor-core kernel (else null)
+  float imag_tau;
 };
 
 // Trial-pair packing of the selected trials (k = 2 kp, 2 kp + 1) into the layouts the
@@ -224,9 +226,9 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
-                 int L, float* plv_bins, float* plv_band, cudaStream_t st);
+                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, cudaStream_t st);
 
-bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) {
+bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, bool handoff) {
   cudaMemsetAsync(a.counters, 0, 3 * sizeof(int), st);
   if (!p.reuse_prep) {
     PhaseMark ph(p, "lag_prep", st);
@@ -267,7 +269,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st) 
     }
     if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
                      a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.recs, a.counters, a.flag_cap,
-                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, st))
+                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, a.imag_in, a.imag_tau, st))
       return false;
   }
   {
@@ -296,8 +298,26 @@ static bool imag_on_tensor_cores(unsigned mask) {
   return (mask & CS_IMAGCOHY) && !(mask & (CS_PLI | CS_USPLI | CS_WPLI | CS_DSWPLI | CS_COHY));
 }
 
+// The fused call (every phase-lag output plus IMAGCOHY and COH, single taper, no COHY):
+// the tensor-core kernel's D_im already is sum Im, so it writes IMAGCOHY and the
+// phase-lag kernel reads it for WPLI's numerator instead of accumulating sum Im in its
+// trial loop (one FADD2 of four FMA-pipe operations per update).  Entries whose
+// per-bin IMAGCOHY comes from the tensor-core kernel (|err| < tau = imag_tau_of); the
+// phase-lag kernel forms its band mean, and its guard-flagged entries -- and those whose
+// sum |Im| is too small for WPLI's numerator error -- are re-folded in fp64 with IMAGCOHY.
+// CSCONN_IMAG_TC=0 turns the hand-off off (A/B).
+static bool imag_handoff(const Plan& p, unsigned mask, int K, const cs_outputs* out) {
+  static const bool off = getenv("CSCONN_IMAG_TC") && getenv("CSCONN_IMAG_TC")[0] == '0';
+  if (off || p.L != 1 || (mask & CS_COHY) || !(mask & CS_COH) || (K + 1) / 2 >= 65536) return false;
+  for (int q = 0; q < 5; ++q)
+    if (!(mask & kLagBits[q]) || !out->bins[kLagIdx[q]] || !out->band[kLagIdx[q]]) return false;
+  return true;
+}
+static float imag_tau_of(int Kc) { return 1e-5f + 6e-8f * (float)Kc; }  // pairs_tc.cu: D_im error / norm
+
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
+  const bool handoff = imag_handoff(p, mask, K, out) && (uint64_t)nbb * (uint64_t)out->pair_stride < (1ull << 32);
   if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
   unsigned any = 0;
   for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
@@ -366,22 +386,27 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     p.rec_cap = n_rec;
   }
   a.recs = p.recs;
-  if (!run_pairs_lag(p, a, n_tiles, st)) return -1;
+  if (handoff) {
+    a.imag_in = (const float*)out->bins[2];
+    a.imag_tau = imag_tau_of(K * p.L);
+  }
+  if (!run_pairs_lag(p, a, n_tiles, st, handoff)) return -1;
   return 2;
 }
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
-                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st);
+                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st, bool handoff);
 
 int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
-  const bool do_imag = imag_on_tensor_cores(mask);
+  const bool handoff = imag_handoff(p, mask, K, out) && (uint64_t)nbb * (uint64_t)out->pair_stride < (1ull << 32);
+  const bool do_imag = imag_on_tensor_cores(mask) || handoff;
   const bool do_x = (mask & (CS_COHY | CS_COH)) != 0 || do_imag;
   const bool do_u = (mask & CS_PLV) != 0 && p.L == 1;  // multitaper PLV runs in the lag kernel
   if (!do_x && !do_u) return 0;
-  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, do_imag, out, p.nscale, st))
+  if (!run_pairs_tc(p, slots, K, bin_lo, nbb, rb, re, do_x, do_u, do_imag, out, p.nscale, st, handoff))
     return -1;
-  if (do_imag && (out->bins[2] || out->band[2])) {  // fp64 values for the near-zero IMAGCOHY entries
+  if (do_imag && !handoff && (out->bins[2] || out->band[2])) {  // fp64 values for the near-zero IMAGCOHY entries
     LagArgs a{};
     a.X64 = p.X64;
     a.N = p.N; a.nb = p.nb; a.L = p.L;

@@ -101,6 +101,8 @@ struct Lag1Args {
   int* counters;
   int flag_cap;
   bool wide;                 // K >= 2^17: sign counts decoded per stage (see neg[] below)
+  const float* imag_in;      // IMAGIN: IMAGCOHY per bin from the tensor-core kernel, [nbb][pair_stride]
+  float imag_tau;            // IMAGIN: its error bound (entries below it went to the fp64 fallback)
 };
 
 // L == 1 uses a dedicated producer warpgroup (20 warps; setmaxnreg gives the 16 compute
@@ -114,7 +116,10 @@ constexpr unsigned kStSign = 1, kStSum = 2, kStAbs = 4, kStAll = 7;
 // epilogue needs no per-store pointer checks.
 // WIDE: K >= 2^17 trials, where the two 16-bit sign-count fields could wrap: the
 // packed counts are decoded into plain 32-bit counters after every stage.
-template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false, bool WIDE = false>
+// IMAGIN: the tensor-core kernel already wrote the per-bin IMAGCOHY for this call (its
+// D_im is sum Im; this kernel still forms the band mean); sum t is not accumulated here -- WPLI's numerator is IMAGCOHY sqrt(psd_i psd_j)
+// -- which takes the FADD2 out of the trial loop (see run_lag_family).
+template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false, bool WIDE = false, bool IMAGIN = false>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
 k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
              const Lag1Args a) {
@@ -145,7 +150,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     bin_mask |= (a.plv_bins != nullptr) << 5;
     band_mask |= (a.plv_band != nullptr) << 5;
   }
-  if (FULL) bin_mask = band_mask = 31u;
+  if (FULL) {  // IMAGIN: the per-bin IMAGCOHY is the tensor-core kernel's, its band mean is summed here
+    bin_mask = IMAGIN ? 30u : 31u;
+    band_mask = 31u;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < k1Stages; ++s) {
       mbar_init(&full[s], 1);
@@ -358,6 +366,19 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     }
     const int64_t bin_off = (int64_t)bl * a.pair_stride;
     unsigned fl = 0;  // exact-sign guard: this thread's entries the fp64 fallback writes
+    float imv[IMAGIN ? k1NP : 1];
+    if (IMAGIN) {  // issued with the node-factor loads above, so their latencies overlap
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) {
+        const int i = iBase + ty + k1TY * r;
+        const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base + bin_off;
+#pragma unroll
+        for (int c = 0; c < k1TC; ++c) {
+          const int j = jBase + tx + k1TX * c;
+          imv[r * k1TC + c] = (i < j && j < a.N) ? __ldcs(&a.imag_in[rowoff + j]) : 0.f;
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < k1TR; ++r) {
       const int li = ty + k1TY * r, i = iBase + li;
@@ -369,10 +390,21 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         const bool valid = (i < j) && (j < a.N);
         // dead: a node with a zero spectrum in this bin (or DC / Nyquist): all Im are 0
         const bool dead = Mi[r] * Mj[c] == 0.f;
-        const bool flagged = valid && !dead && mn[p] <= gMi[r] * Mj[c];
-        fl |= (unsigned)flagged << p;
         const float tph = phI[r] * phJ[c];  // odd-K phantom trial (0 when K is even)
-        const float s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+        float s_im;
+        bool flagged;
+        if (IMAGIN) {
+          const float rr = rPi[r] * rPj[c];
+          s_im = (dead || rr == 0.f) ? 0.f : imv[p] * rcp_approx(rr);
+          // re-folded in fp64 (IMAGCOHY included): a sign within the fp32 guard (this also
+          // catches the reference's exact zeros: every trial's |Im| is below the guard), or a
+          // sum |Im| too small for WPLI's numerator error tau / (rPi rPj)
+          flagged = valid && !dead && (mn[p] <= gMi[r] * Mj[c] || a.imag_tau > 1e-4f * rr * (sabs[p] - tph));
+        } else {
+          s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+          flagged = valid && !dead && mn[p] <= gMi[r] * Mj[c];
+        }
+        fl |= (unsigned)flagged << p;
         const float s_abs = dead ? 0.f : sabs[p] - tph;
         const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
         const int n_neg = WIDE ? (int)negw[p] : L == 1 ? (int)(nA + nB) : (int)neg[p];
@@ -454,7 +486,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
-                 int L, float* plv_bins, float* plv_band, cudaStream_t st) {
+                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -489,6 +521,8 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   a.g = g; a.flags = flags; a.recs = recs; a.counters = counters; a.flag_cap = flag_cap;
   a.plv_bins = plv_bins;
   a.plv_band = plv_band;
+  a.imag_in = imag_in;
+  a.imag_tau = imag_tau;
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
   const unsigned grid = (unsigned)(n_tiles * nbc);
   const bool plvk = plv_bins || plv_band;
@@ -502,7 +536,10 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     CS_SMEM_ONCE((k_pairs_lag1<LL, PV>), smem);                                                         \
     k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);         \
   } while (0)
-  if (L == 1 && Kp >= 65536) {  // a 16-bit sign-count field could wrap: per-stage decode
+  if (imag_in) {  // the fused call with IMAGCOHY from the tensor cores (run_lag_family checked the shape)
+    CS_SMEM_ONCE((k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true>), smem);
+    k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
+  } else if (L == 1 && Kp >= 65536) {  // a 16-bit sign-count field could wrap: per-stage decode
     CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, false, true>), smem);
     k_pairs_lag1<1, false, kStAll, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
   } else if (L == 1) {

@@ -665,7 +665,7 @@ const int2* tc_tile_list(Plan& p, int i_lo, int i_hi, int nt64, int64_t* n_tiles
 }
 
 bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
-                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st) {
+                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st, bool handoff) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -748,9 +748,10 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.plv_bins = do_u ? (float*)out->bins[3] : nullptr;
   a.plv_band = do_u ? (float*)out->band[3] : nullptr;
   a.imag_bins = do_imag ? (float*)out->bins[2] : nullptr;
-  a.imag_band = do_imag ? (float*)out->band[2] : nullptr;
+  // hand-off: per-bin IMAGCOHY only (the phase-lag kernel forms the band mean and flags)
+  a.imag_band = do_imag && !handoff ? (float*)out->band[2] : nullptr;
   a.do_x = do_x; a.do_u = do_u;
-  if (do_imag && (a.imag_bins || a.imag_band)) {
+  if (do_imag && !handoff && (a.imag_bins || a.imag_band)) {
     a.flags = p.flags;
     a.counters = p.counters;
     a.flag_cap = p.flag_cap;
