@@ -451,12 +451,16 @@ def main():
         upd = P_loc * c.n_bins * c.K
         L_k3 = 1 if not isinstance(c.taper, tuple) else c.taper[2]
         plv_k3 = L_k3 > 1 and "PLV" in metrics
-        w_upd = 2 * L_k3 + 2 + ((2 * L_k3 + 4) if plv_k3 else 0)
+        # IMAGCOHY hand-off (cs_last_imag_handoff): sum t comes from the tensor-core D_im
+        handoff = full.guard_stats()["imag_handoff"]
+        w_upd = 2 * L_k3 + (1 if handoff else 2) + ((2 * L_k3 + 4) if plv_k3 else 0)
         ach = w_upd * upd / (lag_ms * 1e-3)
         roof_k3 = {"kernel": "k_pairs_lag", "bound": "fp32", "achieved": ach / 1e12, "peak": fp32_ops / 1e12,
                 "unit": "T FP32-pipe lane-ops/s", "frac": ach / fp32_ops, "traffic": None,
                 "peak_source": "measured live on this GPU by cs_probe_peaks (dependent FFMA chains)",
-                "work_per_update": (f"{w_upd} FP32 lane-ops: t over {L_k3} taper(s) {2 * L_k3}, sum t 1, sum |t| 1"
+                "work_per_update": (f"{w_upd} FP32 lane-ops: t over {L_k3} taper(s) {2 * L_k3}, "
+                                    + ("sum |t| 1 (sum t: IMAGCOHY hand-off from k_pairs_tc)" if handoff
+                                       else "sum t 1, sum |t| 1")
                                     + (f", multitaper PLV {2 * L_k3 + 4}" if plv_k3 else ""))}
     if per.get(spec_key, 0.0) > 0:
         k1_ms = per[spec_key]

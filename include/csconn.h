@@ -210,6 +210,10 @@ int cs_last_fallback_count(cs_plan* plan, void* stream, int64_t* n_flagged);
 int cs_last_guard_stats(cs_plan* plan, void* stream, int64_t* n_flagged, int64_t* n_records);
 int64_t cs_fft_call_count(const cs_plan* plan);
 void cs_reset_fft_call_count(cs_plan* plan);
+/* 1 when the last cs_pair_metrics call took the IMAGCOHY hand-off (the tensor-core
+ * kernel's per-bin IMAGCOHY read by the phase-lag kernel in place of its own sum of
+ * Im), else 0.  Instrumentation: the bench's work count. */
+int cs_last_imag_handoff(const cs_plan* plan);
 
 /* Instrumentation (bench evidence): CUDA events around every kernel phase on
  * the launching stream; cs_profile_read returns "name:total_ms:count;..." and

@@ -68,6 +68,8 @@ def lib():
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cs_last_fallback_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
     L.cs_last_guard_stats.argtypes = [vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.cs_last_imag_handoff.argtypes = [vp]
+    L.cs_last_imag_handoff.restype = ctypes.c_int
     L.cs_fft_call_count.argtypes = [vp]
     L.cs_fft_call_count.restype = i64
     L.cs_reset_fft_call_count.argtypes = [vp]
@@ -101,7 +103,7 @@ CS_PM_REUSE_PREP = 1
 
 EXPORTED = ("cs_plan_create", "cs_plan_destroy", "cs_spectra", "cs_pair_metrics", "cs_pair_metrics_ex", "cs_pair_sums",
             "cs_get_spectra", "cs_put_spectra", "cs_put_taper_spectra", "cs_net_normalize", "cs_net_threshold", "cs_cor_sums", "cs_xcor_sums", "cs_apply_inverse", "cs_project_ring", "cs_fir_apply",
-            "cs_window_create", "cs_window_destroy", "cs_window_reset", "cs_window_update", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count", "cs_last_guard_stats",
+            "cs_window_create", "cs_window_destroy", "cs_window_reset", "cs_window_update", "cs_plan_k1_kind", "cs_num_row_tiles", "cs_row_tile_range", "cs_last_fallback_count", "cs_last_guard_stats", "cs_last_imag_handoff",
             "cs_fft_call_count", "cs_reset_fft_call_count", "cs_plan_set_profiling", "cs_profile_read",
             "cs_launch_count", "cs_ring_view", "cs_spectra_nodes", "cs_ring_export", "cs_ring_attach",
             "cs_ring_attach_ptrs", "cs_ring_push", "cs_probe_peaks", "cs_last_error", "cs_version")

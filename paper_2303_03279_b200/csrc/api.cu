@@ -423,6 +423,7 @@ int cs_pair_metrics_ex(cs_plan* p, const int* slots, int K, unsigned mask, int b
     if (!(mask & (1u << m))) o.bins[m] = o.band[m] = nullptr;
   // tensor-core family (COHY, COH, PLV; IMAGCOHY when no sign-based metric is asked),
   // then the phase-lag family
+  p->imag_handoff = false;
   const int rc1 = cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
   const int rc2 = rc1 < 0 ? -1 : cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
   p->reuse_prep = false;
@@ -531,6 +532,7 @@ int cs_ring_view(cs_plan* p, void** x64, void** x32, int64_t* n_elems) {
 }
 
 int64_t cs_fft_call_count(const cs_plan* p) { return p ? p->fft_calls : 0; }
+int cs_last_imag_handoff(const cs_plan* p) { return p && p->imag_handoff ? 1 : 0; }
 
 int cs_plan_k1_kind(const cs_plan* p) {
   if (!p) return -1;

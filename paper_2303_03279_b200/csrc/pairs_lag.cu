@@ -306,9 +306,10 @@ static bool imag_on_tensor_cores(unsigned mask) {
 // phase-lag kernel forms its band mean, and its guard-flagged entries -- and those whose
 // sum |Im| is too small for WPLI's numerator error -- are re-folded in fp64 with IMAGCOHY.
 // CSCONN_IMAG_TC=0 turns the hand-off off (A/B).
-static bool imag_handoff(const Plan& p, unsigned mask, int K, const cs_outputs* out) {
+static bool imag_handoff(const Plan& p, unsigned mask, int K, int nbb, const cs_outputs* out) {
   static const bool off = getenv("CSCONN_IMAG_TC") && getenv("CSCONN_IMAG_TC")[0] == '0';
   if (off || p.L != 1 || (mask & CS_COHY) || !(mask & CS_COH) || (K + 1) / 2 >= 65536) return false;
+  if ((uint64_t)nbb * (uint64_t)out->pair_stride >= (1ull << 32)) return false;  // the FULL kernel's 32-bit offsets
   for (int q = 0; q < 5; ++q)
     if (!(mask & kLagBits[q]) || !out->bins[kLagIdx[q]] || !out->band[kLagIdx[q]]) return false;
   return true;
@@ -317,7 +318,7 @@ static float imag_tau_of(int Kc) { return 1e-5f + 6e-8f * (float)Kc; }  // pairs
 
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
-  const bool handoff = imag_handoff(p, mask, K, out) && (uint64_t)nbb * (uint64_t)out->pair_stride < (1ull << 32);
+  const bool handoff = imag_handoff(p, mask, K, nbb, out);
   if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
   unsigned any = 0;
   for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
@@ -399,7 +400,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
 
 int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st) {
-  const bool handoff = imag_handoff(p, mask, K, out) && (uint64_t)nbb * (uint64_t)out->pair_stride < (1ull << 32);
+  const bool handoff = imag_handoff(p, mask, K, nbb, out);
+  p.imag_handoff = handoff;
   const bool do_imag = imag_on_tensor_cores(mask) || handoff;
   const bool do_x = (mask & (CS_COHY | CS_COH)) != 0 || do_imag;
   const bool do_u = (mask & CS_PLV) != 0 && p.L == 1;  // multitaper PLV runs in the lag kernel

@@ -221,7 +221,8 @@ class DevicePlan:
         the overflow records used when the work list was full (none is ever dropped)."""
         n, r = ctypes.c_int64(), ctypes.c_int64()
         _lib.check(_lib.lib().cs_last_guard_stats(self._h, _stream_ptr(stream), ctypes.byref(n), ctypes.byref(r)))
-        return {"flagged": int(n.value), "records": int(r.value)}
+        return {"flagged": int(n.value), "records": int(r.value),
+                "imag_handoff": bool(_lib.lib().cs_last_imag_handoff(self._h))}
 
     def get_spectra(self, slots: torch.Tensor, bin_lo: int = 0, n_bins: int | None = None, stream=None):
         if n_bins is None:

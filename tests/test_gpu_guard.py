@@ -74,6 +74,7 @@ def test_guard_at_baseline_scale_no_exclusions(cfg5_sub):
     n_upd = x.shape[1] * (x.shape[1] - 1) // 2 * c.n_bins * c.K
     assert n_upd >= 3e8
     assert st["flagged"] > 0, "the guard was never exercised"
+    assert st["imag_handoff"], "the fused seven-metric call takes the IMAGCOHY hand-off"
     _compare_all(c, out, want, c.K, c.metrics)
 
 
@@ -131,7 +132,27 @@ def test_guard_list_overflow_through_compute_metric():
     assert np.all(out["WPLI"]["bins"].T.cpu().numpy()[zl] == 0.0)
 
 
-@pytest.mark.parametrize("metrics", [("PLI", "USPLI", "WPLI", "DSWPLI", "IMAGCOHY"), ("PLI",), ("WPLI",)])
+def test_imag_handoff_exact_zeros_and_overflow():
+    """The fused seven-metric call: per-bin IMAGCOHY from the tensor-core kernel, the
+    phase-lag kernel reads it; zero-lag copies (guard-flagged, > the list capacity) get
+    the reference's exact zeros for IMAGCOHY as well, and every entry matches."""
+    K, N, T, nfft, lo, hi = 30, 400, 256, 256, 10, 109
+    x = _zero_lag_epochs(K, N, T)
+    out, plan = compute_connectivity(torch.tensor(x, device="cuda"), nfft, lo, hi, metrics=SEVEN)
+    st = plan.guard_stats()
+    assert st["imag_handoff"] and st["records"] > 0, st
+    want, _ = O.compute(list(x), nfft, lo, hi, SEVEN)
+    _compare_all(None, out, want, K, SEVEN)
+    i, j = np.triu_indices(N, 1)
+    zl = (i <= 80) & (j <= 80)
+    for m in ("IMAGCOHY", "PLI", "WPLI"):
+        assert np.all(out[m]["bins"].T.cpu().numpy()[zl] == 0.0), m
+
+
+SEVEN = ("COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI")
+
+
+@pytest.mark.parametrize("metrics", [("PLI", "USPLI", "WPLI", "DSWPLI", "IMAGCOHY"), ("PLI",), ("WPLI",), SEVEN])
 def test_guard_forced_tiny_list(metrics):
     """A 16-entry work list (CSCONN_FLAG_CAP, read at plan creation): nearly every
     flagged entry goes through an overflow record; outputs still match exactly."""
@@ -146,6 +167,7 @@ def test_guard_forced_tiny_list(metrics):
     finally:
         del os.environ["CSCONN_FLAG_CAP"]
     assert st["records"] > 0, st
+    assert st["imag_handoff"] == (metrics == SEVEN), st
     want, _ = O.compute(list(x), nfft, lo, hi, metrics, taper=np.hanning(T))
     _compare_all(None, out, want, K, metrics)
 
