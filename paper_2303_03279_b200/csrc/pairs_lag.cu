@@ -56,6 +56,7 @@ struct LagArgs {
   int node_block;
   const float* imag_in;    // hand-off: IMAGCOHY per bin from the tensor-core kernel (else null)
   float imag_tau;
+  float4* nf;              // [nbb][N64] node factors of the phase-lag epilogue (k_lag_prep)
 };
 
 // Trial-pair packing of the selected trials (k = 2 kp, 2 kp + 1) into the layouts the
@@ -66,11 +67,26 @@ struct LagArgs {
 constexpr float kPhantom = 9.765625e-4f;  // 2^-10
 __global__ void k_lag_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int Kp,
                            int N, int N64, int nb, int L, int bin_lo, const float* __restrict__ mag,
-                           float4* __restrict__ PkI, float4* __restrict__ PkJ) {
+                           const float* __restrict__ psd, int real0, int real1, float g,
+                           float4* __restrict__ PkI, float4* __restrict__ PkJ, float4* __restrict__ nf) {
   // layout [bl][kp][l][n]: taper l of trial pair kp
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int bl = blockIdx.z;
   if (n >= N64) return;
+  if (blockIdx.y == 0) {
+    // per-node epilogue factors {M', g M', 1/sqrt(psd), M' 2^-10}; M' = 0 on exactly-real
+    // bins (all Im exactly 0: dead pairs), zeros past N
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n < N) {
+      const int b = bin_lo + bl;
+      const float m = (b == real0 || b == real1) ? 0.f : mag[(int64_t)bl * N + n];
+      const float pw = psd[(int64_t)bl * N + n];
+      float rp = 0.f;
+      if (pw > 0.f) asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rp) : "f"(pw));
+      f = make_float4(m, g * m, rp, m * kPhantom);
+    }
+    nf[(int64_t)bl * N64 + n] = f;
+  }
   for (int y = blockIdx.y; y < Kp * L; y += gridDim.y) {  // grid.y <= 65535 (very long sessions)
   const int kp = y / L, l = y % L;
   float2 va = make_float2(0.f, 0.f), vb = make_float2(0.f, 0.f);
@@ -226,15 +242,16 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
-                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, cudaStream_t st);
+                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, const float4* nf,
+                 cudaStream_t st);
 
 bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, bool handoff) {
   cudaMemsetAsync(a.counters, 0, 3 * sizeof(int), st);
   if (!p.reuse_prep) {
     PhaseMark ph(p, "lag_prep", st);
     dim3 grid((a.N64 + 127) / 128, a.Kp * a.L < 65535 ? a.Kp * a.L : 65535, a.nbb);
-    k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag,
-                                     (float4*)a.PkI, (float4*)a.PkJ);
+    k_lag_prep<<<grid, 128, 0, st>>>(p.X32, a.slots, a.K, a.Kp, a.N, a.N64, a.nb, a.L, a.bin_lo, a.mag, a.psd,
+                                     a.real0, a.real1, a.g, (float4*)a.PkI, (float4*)a.PkJ, a.nf);
   }
   {
     PhaseMark ph(p, "pairs_lag", st);
@@ -269,7 +286,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, 
     }
     if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
                      a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.recs, a.counters, a.flag_cap,
-                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, a.imag_in, a.imag_tau, st))
+                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, a.imag_in, a.imag_tau, a.nf, st))
       return false;
   }
   {
@@ -309,7 +326,7 @@ static bool imag_on_tensor_cores(unsigned mask) {
 static bool imag_handoff(const Plan& p, unsigned mask, int K, int nbb, const cs_outputs* out) {
   static const bool off = getenv("CSCONN_IMAG_TC") && getenv("CSCONN_IMAG_TC")[0] == '0';
   if (off || p.L != 1 || (mask & CS_COHY) || !(mask & CS_COH) || (K + 1) / 2 >= 65536) return false;
-  if ((uint64_t)nbb * (uint64_t)out->pair_stride >= (1ull << 32)) return false;  // the FULL kernel's 32-bit offsets
+  if ((uint64_t)nbb * (uint64_t)out->pair_stride + kTile >= (1ull << 32)) return false;  // FULL kernel's 32-bit offsets
   for (int q = 0; q < 5; ++q)
     if (!(mask & kLagBits[q]) || !out->bins[kLagIdx[q]] || !out->band[kLagIdx[q]]) return false;
   return true;
@@ -336,7 +353,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.slots = slots; a.K = K;
   a.Kp = (K + 1) / 2;
   {
-    const size_t need = (size_t)2 * nbb * a.Kp * p.L * a.N64 * sizeof(float4);
+    const size_t need = (size_t)(2 * nbb * a.Kp * p.L + nbb) * a.N64 * sizeof(float4);
     if (need > p.lag_bytes) {
       if (p.lag_ops) cudaFreeAsync(p.lag_ops, st);
       if (cudaMallocAsync(&p.lag_ops, need, st) != cudaSuccess) {
@@ -349,6 +366,7 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
     }
     a.PkI = (const float4*)p.lag_ops;
     a.PkJ = a.PkI + (size_t)nbb * a.Kp * p.L * a.N64;
+    a.nf = (float4*)a.PkJ + (size_t)nbb * a.Kp * p.L * a.N64;
   }
   a.bin_lo = bin_lo; a.nbb = nbb;
   a.psd = p.psd; a.mag = p.mag;

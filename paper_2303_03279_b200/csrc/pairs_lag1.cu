@@ -84,6 +84,13 @@ __device__ __noinline__ void guard_push(int4* flags, int4* recs, int* counters, 
 static_assert(k1NP == 8 && k1Warps == kGuardWarps && k1TY == kGuardRowStep && k1TX == kGuardColStep && k1TC == kGuardTC,
               "guard record layout (common.cuh)");
 
+// first pair index of row i minus one, i (N - 1) - i (i - 1) / 2 - i - 1, mod 2^32: the FULL
+// path's per-bin offsets are host-checked < 2^32, so unsigned wrap-around is exact
+__device__ __forceinline__ uint32_t row_off32(uint32_t i, uint32_t N) {
+  const uint32_t tri = (i & 1u) ? i * ((i - 1u) >> 1) : (i >> 1) * (i - 1u);
+  return i * (N - 1u) - tri - i - 1u;
+}
+
 struct Lag1Args {
   int N, N64, K, Kp, bin_lo, nbb;
   int bpc, nbc;              // bins per CTA, bin chunks per tile (small pair spaces split bins)
@@ -103,6 +110,8 @@ struct Lag1Args {
   bool wide;                 // K >= 2^17: sign counts decoded per stage (see neg[] below)
   const float* imag_in;      // IMAGIN: IMAGCOHY per bin from the tensor-core kernel, [nbb][pair_stride]
   float imag_tau;            // IMAGIN: its error bound (entries below it went to the fp64 fallback)
+  const float4* nf;          // [nbb][N64] node factors {M', g M', rsqrt(psd), M' 2^-10} (k_lag_prep;
+                             // M' = 0 on exactly-real bins): the FULL epilogue's per-node inputs
 };
 
 // L == 1 uses a dedicated producer warpgroup (20 warps; setmaxnreg gives the 16 compute
@@ -129,7 +138,15 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   float4* XI = (float4*)lag1_smem;                       // [stages][KC][64]
   float4* XJ = XI + k1Stages * k1StageF4;                // [stages][KC][64]
   float* band_s = (float*)(XJ + k1Stages * k1StageF4);   // [NM][64][64]
-  uint64_t* full = (uint64_t*)(band_s + 6 * kTile * kTile);
+  // FULL single-taper epilogue (kF): band_s holds per-thread band sums instead, float4
+  // [metric][pair half][compute thread] (80 KB), then IMAGCOHY staging [pair][thread]
+  // (16 KB); nf_s: the bin's node factors [bin % 3][I 64 | J 64], bulk-copied by the
+  // producer with the bin's last stage
+  constexpr bool kF = FULL && L == 1;
+  float4* band4 = (float4*)band_s;
+  float* imv_s = band_s + 5 * kTile * kTile;
+  float4* nf_s = (float4*)(band_s + 6 * kTile * kTile);
+  uint64_t* full = (uint64_t*)(nf_s + 3 * 2 * kTile);
   uint64_t* empty = full + k1Stages;
 
   int I, J;
@@ -194,9 +211,15 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           mbar_wait_backoff(&empty[s], ((t / k1Stages) & 1) ^ 1);
           const int bl = bl0 + t / n_stage, st = t % n_stage;
           const int row = (bl * a.Kp + st * kc) * L;
-          mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16);
+          const bool nf_now = kF && st == n_stage - 1;  // the bin's node factors ride on its last stage
+          mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16 + (nf_now ? 2 * kTile * 16 : 0));
           tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
           tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
+          if (nf_now) {
+            float4* dst = nf_s + (bl % 3) * 2 * kTile;
+            bulk_load_1d(dst, a.nf + (int64_t)bl * a.N64 + iBase, kTile * 16, &full[s]);
+            bulk_load_1d(dst + kTile, a.nf + (int64_t)bl * a.N64 + jBase, kTile * 16, &full[s]);
+          }
         }
       return;
     }
@@ -239,6 +262,21 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       ++bl;
     }
     const int s = t % k1Stages;
+    if (kF && IMAGIN && st == n_stage - 1) {
+      // the bin's tensor-core IMAGCOHY of this thread's pairs, copied while the last stage runs
+      const uint32_t bin_off = (uint32_t)bl * (uint32_t)a.pair_stride;
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) {
+        const uint32_t i = (uint32_t)(iBase + ty + k1TY * r);
+        const uint32_t ro = row_off32(i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off;
+#pragma unroll
+        for (int c = 0; c < k1TC; ++c) {
+          const int j = jBase + tx + k1TX * c;
+          if ((int)i < j && j < a.N)
+            cp_async_4(smem_u32(imv_s + (r * k1TC + c) * k1Threads + tid), a.imag_in + (ro + (uint32_t)j));
+        }
+      }
+    }
     mbar_wait(&full[s], (t / k1Stages) & 1);
     const float4* sI = XI + s * k1StageF4;
     const float4* sJ = XJ + s * k1StageF4;
@@ -338,6 +376,87 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (st + 1 < n_stage) continue;
+
+    if constexpr (kF) {
+      // ---- FULL epilogue for bin bl: node factors and IMAGCOHY already staged in shared
+      // memory, 32-bit per-bin offsets, one store address per (row, metric) (the c = 1 pair is
+      // +32 floats), band sums in this thread's own float4 slots, predicated stores
+      const float4* nfs = nf_s + (bl % 3) * 2 * kTile;
+      float4 fI[k1TR], fJ[k1TC];  // {M', g M', rsqrt(psd), M' 2^-10}
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) fI[r] = nfs[ty + k1TY * r];
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c) fJ[c] = nfs[kTile + tx + k1TX * c];
+      if (IMAGIN) cp_async_wait_all();
+      const uint32_t bin_off = (uint32_t)bl * (uint32_t)a.pair_stride;
+      unsigned fl = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // pairs 4h .. 4h + 3: rows r = 2h, 2h + 1
+        float bsum[5][4];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const float4 q = band4[(m * 2 + h) * k1Threads + tid];
+          bsum[m][0] = q.x; bsum[m][1] = q.y; bsum[m][2] = q.z; bsum[m][3] = q.w;
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int r = 2 * h + rr;
+          const int i = iBase + ty + k1TY * r;
+          // offset of the c = 1 pair (i, jBase + tx + 32): exact whenever either pair is valid
+          // (the c = 0 offset wraps below 0 for i = 0, tx = 0); c = 0 stores at -32 floats
+          const uint32_t ro = row_off32((uint32_t)i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off +
+                              (uint32_t)(jBase + tx + k1TX);
+          float* pb[5];
+#pragma unroll
+          for (int m = IMAGIN ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
+          const float phI = odd ? fI[r].w : 0.f;
+#pragma unroll
+          for (int c = 0; c < k1TC; ++c) {
+            const int p = r * k1TC + c;
+            const int j = jBase + tx + k1TX * c;
+            const bool valid = (i < j) && (j < a.N);
+            const bool dead = fI[r].x * fJ[c].x == 0.f;
+            const float tph = phI * fJ[c].w;
+            const float rr2 = fI[r].z * fJ[c].z;
+            const float s_abs = dead ? 0.f : sabs[p] - tph;
+            float s_im, v0;
+            bool flagged;
+            if (IMAGIN) {
+              const float im = imv_s[p * k1Threads + tid];
+              s_im = (dead || rr2 == 0.f) ? 0.f : im * rcp_approx(rr2);
+              v0 = dead ? 0.f : im;
+              flagged = valid && !dead && (mn[p] <= fI[r].y * fJ[c].x || a.imag_tau > 1e-4f * rr2 * s_abs);
+            } else {
+              s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+              v0 = s_im * rr2;
+              flagged = valid && !dead && mn[p] <= fI[r].y * fJ[c].x;
+            }
+            fl |= (unsigned)flagged << p;
+            const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
+            const int pli_sum = dead ? 0 : a.K - 2 * (int)(nA + nB);
+            const float pli = fabsf((float)pli_sum) * invK;
+            const float w = s_abs > 0.f ? fminf(fabsf(s_im) * rcp_approx(s_abs), 1.f) : 0.f;
+            const float v[5] = {v0, pli, pli * pli * uspA - uspB, w, w * w};
+            const bool ok = valid && !flagged;
+#pragma unroll
+            for (int m = 0; m < 5; ++m) {
+              if (m > 0 || !IMAGIN)
+                if (ok) __stcs(pb[m] - k1TX * (1 - c), v[m]);  // streaming: keep the operands in L2
+              bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
+            }
+            sim[p] = 0ull;
+            sabs[p] = 0.f;
+            mn[p] = 3.0e38f;
+            neg[p] = 0u;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < 5; ++m)
+          band4[(m * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
+      }
+      if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
+      continue;
+    }
 
     // ---- epilogue for bin bl ----
     // per-node factors first (6 nodes per thread), then ~30 instructions per pair
@@ -451,7 +570,32 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
   }
 
-  if (band_mask) {
+  if (kF) {
+    // FULL: each thread writes its own band sums (no barrier); per (row, column half)
+    // a warp covers 32 contiguous pair columns
+    const float inv = 1.f / (float)a.nbb;
+#pragma unroll
+    for (int r = 0; r < k1TR; ++r) {
+      const int i = iBase + ty + k1TY * r;
+      const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const float4 q = band4[(m * 2 + r / 2) * k1Threads + tid];
+#pragma unroll
+        for (int c = 0; c < k1TC; ++c) {
+          const int j = jBase + tx + k1TX * c;
+          const int e = (r % 2) * 2 + c;
+          const float v = (e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w) * inv;
+          if (i < j && j < a.N) {
+            if (a.nbc > 1)
+              atomicAdd(a.band[m] + rowoff + j, v);  // bins split over CTAs: band zeroed by the host
+            else
+              __stcs(a.band[m] + rowoff + j, v);
+          }
+        }
+      }
+    }
+  } else if (band_mask) {
     // band write-out by rows: the compute warps' band slots are complete after one
     // named barrier (the producer warp has left); warp w writes rows w, w + 16, ...
     // of every requested metric, lanes over 64 contiguous pair columns.
@@ -486,7 +630,8 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  const float* psd, const float* mag, int real0, int real1, int nt, int row_begin,
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
-                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, cudaStream_t st) {
+                 int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, const float4* nf,
+                 cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -523,7 +668,9 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   a.plv_band = plv_band;
   a.imag_in = imag_in;
   a.imag_tau = imag_tau;
-  const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 2 * k1Stages * 8;
+  a.nf = nf;
+  const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 3 * 2 * kTile * 16 +
+                     2 * k1Stages * 8;
   const unsigned grid = (unsigned)(n_tiles * nbc);
   const bool plvk = plv_bins || plv_band;
 #define CS_LAG1S(LL, PV, SS)                                                                           \
@@ -553,7 +700,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
       case kStSign | kStSum: CS_LAG1S(1, false, kStSign | kStSum); break;
       case kStSum | kStAbs: CS_LAG1S(1, false, kStSum | kStAbs); break;
       default: {
-        bool full = (uint64_t)nbb * (uint64_t)pair_stride < (1ull << 32);  // 32-bit per-bin offsets
+        bool full = (uint64_t)nbb * (uint64_t)pair_stride + kTile < (1ull << 32);  // 32-bit per-bin offsets
         for (int m = 0; m < 5; ++m) full = full && bins[m] && band[m];
         if (full) {
           CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, true>), smem);
