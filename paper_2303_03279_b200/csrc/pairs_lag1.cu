@@ -14,6 +14,8 @@
 // Per trial pair and pair of nodes: FMUL2 + FFMA2 (t = Im X_i conj X_j for two
 // trials), FADD2 (sum t), 2 FADD |.| (sum |t|), 2 LEA.HI (#(t < 0)), FMNMX3
 // (min |t|, the exact-sign guard of pairs_lag.cu).
+#include <type_traits>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -156,6 +158,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   const int nbl = min(a.bpc, a.nbb - bl0);
   const int iBase = I * kTile, jBase = J * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool interior = iBase + kTile <= jBase && jBase + kTile <= a.N;  // every i < j < N
 
   unsigned bin_mask = 0, band_mask = 0;
 #pragma unroll
@@ -389,71 +392,86 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       for (int c = 0; c < k1TC; ++c) fJ[c] = nfs[kTile + tx + k1TX * c];
       if (IMAGIN) cp_async_wait_all();
       const uint32_t bin_off = (uint32_t)bl * (uint32_t)a.pair_stride;
+      const float tau = IMAGIN ? a.imag_tau : 0.f;
       unsigned fl = 0;
+      // kFast: an interior tile (every i < j < N) whose nodes all have non-zero spectra in
+      // this bin (warp-uniform): no validity or dead-node predicates per pair
+      auto pairs = [&](auto fast_tag) {
+        constexpr bool kFast = decltype(fast_tag)::value;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // pairs 4h .. 4h + 3: rows r = 2h, 2h + 1
-        float bsum[5][4];
+        for (int h = 0; h < 2; ++h) {  // pairs 4h .. 4h + 3: rows r = 2h, 2h + 1
+          float bsum[5][4];
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const float4 q = band4[(m * 2 + h) * k1Threads + tid];
-          bsum[m][0] = q.x; bsum[m][1] = q.y; bsum[m][2] = q.z; bsum[m][3] = q.w;
-        }
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int r = 2 * h + rr;
-          const int i = iBase + ty + k1TY * r;
-          // offset of the c = 1 pair (i, jBase + tx + 32): exact whenever either pair is valid
-          // (the c = 0 offset wraps below 0 for i = 0, tx = 0); c = 0 stores at -32 floats
-          const uint32_t ro = row_off32((uint32_t)i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off +
-                              (uint32_t)(jBase + tx + k1TX);
-          float* pb[5];
-#pragma unroll
-          for (int m = IMAGIN ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
-          const float phI = odd ? fI[r].w : 0.f;
-#pragma unroll
-          for (int c = 0; c < k1TC; ++c) {
-            const int p = r * k1TC + c;
-            const int j = jBase + tx + k1TX * c;
-            const bool valid = (i < j) && (j < a.N);
-            const bool dead = fI[r].x * fJ[c].x == 0.f;
-            const float tph = phI * fJ[c].w;
-            const float rr2 = fI[r].z * fJ[c].z;
-            const float s_abs = dead ? 0.f : sabs[p] - tph;
-            float s_im, v0;
-            bool flagged;
-            if (IMAGIN) {
-              const float im = imv_s[p * k1Threads + tid];
-              s_im = (dead || rr2 == 0.f) ? 0.f : im * rcp_approx(rr2);
-              v0 = dead ? 0.f : im;
-              flagged = valid && !dead && (mn[p] <= fI[r].y * fJ[c].x || a.imag_tau > 1e-4f * rr2 * s_abs);
-            } else {
-              s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
-              v0 = s_im * rr2;
-              flagged = valid && !dead && mn[p] <= fI[r].y * fJ[c].x;
-            }
-            fl |= (unsigned)flagged << p;
-            const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
-            const int pli_sum = dead ? 0 : a.K - 2 * (int)(nA + nB);
-            const float pli = fabsf((float)pli_sum) * invK;
-            const float w = s_abs > 0.f ? fminf(fabsf(s_im) * rcp_approx(s_abs), 1.f) : 0.f;
-            const float v[5] = {v0, pli, pli * pli * uspA - uspB, w, w * w};
-            const bool ok = valid && !flagged;
-#pragma unroll
-            for (int m = 0; m < 5; ++m) {
-              if (m > 0 || !IMAGIN)
-                if (ok) __stcs(pb[m] - k1TX * (1 - c), v[m]);  // streaming: keep the operands in L2
-              bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
-            }
-            sim[p] = 0ull;
-            sabs[p] = 0.f;
-            mn[p] = 3.0e38f;
-            neg[p] = 0u;
+          for (int m = 0; m < 5; ++m) {
+            const float4 q = band4[(m * 2 + h) * k1Threads + tid];
+            bsum[m][0] = q.x; bsum[m][1] = q.y; bsum[m][2] = q.z; bsum[m][3] = q.w;
           }
-        }
 #pragma unroll
-        for (int m = 0; m < 5; ++m)
-          band4[(m * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
-      }
+          for (int rr = 0; rr < 2; ++rr) {
+            const int r = 2 * h + rr;
+            const int i = iBase + ty + k1TY * r;
+            // offset of the c = 1 pair (i, jBase + tx + 32): exact whenever either pair is valid
+            // (the c = 0 offset wraps below 0 for i = 0, tx = 0); c = 0 stores at -32 floats
+            const uint32_t ro = row_off32((uint32_t)i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off +
+                                (uint32_t)(jBase + tx + k1TX);
+            float* pb[5];
+#pragma unroll
+            for (int m = IMAGIN ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
+            const float phI = odd ? fI[r].w : 0.f;
+#pragma unroll
+            for (int c = 0; c < k1TC; ++c) {
+              const int p = r * k1TC + c;
+              const int j = jBase + tx + k1TX * c;
+              const bool valid = kFast || ((i < j) && (j < a.N));
+              const bool dead = !kFast && fI[r].x * fJ[c].x == 0.f;
+              const float tph = phI * fJ[c].w;
+              const float rr2 = fI[r].z * fJ[c].z;
+              const float s_abs = dead ? 0.f : sabs[p] - tph;
+              float s_im, v0;
+              bool flagged;
+              if (IMAGIN) {
+                const float im = imv_s[p * k1Threads + tid];
+                s_im = (dead || (!kFast && rr2 == 0.f)) ? 0.f : im * rcp_approx(rr2);
+                v0 = dead ? 0.f : im;
+                flagged = valid && !dead && (mn[p] <= fI[r].y * fJ[c].x || tau > 1e-4f * rr2 * s_abs);
+              } else {
+                s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
+                v0 = s_im * rr2;
+                flagged = valid && !dead && mn[p] <= fI[r].y * fJ[c].x;
+              }
+              fl |= (unsigned)flagged << p;
+              const unsigned nA = (0u - neg[p]) & 0xFFFFu, nB = ((65535u * nA - neg[p]) >> 16) & 0xFFFFu;
+              const int pli_sum = dead ? 0 : a.K - 2 * (int)(nA + nB);
+              const float pli = fabsf((float)pli_sum) * invK;
+              const float w = s_abs > 0.f ? fminf(fabsf(s_im) * rcp_approx(s_abs), 1.f) : 0.f;
+              const float v[5] = {v0, pli, pli * pli * uspA - uspB, w, w * w};
+              const bool ok = valid && !flagged;
+#pragma unroll
+              for (int m = 0; m < 5; ++m) {
+                if (m > 0 || !IMAGIN)
+                  if (ok) __stcs(pb[m] - k1TX * (1 - c), v[m]);  // streaming: keep the operands in L2
+                bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
+              }
+              sim[p] = 0ull;
+              sabs[p] = 0.f;
+              mn[p] = 3.0e38f;
+              neg[p] = 0u;
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < 5; ++m)
+            band4[(m * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
+        }
+      };
+      bool fast = interior;
+#pragma unroll
+      for (int r = 0; r < k1TR; ++r) fast = fast && fI[r].x != 0.f;
+#pragma unroll
+      for (int c = 0; c < k1TC; ++c) fast = fast && fJ[c].x != 0.f;
+      if (__all_sync(0xffffffffu, fast))
+        pairs(std::true_type{});
+      else
+        pairs(std::false_type{});
       if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
       continue;
     }
