@@ -28,6 +28,18 @@
 
 namespace cs {
 
+// outputs of the tensor-core part of the fused call (pairs_lag1.cu FU): the fp16
+// split operands (k_tc_prep) and the COH / PLV per-bin and band arrays
+struct FusedOut {
+  const void* G;
+  int K_pad;
+  float* coh_bins;
+  float* coh_band;
+  float* plv_bins;
+  float* plv_band;
+  const int2* tiles;  // grouped tile order (pairs_tc.cu tile_list)
+};
+
 constexpr int kTile = 64;        // node tile edge of the upper-triangular pair tiling
 constexpr int kThreads = 256;    // pair-kernel CTA size (16 x 16 threads, 4 x 4 pairs each)
 // exact-sign guard overflow records (pairs_lag1.cu guard_push): bit (r kGuardTC + c) of
@@ -86,6 +98,7 @@ struct Plan {
   bool prep_valid = false;
   bool reuse_prep = false;       // set for the duration of one call
   bool imag_handoff = false;     // the last call handed IMAGCOHY from K2 to K3
+  bool fused_last = false;       // ... ran K2 and K3 as one fused kernel
   // multi-GPU (shard.cu): peers' rings attached by cs_ring_attach[_ptrs]
   int n_ranks = 0, rank = 0, node_block = 0;  // node n's fp64 spectra live on rank n / node_block
   double2** peer_x64 = nullptr;  // device [n_ranks] fp64 ring of every rank (own included)

@@ -118,38 +118,6 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float* v, uint32_t tb, 
   }
 }
 
-// 8-column variants (16 epilogue warps: 96 registers per thread)
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
-}
-__device__ __forceinline__ void tmem_ld8x2(uint32_t ta, float* v, uint32_t tb, float* w) {
-  uint32_t r[8], s[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(ta));
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]), "=r"(s[7])
-               : "r"(tb));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    v[q] = __uint_as_float(r[q]);
-    w[q] = __uint_as_float(s[q]);
-  }
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-               ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
-}
-
 // K-major operand tile [128 rows x 32 fp16] written by TMA with SWIZZLE_64B:
 // 64-byte rows, 8-row core groups 512 B apart (SBO), LBO unused, descriptor version 1.
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
@@ -629,10 +597,9 @@ size_t tc_smem_bytes() {
 // grouped order: bands of 8 row tiles swept column by column, so the CTAs resident at
 // once touch ~8 x 128 + 18 x 64 nodes of operands (L2 resident).  Built once per row
 // range and cached in the plan (a blocking upload: first call for that range only).
-const int2* tc_tile_list(Plan& p, int i_lo, int i_hi, int nt64, int64_t* n_tiles, cudaStream_t st) {
-  const int tile_row0 = i_lo / kTcTile;
-  const int tile_row1 = (i_hi + kTcTile - 1) / kTcTile;
-  const uint64_t key = ((uint64_t)tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)nt64;
+// rmul = 2: 128-row tiles (J >= 2 I); rmul = 1: 64 x 64 tiles (J >= I) over row tiles [tile_row0, tile_row1)
+const int2* tile_list(Plan& p, int tile_row0, int tile_row1, int nt64, int rmul, int64_t* n_tiles, cudaStream_t st) {
+  const uint64_t key = ((uint64_t)tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)nt64 ^ ((uint64_t)rmul << 62);
   Plan::TileList* tle = nullptr;
   for (auto& e : p.tc_tiles)
     if (e.key == key && e.ptr) tle = &e;
@@ -642,7 +609,7 @@ const int2* tc_tile_list(Plan& p, int i_lo, int i_hi, int nt64, int64_t* n_tiles
     for (int b0 = tile_row0; b0 < tile_row1; b0 += GR)
       for (int J = 0; J < nt64; ++J)
         for (int I = b0; I < b0 + GR && I < tile_row1; ++I)
-          if (J >= 2 * I) tl.push_back(make_int2(I, J));
+          if (J >= rmul * I) tl.push_back(make_int2(I, J));
     tle = &p.tc_tiles[p.tc_tiles_next];
     p.tc_tiles_next = (p.tc_tiles_next + 1) % Plan::kTileCache;
     if (tle->ptr) {
@@ -664,13 +631,9 @@ const int2* tc_tile_list(Plan& p, int i_lo, int i_hi, int nt64, int64_t* n_tiles
   return (const int2*)tle->ptr;
 }
 
-bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
-                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st, bool handoff) {
-  EncodeTiledFn enc = get_encode();
-  if (!enc) {
-    cs_set_error("cuTensorMapEncodeTiled unavailable");
-    return false;
-  }
+// fp16 hi/lo split operands of the call (k_tc_prep) in the plan's buffer: [nbb][pass][plane][N][K_pad]
+__half* tc_prep_ops(Plan& p, const int* slots, int K, int bin_lo, int nbb, const float* nscale, cudaStream_t st,
+                    int* K_pad_out) {
   const int Kc = K * p.L;                       // contraction length: trials x tapers
   const int K_pad = (Kc + 15) / 16 * 16;        // UMMA K granularity; the last TMA box is zero-filled
   const size_t need = (size_t)nbb * 8 * p.N * K_pad * sizeof(__half);
@@ -680,7 +643,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
       cs_set_error("device allocation failed (tensor-core operands %zu bytes)", need);
       p.tc_ops = nullptr;
       p.tc_bytes = 0;
-      return false;
+      return nullptr;
     }
     p.tc_bytes = need;
   }
@@ -690,6 +653,21 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     dim3 grid((K_pad + 31) / 32, (p.N + 7) / 8, nbb);
     k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, Kc, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
   }
+  *K_pad_out = K_pad;
+  return G;
+}
+
+bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb, int re, bool do_x, bool do_u,
+                  bool do_imag, const cs_outputs* out, const float* nscale, cudaStream_t st, bool handoff) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    cs_set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  int K_pad = 0;
+  __half* G = tc_prep_ops(p, slots, K, bin_lo, nbb, nscale, st, &K_pad);
+  if (!G) return false;
+  const int Kc = K * p.L;
   CUtensorMap mapA, mapB;
   cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 8};
   cuuint64_t strides[2] = {(cuuint64_t)K_pad * 2, (cuuint64_t)p.N * K_pad * 2};
@@ -713,7 +691,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
   a.tile_row0 = a.i_lo / kTcTile;
   int64_t n_tiles = 0;
-  a.tiles = tc_tile_list(p, a.i_lo, a.i_hi, a.nt, &n_tiles, st);
+  a.tiles = tile_list(p, a.i_lo / kTcTile, (a.i_hi + kTcTile - 1) / kTcTile, a.nt, 2, &n_tiles, st);
   if (!a.tiles) return false;
   a.n_tiles = (int)n_tiles;
   {  // small pair spaces: split bins over CTAs.  Persistent CTAs overlap most of a

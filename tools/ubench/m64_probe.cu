@@ -27,7 +27,8 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__global__ void k_probe(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, float* out) {
+__global__ void k_probe(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, float* out,
+                        float* out2) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* sA = sm;          // 64 x 32 B
   unsigned char* sB = sm + 2048;   // 64 x 32 B
@@ -89,6 +90,21 @@ __global__ void k_probe(const __grid_constant__ CUtensorMap mA, const __grid_con
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     out[row * 64 + c] = __uint_as_float(v);
   }
+  // unique values lane * 1000 + column, then read back with 16x256b.x2
+  for (int c = 0; c < 64; ++c) {
+    const float v = (float)(row * 1000 + c);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
+                 "r"(__float_as_uint(v)));
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  {  // 16x256b.x2: 16 lanes x 16 columns per warp, 8 registers per thread
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(tmem + ((uint32_t)(warp * 32) << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int q = 0; q < 8; ++q) out2[(warp * 32 + lane) * 8 + q] = __uint_as_float(r[q]);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -108,6 +124,8 @@ int main() {
   }
   __half *dA, *dB;
   float* dO;
+  float* dO2;
+  cudaMalloc(&dO2, 128 * 8 * 4);
   cudaMalloc(&dA, A.size() * 2);
   cudaMalloc(&dB, B.size() * 2);
   cudaMalloc(&dO, 128 * 64 * 4);
@@ -126,7 +144,7 @@ int main() {
                                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("encode %d %d\n", (int)r1, (int)r2);
   cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192);
-  k_probe<<<1, 128, 8192>>>(mA, mB, dO);
+  k_probe<<<1, 128, 8192>>>(mA, mB, dO, dO2);
   cudaError_t e = cudaDeviceSynchronize();
   printf("kernel %s\n", cudaGetErrorString(e));
   std::vector<float> O(128 * 64);
@@ -149,6 +167,14 @@ int main() {
     for (int c = 0; c < 4; ++c) printf(" %6.1f", O[l * 64 + c]);
     printf("   ref rows:");
     for (int m = 0; m < 64; m += 16) printf(" %6.1f", ref(m, 0));
+    printf("\n");
+  }
+  // 16x256b.x2 mapping: register value = lane * 1000 + column
+  std::vector<float> O2(128 * 8);
+  cudaMemcpy(O2.data(), dO2, O2.size() * 4, cudaMemcpyDeviceToHost);
+  for (int t = 0; t < 32; ++t) {
+    printf("warp0 thread %2d:", t);
+    for (int q = 0; q < 8; ++q) printf(" (l%d,c%d)", (int)O2[t * 8 + q] / 1000, (int)O2[t * 8 + q] % 1000);
     printf("\n");
   }
   return 0;
