@@ -40,6 +40,10 @@ struct FusedOut {
   const int2* tiles;  // grouped tile order (pairs_tc.cu tile_list)
 };
 
+// fp16 split operand planes per (bin, pass) (k_tc_prep): re_h, re_l, im_h, im_l, -im_h, -im_l
+// (the negated Im planes are the CTA-pair kernel's second B half, pairs_tc.cu)
+constexpr int kTcPlanes = 6;
+
 constexpr int kTile = 64;        // node tile edge of the upper-triangular pair tiling
 constexpr int kThreads = 256;    // pair-kernel CTA size (16 x 16 threads, 4 x 4 pairs each)
 // exact-sign guard overflow records (pairs_lag1.cu guard_push): bit (r kGuardTC + c) of

@@ -294,7 +294,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
                 unsigned char* stg = k2ring + ks * kFStageBytes;
 #pragma unroll
                 for (int pl = 0; pl < 4; ++pl) {
-                  const int z = ((bl0 + b) * 2 + pass) * 4 + pl;
+                  const int z = ((bl0 + b) * 2 + pass) * kTcPlanes + pl;
                   tma_load_3d(stg + pl * kFPlane, &mapG, &kfull[ks], c * kFChunk, iBase, z);
                   tma_load_3d(stg + (4 + pl) * kFPlane, &mapG, &kfull[ks], c * kFChunk, jBase, z);
                 }
@@ -925,7 +925,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   // FU: the fp16 operands [nbb][pass][plane][N][K_pad] (k_tc_prep), 16-trial x 64-node boxes
   CUtensorMap mG = mI;
   if (r == CUDA_SUCCESS && fo) {
-    cuuint64_t gd[3] = {(cuuint64_t)fo->K_pad, (cuuint64_t)N, (cuuint64_t)nbb * 8};
+    cuuint64_t gd[3] = {(cuuint64_t)fo->K_pad, (cuuint64_t)N, (cuuint64_t)nbb * 2 * kTcPlanes};
     cuuint64_t gs[2] = {(cuuint64_t)fo->K_pad * 2, (cuuint64_t)N * fo->K_pad * 2};
     cuuint32_t gb[3] = {(cuuint32_t)kFChunk, (cuuint32_t)kTile, 1};
     cuuint32_t ge[3] = {1, 1, 1};

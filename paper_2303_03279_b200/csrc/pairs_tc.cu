@@ -129,13 +129,13 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
   d |= (uint64_t)4 << 61;                             // SWIZZLE_64B
   return d;
 }
-// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, K-major A and B, M = N = 128
-__host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, K-major A and B, M x N
+__host__ __device__ constexpr uint32_t idesc_f16(bool neg_a, int M = kTcTile, int N = kTcTileJ) {
   return (1u << 4)                     // D format f32
          | (0u << 7) | (0u << 10)      // A, B format f16
          | ((neg_a ? 1u : 0u) << 13)   // negate A
-         | ((uint32_t)(kTcTileJ >> 3) << 17)  // N >> 3
-         | ((uint32_t)(kTcTile >> 4) << 24);  // M >> 4
+         | ((uint32_t)(N >> 3) << 17)  // N >> 3
+         | ((uint32_t)(M >> 4) << 24); // M >> 4
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -166,6 +166,17 @@ __device__ __forceinline__ void epi_bar() {  // the epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(kTcEpiWarps * 32) : "memory");
 }
 
+// PAIR: a CTA pair (cluster of 2, cta_group::2) works on a 256 x 64 tile: CTA r holds
+// rows [256 I + 128 r, +128) as A and one half of the stacked B' = [B1 | B2] (N = 128), so
+// one M = 256 x N = 128 MMA gives both CTAs' D_re (columns 0-63) and D_im (64-127):
+//   A = Re_i^a : B' = [Re_j^b | -Im_j^b]     A = Im_i^a : B' = [Im_j^b | Re_j^b]
+// (rank 0's B slots hold re_h re_l im_h im_l, rank 1's -im_h -im_l re_h re_l).  Six MMAs
+// per 16-trial step instead of 2 x 12 single-CTA 128 x 64 MMAs, each SM reading the same
+// 6 KB of operands per MMA for twice the products (the single-CTA N = 64 MMA is bound by
+// the shared-memory read port, 48 of 32 cycles: tools/ubench/mma_rate.cu).  The leader's
+// MMA warp issues; both CTAs' TMA loads complete on the leader's stage barrier; commits
+// multicast to both CTAs; both CTAs' epilogue warps release a TMEM region on the leader.
+template <bool PAIR>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const TcArgs a) {
   // dynamic shared memory starts at the (1024-aligned) base of the CTA's window: no
@@ -182,10 +193,14 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   uint32_t* tmem_slot = (uint32_t*)(tempty + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // persistent CTAs: work unit u = (tile u / nbc, bin chunk u % nbc), strided by the grid;
-  // the smem ring and TMEM phases carry over between units, so the next unit's loads
-  // and MMAs overlap this unit's epilogue
+  // persistent CTAs (PAIR: CTA pairs): work unit u = (tile u / nbc, bin chunk u % nbc),
+  // strided by the grid; the smem ring and TMEM phases carry over between units, so the
+  // next unit's loads and MMAs overlap this unit's epilogue
   const int n_units = a.n_tiles * a.nbc;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int u0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  constexpr int kUnitRows = PAIR ? 2 * kTcTile : kTcTile;  // tile rows per unit
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // swizzled TMA/UMMA tiles need 1024-byte alignment
@@ -195,16 +210,24 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     }
     for (int r = 0; r < 3; ++r) {
       mbar_init(&tfull[r], 1);
-      mbar_init(&tempty[r], kTcEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&tempty[r], (PAIR ? 2 : 1) * kTcEpiWarps);  // one arrive per epilogue warp (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync();  // the peer signals the leader's barriers only after they exist
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -225,10 +248,13 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      // PAIR: every load completes on the leader's stage barrier (which expects both CTAs' bytes)
+      const uint32_t full0 = PAIR ? mapa_u32(smem_u32(full), 0) : 0u;
+      constexpr int bplane_peer[4] = {4, 5, 0, 1};  // rank 1's B slots: -im_h, -im_l, re_h, re_l
+      for (int u = u0; u < n_units; u += ustep) {
         const int2 tij = a.tiles[u / a.nbc];
         const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
-        const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
+        const int iBase = tij.x * kUnitRows + (int)rank * kTcTile, jBase = tij.y * kTcTileJ;
       for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
           const int pass = pass0 + ps;
@@ -240,11 +266,22 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
               if (++stage == kTcStages) { stage = 0; phase ^= 1; }
               continue;
             }
-            mbar_expect_tx(&full[stage], kTcStageBytes);
-            for (int pl = 0; pl < 4; ++pl) {
-              const int z = (bl * 2 + pass) * 4 + pl;
-              tma_load_3d(st + pl * kTcPlaneA, &mapA, &full[stage], c * kTcChunk, iBase, z);
-              tma_load_3d(st + 4 * kTcPlaneA + pl * kTcPlaneB, &mapB, &full[stage], c * kTcChunk, jBase, z);
+            if (!PAIR) {
+              mbar_expect_tx(&full[stage], kTcStageBytes);
+              for (int pl = 0; pl < 4; ++pl) {
+                const int z = (bl * 2 + pass) * kTcPlanes + pl;
+                tma_load_3d(st + pl * kTcPlaneA, &mapA, &full[stage], c * kTcChunk, iBase, z);
+                tma_load_3d(st + 4 * kTcPlaneA + pl * kTcPlaneB, &mapB, &full[stage], c * kTcChunk, jBase, z);
+              }
+            } else {
+              if (rank == 0) mbar_expect_tx(&full[stage], 2 * kTcStageBytes);
+              const uint32_t fb = full0 + (uint32_t)stage * 8u;
+              for (int pl = 0; pl < 4; ++pl) {
+                const int z = (bl * 2 + pass) * kTcPlanes;
+                tma_load_3d_cg2(st + pl * kTcPlaneA, &mapA, fb, c * kTcChunk, iBase, z + pl);
+                tma_load_3d_cg2(st + 4 * kTcPlaneA + pl * kTcPlaneB, &mapB, fb, c * kTcChunk, jBase,
+                                z + (rank ? bplane_peer[pl] : pl));
+              }
             }
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
@@ -256,21 +293,30 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     // the whole warp runs the (uniform) loop so descriptors stay in uniform registers;
     // one elected lane issues each tcgen05.mma / commit
     // (A plane, B plane) for D_re then D_im; planes: 0 re_h, 1 re_l, 2 im_h, 3 im_l;
-    // the last three D_im products are -(Re_i Im_j) via the A-negate bit
-    constexpr int prod_a[12] = {0, 0, 1, 2, 2, 3, 2, 2, 3, 0, 0, 1};
-    constexpr int prod_b[12] = {0, 1, 0, 2, 3, 2, 0, 1, 0, 2, 3, 2};
+    // the first three D_im products are -(Re_i Im_j) via the A-negate bit
+    // (D_im: the -Re_i Im_j products first, the order of the CTA-pair kernel's N = 128 MMAs)
+    constexpr int prod_a[12] = {0, 0, 1, 2, 2, 3, 0, 0, 1, 2, 2, 3};
+    constexpr int prod_b[12] = {0, 1, 0, 2, 3, 2, 2, 3, 2, 0, 1, 0};
     constexpr uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
+    // PAIR: (A plane, B slot) per MMA: A = re_h re_h re_l against B' = [Re | -Im] (slots 0, 1),
+    // A = im_h im_h im_l against B' = [Im | Re] (slots 2, 3); all into one N = 128 D
+    constexpr int pa2[6] = {0, 0, 1, 2, 2, 3};
+    constexpr int pb2[6] = {0, 1, 0, 2, 3, 2};
+    constexpr uint32_t id_pair = idesc_f16(false, 2 * kTcTile, 2 * kTcTileJ);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t tuse = 0;  // bit r: phase of TMEM region r
-    int seq = 0;        // (bin, pass) counter -> region seq % nreg
+    int seq = 0;        // region of the next (bin, pass): round-robin over nreg
     const uint64_t desc0 = umma_desc_sw64(smem_u32(smem));
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    if (PAIR && rank != 0) {
+      // the peer's MMA warp idles: the leader issues for both CTAs
+    } else
+    for (int u = u0; u < n_units; u += ustep) {
       const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
       for (int bl = bl0; bl < bl1; ++bl)
         for (int ps = 0; ps < npass; ++ps) {
-          const int reg = seq % nreg;
-          ++seq;
+          const int reg = seq;
+          seq = seq + 1 == nreg ? 0 : seq + 1;
           mbar_wait(&tempty[reg], ((tuse >> reg) & 1) ^ 1);
           tuse ^= 1u << reg;
           tc_fence_after();
@@ -282,20 +328,30 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             const int n_steps = TC_ABL(8) ? 0 : min(kTcChunk / 16, (a.K_pad - c * kTcChunk) / 16);
 #pragma unroll
             for (int s = 0; s < kTcChunk / 16; ++s) {
-              if (s < n_steps) {
+                if (PAIR && s < n_steps) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                  const uint64_t ad = sd + (uint64_t)((pa2[q] * kTcPlaneA + s * 32) >> 4);
+                  const uint64_t bd = sd + (uint64_t)((4 * kTcPlaneA + pb2[q] * kTcPlaneB + s * 32) >> 4);
+                  tc_mma2_elect(d_re, ad, bd, id_pair, (c == 0 && s == 0 && q == 0) ? 0u : 1u);
+                }
+              } else if (s < n_steps) {
 #pragma unroll
                 for (int q = 0; q < 12; ++q) {
                   const uint64_t ad = sd + (uint64_t)((prod_a[q] * kTcPlaneA + s * 32) >> 4);
                   const uint64_t bd = sd + (uint64_t)((4 * kTcPlaneA + prod_b[q] * kTcPlaneB + s * 32) >> 4);
                   const bool first = (c == 0 && s == 0 && (q == 0 || q == 6));
-                  tc_mma_elect(q < 6 ? d_re : d_im, ad, bd, (q >= 9) ? id_neg : id_pos, first ? 0u : 1u);
+                  tc_mma_elect(q < 6 ? d_re : d_im, ad, bd, (q >= 6 && q < 9) ? id_neg : id_pos, first ? 0u : 1u);
                 }
               }
             }
-            tc_commit_elect(&empty[stage]);  // frees the smem stage when these MMAs finish
+            // frees the smem stage (PAIR: in both CTAs) when these MMAs finish
+            if (PAIR) tc_commit2_elect(&empty[stage]);
+            else tc_commit_elect(&empty[stage]);
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
-          tc_commit_elect(&tfull[reg]);      // accumulators of (bin, pass) complete
+          if (PAIR) tc_commit2_elect(&tfull[reg]);  // accumulators of (bin, pass) complete
+          else tc_commit_elect(&tfull[reg]);
         }
     }
   }
@@ -313,13 +369,18 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
     const uint32_t xrow = xb + (uint32_t)(r * kTcXStride) * 8u;  // this thread's transpose row
     const bool cohy = a.cohy_bins || a.cohy_band;
     uint32_t tuse = 0;  // bit r: phase of TMEM region r
-    int seq = 0;        // (bin, pass) counter, as in the MMA warp
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    int seq = 0;        // region of the next (bin, pass), as in the MMA warp
+    const uint32_t tempty0 = PAIR ? mapa_u32(smem_u32(tempty), 0) : 0u;  // the leader's region barriers
+    for (int u = u0; u < n_units; u += ustep) {
     const int2 tij = a.tiles[u / a.nbc];
     const int bl0 = (u % a.nbc) * a.bpc, bl1 = min(a.nbb, bl0 + a.bpc);
-    const int iBase = tij.x * kTcTile, jBase = tij.y * kTcTileJ;
+    const int iBase = tij.x * kUnitRows + (int)rank * kTcTile, jBase = tij.y * kTcTileJ;
     const int i = iBase + r;
     const int chi = a.N - jBase;             // valid tile columns: c < chi (and c > i - jBase)
+    // every (row, column) of the tile is a stored pair (strictly above the diagonal, inside N
+    // and the row range): the per-bin stores need no predicates (warp-uniform)
+    const bool full_tile = iBase + kTcTile <= jBase && jBase + kTcTileJ <= a.N && iBase >= a.i_lo &&
+                           iBase + kTcTile <= a.i_hi;
     // (the previous unit's last epi_bar ordered its rowoff_s reads before these writes)
     if (et < kTcTile) {
       const int ii = iBase + et;
@@ -350,8 +411,8 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
       epi_bar();
       for (int ps = 0; ps < npass; ++ps) {
         const int pass = pass0 + ps;
-        const int reg = seq % nreg;
-        ++seq;
+        const int reg = seq;
+        seq = seq + 1 == nreg ? 0 : seq + 1;
         mbar_wait(&tfull[reg], (tuse >> reg) & 1);
         tuse ^= 1u << reg;
         tc_fence_after();
@@ -445,7 +506,10 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[reg]);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster_relaxed(tempty0 + (uint32_t)reg * 8u);
+          else mbar_arrive(&tempty[reg]);
+        }
         epi_bar();
         // per-bin outputs: warp e stores rows [8 e, 8 e + 8), 64 contiguous pairs each;
         // four rows per group, all shared loads of a group issued before its stores
@@ -454,6 +518,34 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
           float* const py = pass == 0 ? a.imag_bins : nullptr;     // .y: IMAGCOHY
           float2* const pc = (pass == 0 && cohy) ? a.cohy_bins : nullptr;
           const bool magx = pass == 0 && cohy;                     // buffer holds COHY: COH = |.|
+          if (full_tile && !pc && px) {
+            // interior tile, every row in range, no COHY: no per-store predicates, one
+            // 64-bit address per row (the c = 32 half is +32 floats)
+            float* const pxb = px + bo + jBase + lane;
+            float* const pyb = py ? py + bo + jBase + lane : nullptr;
+#pragma unroll
+            for (int g = 0; g < kTcRowsPerWarp; g += 4) {
+              long long ro[4];
+              float2 v0[4], v1[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int row = e * kTcRowsPerWarp + g + t;
+                ro[t] = lds_s64(rob + (uint32_t)row * 8u);
+                const uint32_t xa = xb + (uint32_t)(row * kTcXStride + lane) * 8u;
+                v0[t] = lds_f2(xa);
+                v1[t] = lds_f2(xa + 256u);
+              }
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                __stcs(pxb + ro[t], v0[t].x);  // streaming stores: keep the operands in L2
+                __stcs(pxb + ro[t] + 32, v1[t].x);
+                if (pyb) {
+                  __stcs(pyb + ro[t], v0[t].y);
+                  __stcs(pyb + ro[t] + 32, v1[t].y);
+                }
+              }
+            }
+          } else
           for (int g = 0; g < kTcRowsPerWarp; g += 4) {
             long long ro[4];
             float2 v0[4], v1[4];
@@ -548,14 +640,20 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync();  // neither CTA frees TMEM while the pair's MMAs / epilogues may use it
+  else
+    __syncthreads();
   tc_fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 2) {
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
 }
 
 // ---------------------------------------------------------------- operand prep
-// G[z = (bl*2 + pass)*4 + plane][n][k] fp16, k < K_pad (zero padded):
-//   pass 0: X * 2^-e(n,b) (|.| <= 1), pass 1: U = X/|X|; planes re_h, re_l, im_h, im_l.
+// G[z = (bl*2 + pass)*kTcPlanes + plane][n][k] fp16, k < K_pad (zero padded):
+//   pass 0: X * 2^-e(n,b) (|.| <= 1), pass 1: U = X/|X|; planes re_h, re_l, im_h, im_l, -im_h, -im_l.
 __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int K_pad,
                           int N, int nb, int L, int bin_lo, int nbb, const float* __restrict__ nscale,
                           __half* __restrict__ G) {
@@ -581,9 +679,13 @@ __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict_
       const float v = vals[pass][c];
       const __half h = __float2half_rn(v);
       const __half l = __float2half_rn(v - __half2float(h));
-      const size_t z = ((size_t)bl * 2 + pass) * 4 + c * 2;
+      const size_t z = ((size_t)bl * 2 + pass) * kTcPlanes + c * 2;
       G[(z + 0) * plane + (size_t)n * K_pad + k] = h;
       G[(z + 1) * plane + (size_t)n * K_pad + k] = l;
+      if (c == 1) {  // -im_h, -im_l (exact negations)
+        G[(z + 2) * plane + (size_t)n * K_pad + k] = __hneg(h);
+        G[(z + 3) * plane + (size_t)n * K_pad + k] = __hneg(l);
+      }
     }
 }
 
@@ -599,7 +701,7 @@ size_t tc_smem_bytes() {
 // range and cached in the plan (a blocking upload: first call for that range only).
 // rmul = 2: 128-row tiles (J >= 2 I); rmul = 1: 64 x 64 tiles (J >= I) over row tiles [tile_row0, tile_row1)
 const int2* tile_list(Plan& p, int tile_row0, int tile_row1, int nt64, int rmul, int64_t* n_tiles, cudaStream_t st) {
-  const uint64_t key = ((uint64_t)tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)nt64 ^ ((uint64_t)rmul << 62);
+  const uint64_t key = ((uint64_t)tile_row0 << 40) ^ ((uint64_t)tile_row1 << 20) ^ (uint64_t)nt64 ^ ((uint64_t)rmul << 56);
   Plan::TileList* tle = nullptr;
   for (auto& e : p.tc_tiles)
     if (e.key == key && e.ptr) tle = &e;
@@ -636,7 +738,7 @@ __half* tc_prep_ops(Plan& p, const int* slots, int K, int bin_lo, int nbb, const
                     int* K_pad_out) {
   const int Kc = K * p.L;                       // contraction length: trials x tapers
   const int K_pad = (Kc + 15) / 16 * 16;        // UMMA K granularity; the last TMA box is zero-filled
-  const size_t need = (size_t)nbb * 8 * p.N * K_pad * sizeof(__half);
+  const size_t need = (size_t)nbb * 2 * kTcPlanes * p.N * K_pad * sizeof(__half);
   if (need > p.tc_bytes) {
     if (p.tc_ops) cudaFreeAsync(p.tc_ops, st);
     if (cudaMallocAsync(&p.tc_ops, need, st) != cudaSuccess) {
@@ -669,7 +771,7 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   if (!G) return false;
   const int Kc = K * p.L;
   CUtensorMap mapA, mapB;
-  cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 8};
+  cuuint64_t dims[3] = {(cuuint64_t)K_pad, (cuuint64_t)p.N, (cuuint64_t)nbb * 2 * kTcPlanes};
   cuuint64_t strides[2] = {(cuuint64_t)K_pad * 2, (cuuint64_t)p.N * K_pad * 2};
   cuuint32_t boxA[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTile, 1};
   cuuint32_t boxB[3] = {(cuuint32_t)kTcChunk, (cuuint32_t)kTcTileJ, 1};
@@ -689,17 +791,31 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.i_lo = rb * kTile;
   a.i_hi = re * kTile < p.N ? re * kTile : p.N;
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
-  a.tile_row0 = a.i_lo / kTcTile;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+  // CTA pairs (256 x 64 tiles, cta_group::2) when the whole pair space gives every pair of
+  // SMs at least two tiles; small pair spaces keep single-CTA 128 x 64 tiles and bin
+  // splitting.  Decided by N, not by the row range, so every shard of a multi-GPU split
+  // runs the same kernel as the single-GPU run (identical per-pair arithmetic)
+  const char* pair_s = getenv("CSCONN_K2_PAIR");  // A/B and test override: 0 single CTAs, 1 CTA pairs
+  const int pair_env = pair_s ? atoi(pair_s) : -1;
+  const int rows2 = (p.N + 2 * kTcTile - 1) / (2 * kTcTile);
+  const int64_t est_pair_tiles = (int64_t)rows2 * a.nt - 2LL * rows2 * (rows2 - 1);
+  const bool pair = pair_env >= 0 ? pair_env > 0 : est_pair_tiles >= nsm;
+  const int unit_rows = pair ? 2 * kTcTile : kTcTile;
+  a.tile_row0 = a.i_lo / unit_rows;
   int64_t n_tiles = 0;
-  a.tiles = tile_list(p, a.i_lo / kTcTile, (a.i_hi + kTcTile - 1) / kTcTile, a.nt, 2, &n_tiles, st);
+  a.tiles = tile_list(p, a.i_lo / unit_rows, (a.i_hi + unit_rows - 1) / unit_rows, a.nt, unit_rows / kTcTileJ,
+                      &n_tiles, st);
   if (!a.tiles) return false;
   a.n_tiles = (int)n_tiles;
-  {  // small pair spaces: split bins over CTAs.  Persistent CTAs overlap most of a
+  if (pair) {
+    a.bpc = nbb;
+    a.nbc = 1;
+  } else {  // small pair spaces: split bins over CTAs.  Persistent CTAs overlap most of a
      // work unit's fixed cost, so the time is ~ rounds x (unit overhead + bins x
      // per-bin cost) with the overhead ~2 bins (cfg1/2/4 sweeps); pick the split
      // minimising rounds * (2 + bins per unit).
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
     int nbc = 1;
     double best = 1e300;
     for (int c = 1; c <= nbb && n_tiles > 0; ++c) {
@@ -740,7 +856,8 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   { const char* d = getenv("CSCONN_TC_DBG"); a.dbg = d ? atoi(d) : 0; }
 #endif
   const size_t smem = tc_smem_bytes();
-  CS_SMEM_ONCE(k_pairs_tc, smem);
+  CS_SMEM_ONCE(k_pairs_tc<false>, smem);
+  CS_SMEM_ONCE(k_pairs_tc<true>, smem);
   {
     PhaseMark ph(p, "pairs_tc", st);
     if (a.nbc > 1) {
@@ -749,12 +866,30 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
       if (a.cohy_band) cudaMemsetAsync(a.cohy_band, 0, a.pair_stride * sizeof(float2), st);
       if (a.imag_band) cudaMemsetAsync(a.imag_band, 0, a.pair_stride * sizeof(float), st);
     }
-    if (n_tiles > 0) {  // persistent: one CTA per SM (210 KB smem), units strided over the grid
-      int nsm = 148;
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+    if (n_tiles > 0 && !pair) {  // persistent: one CTA per SM (210 KB smem), units strided over the grid
       const int64_t units = n_tiles * a.nbc;
       const int64_t grid = units < nsm ? units : nsm;
-      k_pairs_tc<<<(unsigned)grid, kTcThreads, smem, st>>>(mapA, mapB, a);
+      k_pairs_tc<false><<<(unsigned)grid, kTcThreads, smem, st>>>(mapA, mapB, a);
+    } else if (n_tiles > 0) {  // persistent CTA pairs (clusters of 2: the two SMs of a TPC)
+      const int64_t units = n_tiles;
+      const int64_t pairs = units < nsm / 2 ? units : nsm / 2;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(2 * pairs));
+      cfg.blockDim = dim3(kTcThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, k_pairs_tc<true>, mapA, mapB, a);
+      if (e != cudaSuccess) {
+        cs_set_error("k_pairs_tc (CTA pairs) launch failed: %s", cudaGetErrorString(e));
+        return false;
+      }
     }
   }
   return true;
