@@ -19,9 +19,8 @@ void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbin
                      cudaStream_t st);
 void run_pair_sums(const Plan& p, const int* slots, int K, int bin_lo, int nbb, const cs_sums* out, cudaStream_t st);
 struct LagArgs;
-bool fused_call(const Plan& p, unsigned mask, int K, int nbb, const cs_outputs* out);
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
-                    int rb, int re, const cs_outputs* out, cudaStream_t st, bool fused);
+                    int rb, int re, const cs_outputs* out, cudaStream_t st);
 int run_coh_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
                     int rb, int re, const cs_outputs* out, cudaStream_t st);
 }  // namespace cs
@@ -425,15 +424,8 @@ int cs_pair_metrics_ex(cs_plan* p, const int* slots, int K, unsigned mask, int b
   // tensor-core family (COHY, COH, PLV; IMAGCOHY when no sign-based metric is asked),
   // then the phase-lag family
   p->imag_handoff = false;
-  p->fused_last = cs::fused_call(*p, mask, K, nbb, &o);
-  int rc1 = 0, rc2 = 0;
-  if (p->fused_last) {  // one kernel for the tensor-core and phase-lag families
-    p->imag_handoff = true;
-    rc2 = cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st, true);
-  } else {
-    rc1 = cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
-    rc2 = rc1 < 0 ? -1 : cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st, false);
-  }
+  const int rc1 = cs::run_coh_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
+  const int rc2 = rc1 < 0 ? -1 : cs::run_lag_family(*p, slots, K, mask, bin_lo, nbb, rb, re, &o, st);
   p->reuse_prep = false;
   if (rc1 < 0 || rc2 < 0) return CS_EPARAM;
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cs_pair_metrics");
@@ -540,7 +532,7 @@ int cs_ring_view(cs_plan* p, void** x64, void** x32, int64_t* n_elems) {
 }
 
 int64_t cs_fft_call_count(const cs_plan* p) { return p ? p->fft_calls : 0; }
-int cs_last_imag_handoff(const cs_plan* p) { return !p ? 0 : p->fused_last ? 2 : p->imag_handoff ? 1 : 0; }
+int cs_last_imag_handoff(const cs_plan* p) { return !p ? 0 : p->imag_handoff ? 1 : 0; }
 
 int cs_plan_k1_kind(const cs_plan* p) {
   if (!p) return -1;

@@ -28,17 +28,6 @@
 
 namespace cs {
 
-// outputs of the tensor-core part of the fused call (pairs_lag1.cu FU): the fp16
-// split operands (k_tc_prep) and the COH / PLV per-bin and band arrays
-struct FusedOut {
-  const void* G;
-  int K_pad;
-  float* coh_bins;
-  float* coh_band;
-  float* plv_bins;
-  float* plv_band;
-  const int2* tiles;  // grouped tile order (pairs_tc.cu tile_list)
-};
 
 // fp16 split operand planes per (bin, pass) (k_tc_prep): re_h, re_l, im_h, im_l, -im_h, -im_l
 // (the negated Im planes are the CTA-pair kernel's second B half, pairs_tc.cu)
@@ -102,7 +91,6 @@ struct Plan {
   bool prep_valid = false;
   bool reuse_prep = false;       // set for the duration of one call
   bool imag_handoff = false;     // the last call handed IMAGCOHY from K2 to K3
-  bool fused_last = false;       // ... ran K2 and K3 as one fused kernel
   // multi-GPU (shard.cu): peers' rings attached by cs_ring_attach[_ptrs]
   int n_ranks = 0, rank = 0, node_block = 0;  // node n's fp64 spectra live on rank n / node_block
   double2** peer_x64 = nullptr;  // device [n_ranks] fp64 ring of every rank (own included)

@@ -60,8 +60,6 @@ struct LagArgs {
   float imag_tau;
   float4* nf;              // [nbb][N64] node factors of the phase-lag epilogue (k_lag_prep)
   const float* nscale;     // [nbb][N] fp16 operand scale of the tensor-core pass (k_tc_prep)
-  bool imag_tc_band;       // fused call: the IMAGCOHY band mean holds the tensor-core value of
-                           // every entry; the fallback corrects it by (fp64 - per-bin value)
 };
 
 // Trial-pair packing of the selected trials (k = 2 kp, 2 kp + 1) into the layouts the
@@ -128,9 +126,6 @@ __device__ __forceinline__ void fallback_entry(const LagArgs& a, int i, int j, i
   const double2* Xi = a.x64_of ? a.x64_of[i / a.node_block] : a.X64;
   const double2* Xj = a.x64_of ? a.x64_of[j / a.node_block] : a.X64;
   const int64_t po = pair_of(i, j, a.N) - a.pair_base;
-  // fused call: the tensor-core IMAGCOHY of this entry (already in the band mean), read
-  // before the trial loop so its latency overlaps the fp64 loads
-  const float old_imag = (a.imag_tc_band && live && lane == 0) ? a.bins[0][(int64_t)bl * a.pair_stride + po] : 0.f;
 #pragma unroll 4
   for (int k = lane; k < (live ? a.K : 0); k += 8) {  // unrolled: the trials' loads are independent
     const int slot = a.slots[k];
@@ -169,9 +164,8 @@ __device__ __forceinline__ void fallback_entry(const LagArgs& a, int i, int j, i
     const float inv = 1.f / (float)a.nbb;
     for (int m = 0; m < 5; ++m) {
       float* bp = a.bins[m] ? a.bins[m] + (int64_t)bl * a.pair_stride + po : nullptr;
-      const float old = m == 0 ? old_imag : 0.f;
       if (bp) *bp = v[m];
-      if (a.band[m]) atomicAdd(&a.band[m][po], (v[m] - old) * inv);
+      if (a.band[m]) atomicAdd(&a.band[m][po], v[m] * inv);
     }
   }
 }
@@ -255,10 +249,9 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, const float4* nf,
-                 const FusedOut* fo, cudaStream_t st);
+                 cudaStream_t st);
 
-bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, bool handoff,
-                   const FusedOut* fo = nullptr) {
+bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, bool handoff) {
   cudaMemsetAsync(a.counters, 0, 3 * sizeof(int), st);
   if (!p.reuse_prep) {
     PhaseMark ph(p, "lag_prep", st);
@@ -267,7 +260,7 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, 
                                      a.nscale, a.real0, a.real1, (float4*)a.PkI, (float4*)a.PkJ, a.nf);
   }
   {
-    PhaseMark ph(p, fo ? "pairs_fused" : "pairs_lag", st);
+    PhaseMark ph(p, "pairs_lag", st);
     // small pair spaces (few tiles, many bins): split the bins over CTAs.  One CTA per
     // SM, so the makespan is waves x (per-CTA fixed cost + bins x per-bin cost); the
     // fixed part (barrier init, band zeroing, first-stage TMA latency, band write-out)
@@ -296,14 +289,10 @@ bool run_pairs_lag(Plan& p, const LagArgs& a, int64_t n_tiles, cudaStream_t st, 
       for (int m = 0; m < 5; ++m)
         if (a.band[m]) cudaMemsetAsync(a.band[m], 0, a.pair_stride * sizeof(float), st);
       if (a.plv_band) cudaMemsetAsync(a.plv_band, 0, a.pair_stride * sizeof(float), st);
-      if (fo) {
-        cudaMemsetAsync(fo->coh_band, 0, a.pair_stride * sizeof(float), st);
-        cudaMemsetAsync(fo->plv_band, 0, a.pair_stride * sizeof(float), st);
-      }
     }
     if (!launch_lag1(a.PkI, a.PkJ, a.N, a.N64, a.K, a.Kp, a.bin_lo, a.nbb, a.psd, a.mag, a.real0, a.real1, a.nt,
                      a.row_begin, a.pair_base, a.pair_stride, a.bins, a.band, a.g, a.flags, a.recs, a.counters, a.flag_cap,
-                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, a.imag_in, a.imag_tau, a.nf, fo, st))
+                     n_tiles, nbc, a.L, a.plv_bins, a.plv_band, a.imag_in, a.imag_tau, a.nf, st))
       return false;
   }
   {
@@ -350,23 +339,9 @@ static bool imag_handoff(const Plan& p, unsigned mask, int K, int nbb, const cs_
 }
 static float imag_tau_of(int Kc) { return 1e-5f + 6e-8f * (float)Kc; }  // pairs_tc.cu: D_im error / norm
 
-__half* tc_prep_ops(Plan& p, const int* slots, int K, int bin_lo, int nbb, const float* nscale, cudaStream_t st,
-                    int* K_pad_out);
-const int2* tile_list(Plan& p, int tile_row0, int tile_row1, int nt64, int rmul, int64_t* n_tiles, cudaStream_t st);
-
-// The fused call (pairs_lag1.cu FU): the hand-off shape with PLV as well -- COH, IMAGCOHY,
-// PLV and the four phase-lag metrics, per bin and band, single taper -- can run as one
-// kernel whose tensor-core MMAs overlap its FP32 trial loop.  Opt-in (CSCONN_FUSED=1) until
-// it beats the two kernels (DESIGN.md section 4 has the measurements).
-bool fused_call(const Plan& p, unsigned mask, int K, int nbb, const cs_outputs* out) {
-  static const bool on = getenv("CSCONN_FUSED") && getenv("CSCONN_FUSED")[0] == '1';
-  return on && imag_handoff(p, mask, K, nbb, out) && (mask & CS_PLV) && out->bins[3] && out->band[3] &&
-         out->bins[1] && out->band[1];
-}
-
 int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, int nbb,
-                    int rb, int re, const cs_outputs* out, cudaStream_t st, bool fused) {
-  const bool handoff = fused || imag_handoff(p, mask, K, nbb, out);
+                    int rb, int re, const cs_outputs* out, cudaStream_t st) {
+  const bool handoff = imag_handoff(p, mask, K, nbb, out);
   if (imag_on_tensor_cores(mask)) mask &= ~(unsigned)CS_IMAGCOHY;
   unsigned any = 0;
   for (int q = 0; q < 5; ++q) any |= mask & kLagBits[q];
@@ -439,24 +414,6 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   if (handoff) {
     a.imag_in = (const float*)out->bins[2];
     a.imag_tau = imag_tau_of(K * p.L);
-  }
-  if (fused) {
-    FusedOut fo{};
-    fo.G = tc_prep_ops(p, slots, K, bin_lo, nbb, p.nscale, st, &fo.K_pad);
-    if (!fo.G) return -1;
-    fo.coh_bins = (float*)out->bins[1];
-    fo.coh_band = (float*)out->band[1];
-    fo.plv_bins = (float*)out->bins[3];
-    fo.plv_band = (float*)out->band[3];
-    if (!getenv("CSCONN_FUSED_ROWORDER")) {
-      int64_t nt_list = 0;
-      fo.tiles = tile_list(p, rb, re, a.nt, 1, &nt_list, st);
-      if (!fo.tiles || nt_list != n_tiles) return -1;
-    }
-    a.nscale = p.nscale;
-    a.imag_tc_band = true;
-    if (!run_pairs_lag(p, a, n_tiles, st, handoff, &fo)) return -1;
-    return 2;
   }
   if (!run_pairs_lag(p, a, n_tiles, st, handoff)) return -1;
   return 2;

@@ -115,39 +115,9 @@ struct Lag1Args {
   const float4* nf;          // [nbb][N64] node factors {M', rsqrt(psd) / s, rsqrt(psd), M' 2^-10}
                              // (k_lag_prep; M' = 0 on exactly-real bins, s = the fp16 operand scale):
                              // the FULL epilogue's per-node inputs
-  // FU (the fused tensor-core + phase-lag call): COH / PLV outputs and the fp16 operands' K
-  float* coh_bins;
-  float* coh_band;
-  float* tplv_bins;
-  float* tplv_band;
-  int K_pad;
-  const int2* tiles;         // (I, J) per CTA tile in a grouped order (else the closed-form row order)
+  const int2* tiles;         // (I, J) per CTA tile in an explicit order (else the closed-form row order)
 };
 
-// ---- FU: the tensor-core contraction of the fused call (k_pairs_tc's complex-as-real
-// fp16 hi/lo products, here M = N = 64 per CTA tile, 16-trial stages with SWIZZLE_32B)
-constexpr int kFChunk = 16;                     // trials per stage (32-byte fp16 rows)
-constexpr int kFStages = 2;
-constexpr int kFPlane = kTile * kFChunk * 2;    // 2 KB: 64 rows x 32 B
-constexpr int kFStageBytes = 8 * kFPlane;       // A planes re_h re_l im_h im_l, then B planes: 16 KB
-constexpr int kFX = kTile + 2;                  // transpose buffer row stride (floats; even: float2 stores)
-// TMEM columns; M = 64 puts accumulator row m in lane 32 (m / 16) + m % 16 (probe:
-// tools/ubench/m64_probe.cu): X re | X im | U re | U im, then band sums COH | PLV | IMAGCOHY
-constexpr int kFtXre = 0, kFtXim = 64, kFtUre = 128, kFtUim = 192, kFtCoh = 256, kFtPlv = 320, kFtImag = 384;
-__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t smem_addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);   // start address
-  d |= (uint64_t)1 << 16;                        // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(256 >> 4) << 32;               // SBO: 8-row groups of 32-byte rows
-  d |= (uint64_t)1 << 46;                        // version (Blackwell)
-  d |= (uint64_t)6 << 61;                        // SWIZZLE_32B
-  return d;
-}
-// kind::f16, fp32 accumulate, K-major A and B, M = N = 64
-__host__ __device__ constexpr uint32_t idesc_m64(bool neg_a) {
-  return (1u << 4) | ((neg_a ? 1u : 0u) << 13) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(64 >> 4) << 24);
-}
-__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;" ::"n"(k1Threads) : "memory"); }
 
 // L == 1 uses a dedicated producer warpgroup (20 warps; setmaxnreg gives the 16 compute
 // warps 112 registers and the producers 24); L > 1 needs 128 registers, so 16 warps
@@ -163,45 +133,29 @@ constexpr unsigned kStSign = 1, kStSum = 2, kStAbs = 4, kStAll = 7;
 // IMAGIN: the tensor-core kernel already wrote the per-bin IMAGCOHY for this call (its
 // D_im is sum Im; this kernel still forms the band mean); sum t is not accumulated here -- WPLI's numerator is IMAGCOHY sqrt(psd_i psd_j)
 // -- which takes the FADD2 out of the trial loop (see run_lag_family).
-// FU: the fused call (FULL, IMAGIN, single taper): warps 17 / 18 also stream the fp16
-// operands and issue the M = 64 tensor-core MMAs of COH / IMAGCOHY / PLV for the same
-// tile into TMEM, and the compute warps drain them at each bin end.
-template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false, bool WIDE = false, bool IMAGIN = false,
-          bool FU = false>
+template <int L, bool PLVK, unsigned STATS = kStAll, bool FULL = false, bool WIDE = false, bool IMAGIN = false>
 __global__ void __launch_bounds__(L == 1 ? k1ThreadsP : k1Threads, 1)
-k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ,
-             const __grid_constant__ CUtensorMap mapG, const Lag1Args a) {
+k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapJ, const Lag1Args a) {
   constexpr int KCL = k1Rows / L;  // max trial pairs per stage
   constexpr int NM = PLVK ? 6 : 5;
   extern __shared__ __align__(128) unsigned char lag1_smem[];
   float4* XI = (float4*)lag1_smem;                       // [stages][KC][64]
   float4* XJ = XI + k1Stages * k1StageF4;                // [stages][KC][64]
-  // FU: the fp16 operand ring of the tensor-core part follows the phase-lag ring
-  unsigned char* k2ring = (unsigned char*)(XJ + k1Stages * k1StageF4);
-  float* band_s = (float*)(k2ring + (FU ? kFStages * kFStageBytes : 0));  // [NM][64][64]
+  float* band_s = (float*)(XJ + k1Stages * k1StageF4);  // [NM][64][64]
   // FULL single-taper epilogue (kF): band_s holds per-thread band sums instead, float4
-  // [metric][pair half][compute thread] (80 KB; FU: 4 metrics, IMAGCOHY's band is in
-  // TMEM), then IMAGCOHY staging [pair][thread] (16 KB; FU: the [64][65] transpose
-  // buffer of the tensor-core values); nf_s: the bin's node factors [bin % 3][I 64 |
-  // J 64], bulk-copied by the producer with the bin's last stage
+  // [metric][pair half][compute thread] (80 KB), then IMAGCOHY staging [pair][thread]
+  // (16 KB); nf_s: the bin's node factors [bin % 3][I 64 | J 64], bulk-copied by the
+  // producer with the bin's last stage
   constexpr bool kF = FULL && L == 1;
-  static_assert(!FU || (kF && IMAGIN && !PLVK && !WIDE), "fused call: FULL single-taper hand-off only");
-  constexpr int kB0 = FU ? 1 : 0;  // first metric whose band sum the phase-lag part keeps
   float4* band4 = (float4*)band_s;
-  float* imv_s = band_s + (FU ? 4 : 5) * kTile * kTile;
-  float* xbuf = imv_s;
-  float4* nf_s = (float4*)(FU ? imv_s + kTile * kFX : band_s + 6 * kTile * kTile);
+  float* imv_s = band_s + 5 * kTile * kTile;
+  float4* nf_s = (float4*)(band_s + 6 * kTile * kTile);
   uint64_t* full = (uint64_t*)(nf_s + 3 * 2 * kTile);
   uint64_t* empty = full + k1Stages;
-  uint64_t* kfull = empty + k1Stages;   // FU: fp16 operand ring
-  uint64_t* kempty = kfull + kFStages;
-  uint64_t* tfull = kempty + kFStages;  // FU: a bin's accumulators complete
-  uint64_t* tempty = tfull + 1;         // FU: ... drained by the compute warps
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
 
   int I, J;
   const int bchunk = blockIdx.x % a.nbc;
-  if (a.tiles) {  // grouped (L2-friendly) tile order
+  if (a.tiles) {  // an explicit tile order
     const int2 tij = a.tiles[blockIdx.x / a.nbc];
     I = tij.x;
     J = tij.y;
@@ -233,26 +187,11 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], k1Warps);
     }
-    if (FU) {
-      for (int s = 0; s < kFStages; ++s) {
-        mbar_init(&kfull[s], 1);
-        mbar_init(&kempty[s], 1);
-      }
-      mbar_init(tfull, 1);
-      mbar_init(tempty, k1Warps);
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (FU && threadIdx.x == 0 && (smem_u32(k2ring) & 255)) __trap();  // SWIZZLE_32B tiles: 256-byte aligned
-  if (FU && warp == k1Warps + 3) {  // TMEM: 448 of 512 columns used
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
   if (band_mask)
-    for (int e = threadIdx.x; e < (FU ? 4 : NM) * kTile * kTile; e += blockDim.x) band_s[e] = 0.f;
-  if (FU) tc_fence_before();
+    for (int e = threadIdx.x; e < NM * kTile * kTile; e += blockDim.x) band_s[e] = 0.f;
   __syncthreads();
-  if (FU) tc_fence_after();
 
   const int n_stage = (a.Kp + KCL - 1) / KCL;
   int kc = (a.Kp + n_stage - 1) / n_stage;         // balanced stage size (<= KCL trial pairs)
@@ -276,79 +215,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   };
   if (kDedicated) {
     if (warp >= k1Warps) {  // producer warpgroup: 24 registers; warp 16 lane 0 issues the stages
-      if (FU)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
-      else
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
-      if (FU && warp == k1Warps + 1) {
-        // ---- fp16 operand producer: per bin, X then U, 16-trial stages of 4 A + 4 B planes
-        if (lane == 0) {
-          const int n_kc = a.K_pad / kFChunk;
-          int ks = 0;
-          uint32_t kph = 0;
-          for (int b = 0; b < nbl; ++b)
-            for (int pass = 0; pass < 2; ++pass)
-              for (int c = 0; c < n_kc; ++c) {
-                mbar_wait(&kempty[ks], kph ^ 1);  // (stages turn over in < 1 us: no back-off)
-                mbar_expect_tx(&kfull[ks], kFStageBytes);
-                unsigned char* stg = k2ring + ks * kFStageBytes;
-#pragma unroll
-                for (int pl = 0; pl < 4; ++pl) {
-                  const int z = ((bl0 + b) * 2 + pass) * kTcPlanes + pl;
-                  tma_load_3d(stg + pl * kFPlane, &mapG, &kfull[ks], c * kFChunk, iBase, z);
-                  tma_load_3d(stg + (4 + pl) * kFPlane, &mapG, &kfull[ks], c * kFChunk, jBase, z);
-                }
-                if (++ks == kFStages) {
-                  ks = 0;
-                  kph ^= 1;
-                }
-              }
-        }
-        return;
-      }
-      if (FU && warp == k1Warps + 2) {
-        // ---- MMA issuer (whole warp; one elected lane issues): D_re, D_im of X and U per bin
-        constexpr int prod_a[12] = {0, 0, 1, 2, 2, 3, 2, 2, 3, 0, 0, 1};
-        constexpr int prod_b[12] = {0, 1, 0, 2, 3, 2, 0, 1, 0, 2, 3, 2};
-        constexpr uint32_t id_pos = idesc_m64(false), id_neg = idesc_m64(true);
-        const uint32_t tmem = *tmem_slot;
-        const int n_kc = a.K_pad / kFChunk;
-        const uint64_t desc0 = umma_desc_sw32(smem_u32(k2ring));
-        int ks = 0;
-        uint32_t kph = 0;
-        for (int b = 0; b < nbl; ++b) {
-          mbar_wait(tempty, (b & 1) ^ 1);  // the previous bin's accumulators were drained
-          tc_fence_after();
-          for (int pass = 0; pass < 2; ++pass) {
-            const uint32_t d_re = tmem + (pass ? kFtUre : kFtXre), d_im = d_re + 64;
-            for (int c = 0; c < n_kc; ++c) {
-              mbar_wait(&kfull[ks], kph);
-              tc_fence_after();
-              const uint64_t sd = desc0 + (uint64_t)((ks * kFStageBytes) >> 4);
-#pragma unroll
-              for (int q = 0; q < 12; ++q) {
-                const uint64_t ad = sd + (uint64_t)((prod_a[q] * kFPlane) >> 4);
-                const uint64_t bd = sd + (uint64_t)(((4 + prod_b[q]) * kFPlane) >> 4);
-                const bool first = c == 0 && (q == 0 || q == 6);
-                tc_mma_elect(q < 6 ? d_re : d_im, ad, bd, q >= 9 ? id_neg : id_pos, first ? 0u : 1u);
-              }
-              tc_commit_elect(&kempty[ks]);  // frees the stage when these MMAs finish
-              if (++ks == kFStages) {
-                ks = 0;
-                kph ^= 1;
-              }
-            }
-          }
-          tc_commit_elect(tfull);
-        }
-        return;
-      }
-      if (FU && warp == k1Warps + 3) {  // TMEM owner: free it once the compute warps are done
-        asm volatile("bar.sync 2, %0;" ::"n"(k1Threads + 32) : "memory");
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
-        return;
-      }
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
       if (warp == k1Warps && lane == 0)
         for (int t = 0; t < total; ++t) {
           const int s = t % k1Stages;
@@ -406,7 +273,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       ++bl;
     }
     const int s = t % k1Stages;
-    if (kF && IMAGIN && !FU && st == n_stage - 1) {
+    if (kF && IMAGIN && st == n_stage - 1) {
       // the bin's tensor-core IMAGCOHY of this thread's pairs, copied while the last stage runs
       const uint32_t bin_off = (uint32_t)bl * (uint32_t)a.pair_stride;
 #pragma unroll
@@ -527,83 +394,12 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       // +32 floats), band sums in this thread's own float4 slots, predicated stores
       const float4* nfs = nf_s + (bl % 3) * 2 * kTile;
       const uint32_t bin_off = (uint32_t)bl * (uint32_t)a.pair_stride;
-      if (FU) {
-        // ---- tensor-core part of the bin: COH, PLV, IMAGCOHY from the TMEM accumulators.
-        // Warp w drains TMEM lane quadrant w % 4 (rows 16 (w % 4) + lane, lanes < 16 hold
-        // data), columns 16 (w / 4) ..; each metric goes through the [64][65] transpose
-        // buffer and leaves as 32-column row stores in the phase-lag mapping; IMAGCOHY stays
-        // in the buffer for the phase-lag epilogue below.
-        named_sync_compute();  // the previous bin's readers of xbuf are done
-        mbar_wait(tfull, (bl - bl0) & 1);
-        tc_fence_after();
-        // 16x256b.x2 loads: thread t holds rows r0 = t / 4 and r0 + 8 of the warp's 16 TMEM
-        // lanes, columns cp, cp + 1, cp + 8, cp + 9 (cp = 2 (t % 4)) of its 16-column group
-        // (probe: tools/ubench/m64_probe.cu), so all 32 lanes carry data
-        const int q4 = warp & 3, c16 = (warp >> 2) * 16;
-        const int r0 = 16 * q4 + (lane >> 2), cp = c16 + 2 * (lane & 3);
-        const uint32_t tl = *tmem_slot + ((uint32_t)(32 * q4) << 16) + c16;
-        const float rsi0 = nfs[r0].y, rsi1 = nfs[r0 + 8].y;
-        const float rsj[4] = {nfs[kTile + cp].y, nfs[kTile + cp + 1].y, nfs[kTile + cp + 8].y, nfs[kTile + cp + 9].y};
-        const float inv_nb = 1.f / (float)a.nbb;
-        const bool acc_band = bl != bl0;
-#pragma unroll 1
-        for (int round = 0; round < 3; ++round) {  // COH, PLV, IMAGCOHY
-          if (round > 0) named_sync_compute();     // the previous round's readers are done
-          float x[8], y[8], val[8], bnd[8];
-          if (round == 0) tmem_ld256x2(tl + kFtXre, x, tl + kFtXim, y);
-          else if (round == 1) tmem_ld256x2(tl + kFtUre, x, tl + kFtUim, y);
-          else tmem_ld256(tl + kFtXim, y);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {  // e: bit 0 column +1, bit 1 row +8, bit 2 column +8
-            const float rs = ((e >> 1) & 1 ? rsi1 : rsi0) * rsj[(e & 1) + ((e >> 2) << 1)];
-            if (round == 0) {
-              const float vr = x[e] * rs, vi = y[e] * rs;
-              val[e] = sqrt_approx(vr * vr + vi * vi);
-            } else if (round == 1) {
-              val[e] = sqrt_approx(x[e] * x[e] + y[e] * y[e]) * invK;
-            } else {
-              val[e] = y[e] * rs;
-            }
-          }
-          const uint32_t bc = tl + (round == 0 ? kFtCoh : round == 1 ? kFtPlv : kFtImag);
-          if (acc_band) tmem_ld256(bc, bnd);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) bnd[e] = acc_band ? fmaf(val[e], inv_nb, bnd[e]) : val[e] * inv_nb;
-          tmem_st256(bc, bnd);
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const int row = r0 + 8 * ((e >> 1) & 1), col = cp + 8 * (e >> 2);
-            *(float2*)&xbuf[row * kFX + col] = make_float2(val[e], val[e + 1]);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (round == 2) {  // every accumulator read: hand TMEM back to the MMA warp
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);
-          }
-          named_sync_compute();  // xbuf holds the round's 64 x 64 values
-          if (round < 2) {
-            float* const dst = round == 0 ? a.coh_bins : a.tplv_bins;
-#pragma unroll
-            for (int r = 0; r < k1TR; ++r) {
-              const int i = iBase + ty + k1TY * r;
-              const uint32_t ro = row_off32((uint32_t)i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off +
-                                  (uint32_t)(jBase + tx + k1TX);
-#pragma unroll
-              for (int c = 0; c < k1TC; ++c) {
-                const int j = jBase + tx + k1TX * c;
-                if (i < j && j < a.N) __stcs(dst + ro - k1TX * (1 - c), xbuf[(ty + k1TY * r) * kFX + tx + k1TX * c]);
-              }
-            }
-          }
-        }
-      }
       float4 fI[k1TR], fJ[k1TC];  // {M', rsqrt(psd) / s, rsqrt(psd), M' 2^-10}
 #pragma unroll
       for (int r = 0; r < k1TR; ++r) fI[r] = nfs[ty + k1TY * r];
 #pragma unroll
       for (int c = 0; c < k1TC; ++c) fJ[c] = nfs[kTile + tx + k1TX * c];
-      if (IMAGIN && !FU) cp_async_wait_all();
+      if (IMAGIN) cp_async_wait_all();
       const float tau = IMAGIN ? a.imag_tau : 0.f;
       unsigned fl = 0;
       // kFast: an interior tile (every i < j < N) whose nodes all have non-zero spectra in
@@ -614,8 +410,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         for (int h = 0; h < 2; ++h) {  // pairs 4h .. 4h + 3: rows r = 2h, 2h + 1
           float bsum[5][4];
 #pragma unroll
-          for (int m = kB0; m < 5; ++m) {
-            const float4 q = band4[((m - kB0) * 2 + h) * k1Threads + tid];
+          for (int m = 0; m < 5; ++m) {
+            const float4 q = band4[(m * 2 + h) * k1Threads + tid];
             bsum[m][0] = q.x; bsum[m][1] = q.y; bsum[m][2] = q.z; bsum[m][3] = q.w;
           }
 #pragma unroll
@@ -628,7 +424,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
                                 (uint32_t)(jBase + tx + k1TX);
             float* pb[5];
 #pragma unroll
-            for (int m = (IMAGIN && !FU) ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
+            for (int m = IMAGIN ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
             const float phI = odd ? fI[r].w : 0.f;
             const float gMi = a.g * fI[r].x;
 #pragma unroll
@@ -643,9 +439,9 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
               float s_im, v0;
               bool flagged;
               if (IMAGIN) {
-                const float im = FU ? xbuf[(ty + k1TY * r) * kFX + tx + k1TX * c] : imv_s[p * k1Threads + tid];
+                const float im = imv_s[p * k1Threads + tid];
                 s_im = (dead || (!kFast && rr2 == 0.f)) ? 0.f : im * rcp_approx(rr2);
-                v0 = FU ? im : dead ? 0.f : im;
+                v0 = dead ? 0.f : im;
                 flagged = valid && !dead && (mn[p] <= gMi * fJ[c].x || tau > 1e-4f * rr2 * s_abs);
               } else {
                 s_im = dead ? 0.f : (lo_of(sim[p]) + hi_of(sim[p])) - tph;
@@ -661,14 +457,10 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
               const bool ok = valid && !flagged;
 #pragma unroll
               for (int m = 0; m < 5; ++m) {
-                // FU: IMAGCOHY (the tensor-core value) for every valid entry: the fp64 fallback
-                // reads it back to correct the band mean of a flagged entry
-                if (FU && m == 0) {
-                  if (valid) __stcs(pb[0] - k1TX * (1 - c), v[0]);
-                } else if (m > 0 || !IMAGIN) {
+                if (m > 0 || !IMAGIN) {
                   if (ok) __stcs(pb[m] - k1TX * (1 - c), v[m]);  // streaming: keep the operands in L2
                 }
-                if (m >= kB0) bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
+                bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
               }
               sim[p] = 0ull;
               sabs[p] = 0.f;
@@ -677,8 +469,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
             }
           }
 #pragma unroll
-          for (int m = kB0; m < 5; ++m)
-            band4[((m - kB0) * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
+          for (int m = 0; m < 5; ++m)
+            band4[(m * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
         }
       };
       bool fast = interior;
@@ -815,8 +607,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       const int i = iBase + ty + k1TY * r;
       const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
 #pragma unroll
-      for (int m = kB0; m < 5; ++m) {
-        const float4 q = band4[((m - kB0) * 2 + r / 2) * k1Threads + tid];
+      for (int m = 0; m < 5; ++m) {
+        const float4 q = band4[(m * 2 + r / 2) * k1Threads + tid];
 #pragma unroll
         for (int c = 0; c < k1TC; ++c) {
           const int j = jBase + tx + k1TX * c;
@@ -830,43 +622,6 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           }
         }
       }
-    }
-    if (FU) {
-      // the tensor-core band means (already divided by nbb) from TMEM through xbuf
-      const int q4 = warp & 3, c16 = (warp >> 2) * 16;
-      const int r0 = 16 * q4 + (lane >> 2), cp = c16 + 2 * (lane & 3);
-      const uint32_t tl = *tmem_slot + ((uint32_t)(32 * q4) << 16) + c16;
-#pragma unroll 1
-      for (int round = 0; round < 3; ++round) {
-        named_sync_compute();
-        float bnd[8];
-        tmem_ld256(tl + (round == 0 ? kFtCoh : round == 1 ? kFtPlv : kFtImag), bnd);
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int row = r0 + 8 * ((e >> 1) & 1), col = cp + 8 * (e >> 2);
-          *(float2*)&xbuf[row * kFX + col] = make_float2(bnd[e], bnd[e + 1]);
-        }
-        named_sync_compute();
-        float* const dst = round == 0 ? a.coh_band : round == 1 ? a.tplv_band : a.band[0];
-#pragma unroll
-        for (int r = 0; r < k1TR; ++r) {
-          const int i = iBase + ty + k1TY * r;
-          const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
-#pragma unroll
-          for (int c = 0; c < k1TC; ++c) {
-            const int j = jBase + tx + k1TX * c;
-            if (i < j && j < a.N) {
-              const float v = xbuf[(ty + k1TY * r) * kFX + tx + k1TX * c];
-              if (a.nbc > 1)
-                atomicAdd(dst + rowoff + j, v);
-              else
-                __stcs(dst + rowoff + j, v);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      asm volatile("bar.arrive 2, %0;" ::"n"(k1Threads + 32) : "memory");  // TMEM may be freed
     }
   } else if (band_mask) {
     // band write-out by rows: the compute warps' band slots are complete after one
@@ -904,7 +659,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
                  int64_t pair_base, int64_t pair_stride, float* const* bins, float* const* band, float g,
                  int4* flags, int4* recs, int* counters, int flag_cap, int64_t n_tiles, int nbc,
                  int L, float* plv_bins, float* plv_band, const float* imag_in, float imag_tau, const float4* nf,
-                 const FusedOut* fo, cudaStream_t st) {
+                 cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     cs_set_error("cuTensorMapEncodeTiled unavailable");
@@ -922,16 +677,6 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
     r = enc(&mJ, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)PkJ, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  // FU: the fp16 operands [nbb][pass][plane][N][K_pad] (k_tc_prep), 16-trial x 64-node boxes
-  CUtensorMap mG = mI;
-  if (r == CUDA_SUCCESS && fo) {
-    cuuint64_t gd[3] = {(cuuint64_t)fo->K_pad, (cuuint64_t)N, (cuuint64_t)nbb * 2 * kTcPlanes};
-    cuuint64_t gs[2] = {(cuuint64_t)fo->K_pad * 2, (cuuint64_t)N * fo->K_pad * 2};
-    cuuint32_t gb[3] = {(cuuint32_t)kFChunk, (cuuint32_t)kTile, 1};
-    cuuint32_t ge[3] = {1, 1, 1};
-    r = enc(&mG, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)fo->G, gd, gs, gb, ge, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
   if (r != CUDA_SUCCESS) {
     cs_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return false;
@@ -952,12 +697,6 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
   a.imag_in = imag_in;
   a.imag_tau = imag_tau;
   a.nf = nf;
-  if (fo) {
-    a.tiles = fo->tiles;
-    a.coh_bins = fo->coh_bins; a.coh_band = fo->coh_band;
-    a.tplv_bins = fo->plv_bins; a.tplv_band = fo->plv_band;
-    a.K_pad = fo->K_pad;
-  }
   const size_t smem = (size_t)2 * k1Stages * k1StageF4 * 16 + 6 * kTile * kTile * 4 + 3 * 2 * kTile * 16 +
                      2 * k1Stages * 8;
   const unsigned grid = (unsigned)(n_tiles * nbc);
@@ -965,24 +704,19 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
 #define CS_LAG1S(LL, PV, SS)                                                                           \
   do {                                                                                                   \
     CS_SMEM_ONCE((k_pairs_lag1<LL, PV, SS>), smem);                                                     \
-    k_pairs_lag1<LL, PV, SS><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, mG, a);    \
+    k_pairs_lag1<LL, PV, SS><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);    \
   } while (0)
 #define CS_LAG1(LL, PV)                                                                              \
   do {                                                                                                   \
     CS_SMEM_ONCE((k_pairs_lag1<LL, PV>), smem);                                                         \
-    k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, mG, a);     \
+    k_pairs_lag1<LL, PV><<<grid, LL == 1 ? k1ThreadsP : k1Threads, smem, st>>>(mI, mJ, a);     \
   } while (0)
-  if (fo) {  // the fused tensor-core + phase-lag call (run_fused checked the shape)
-    const size_t fsmem = (size_t)2 * k1Stages * k1StageF4 * 16 + (size_t)kFStages * kFStageBytes +
-                         4 * kTile * kTile * 4 + kTile * kFX * 4 + 3 * 2 * kTile * 16 + 128;
-    CS_SMEM_ONCE((k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true, true>), fsmem);
-    k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true, true><<<grid, k1ThreadsP, fsmem, st>>>(mI, mJ, mG, a);
-  } else if (imag_in) {  // IMAGCOHY from the tensor-core kernel (run_lag_family checked the shape)
+  if (imag_in) {  // IMAGCOHY from the tensor-core kernel (run_lag_family checked the shape)
     CS_SMEM_ONCE((k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true>), smem);
-    k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, mG, a);
+    k_pairs_lag1<1, false, kStSign | kStAbs, true, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
   } else if (L == 1 && Kp >= 65536) {  // a 16-bit sign-count field could wrap: per-stage decode
     CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, false, true>), smem);
-    k_pairs_lag1<1, false, kStAll, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, mG, a);
+    k_pairs_lag1<1, false, kStAll, false, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
   } else if (L == 1) {
     // statistics the requested outputs need (bins / band pointers: IMAG, PLI, USPLI, WPLI, DSWPLI)
     auto want = [&](int m) { return bins[m] || band[m]; };
@@ -998,7 +732,7 @@ bool launch_lag1(const float4* PkI, const float4* PkJ, int N, int N64, int K, in
         for (int m = 0; m < 5; ++m) full = full && bins[m] && band[m];
         if (full) {
           CS_SMEM_ONCE((k_pairs_lag1<1, false, kStAll, true>), smem);
-          k_pairs_lag1<1, false, kStAll, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, mG, a);
+          k_pairs_lag1<1, false, kStAll, true><<<grid, k1ThreadsP, smem, st>>>(mI, mJ, a);
         } else {
           CS_LAG1(1, false);
         }

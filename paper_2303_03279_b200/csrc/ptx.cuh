@@ -250,39 +250,6 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
                "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
 }
 
-// 16x256b.x2 shape (16 TMEM lanes x 16 columns per warp, all 32 threads): thread t holds
-// lanes t/4 and t/4 + 8, columns 2 (t%4) + {0, 1, 8, 9}, in the order (l, c), (l, c+1),
-// (l+8, c), (l+8, c+1), (l, c+8), (l, c+9), (l+8, c+8), (l+8, c+9)  (tools/ubench/m64_probe.cu)
-__device__ __forceinline__ void tmem_ld256_raw(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld256(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  tmem_ld256_raw(taddr, r);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
-}
-__device__ __forceinline__ void tmem_ld256x2(uint32_t ta, float* v, uint32_t tb, float* w) {
-  uint32_t r[8], s[8];
-  tmem_ld256_raw(ta, r);
-  tmem_ld256_raw(tb, s);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    v[q] = __uint_as_float(r[q]);
-    w[q] = __uint_as_float(s[q]);
-  }
-}
-__device__ __forceinline__ void tmem_st256(uint32_t taddr, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-               ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
-}
-
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
