@@ -19,7 +19,7 @@ hdr = rows[0]
 iname, ival, iunit = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 last, post = {}, collections.defaultdict(list)
 for r in rows[1:]:
-    m = re.search(r"cs::(k_\w+)(<[^(]*>)?", r[iname])
+    m = re.search(r"(?:cs::)?\b(k_\w+)(<[^(]*>)?", r[iname])
     if not m:
         continue
     v = float(r[ival].replace(",", ""))
