@@ -61,6 +61,7 @@ struct Plan {
   float* mag = nullptr;          // [nb][N] max_k sqrt(sum_l |X|^2)
   float* nscale = nullptr;       // [nb][N] 2^-ceil(log2 mag): per-node-bin fp16 operand scale
   void* tc_ops = nullptr;        // tensor-core operand planes (grown on demand)
+  bool tc_neg_planes = false;    // ... the last prep also wrote the -Im planes (CTA-pair kernel)
   size_t tc_bytes = 0;
   void* lag_ops = nullptr;       // packed trial-pair operands of the phase-lag kernel
   size_t lag_bytes = 0;

@@ -656,7 +656,7 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
 //   pass 0: X * 2^-e(n,b) (|.| <= 1), pass 1: U = X/|X|; planes re_h, re_l, im_h, im_l, -im_h, -im_l.
 __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict__ slots, int K, int K_pad,
                           int N, int nb, int L, int bin_lo, int nbb, const float* __restrict__ nscale,
-                          __half* __restrict__ G) {
+                          __half* __restrict__ G, int neg_planes) {
   const int k = blockIdx.x * 32 + threadIdx.x;
   const int n = blockIdx.y * 8 + threadIdx.y;
   const int bl = blockIdx.z;
@@ -682,7 +682,7 @@ __global__ void k_tc_prep(const float2* __restrict__ X32, const int* __restrict_
       const size_t z = ((size_t)bl * 2 + pass) * kTcPlanes + c * 2;
       G[(z + 0) * plane + (size_t)n * K_pad + k] = h;
       G[(z + 1) * plane + (size_t)n * K_pad + k] = l;
-      if (c == 1) {  // -im_h, -im_l (exact negations)
+      if (c == 1 && neg_planes) {  // -im_h, -im_l (exact negations; the CTA-pair kernel's B halves)
         G[(z + 2) * plane + (size_t)n * K_pad + k] = __hneg(h);
         G[(z + 3) * plane + (size_t)n * K_pad + k] = __hneg(l);
       }
@@ -735,7 +735,7 @@ const int2* tile_list(Plan& p, int tile_row0, int tile_row1, int nt64, int rmul,
 
 // fp16 hi/lo split operands of the call (k_tc_prep) in the plan's buffer: [nbb][pass][plane][N][K_pad]
 __half* tc_prep_ops(Plan& p, const int* slots, int K, int bin_lo, int nbb, const float* nscale, cudaStream_t st,
-                    int* K_pad_out) {
+                    int* K_pad_out, bool neg_planes) {
   const int Kc = K * p.L;                       // contraction length: trials x tapers
   const int K_pad = (Kc + 15) / 16 * 16;        // UMMA K granularity; the last TMA box is zero-filled
   const size_t need = (size_t)nbb * 2 * kTcPlanes * p.N * K_pad * sizeof(__half);
@@ -750,10 +750,12 @@ __half* tc_prep_ops(Plan& p, const int* slots, int K, int bin_lo, int nbb, const
     p.tc_bytes = need;
   }
   __half* G = (__half*)p.tc_ops;
-  if (!p.reuse_prep) {
+  if (!p.reuse_prep || (neg_planes && !p.tc_neg_planes)) {
+    p.tc_neg_planes = neg_planes;
     PhaseMark ph(p, "tc_prep", st);
     dim3 grid((K_pad + 31) / 32, (p.N + 7) / 8, nbb);
-    k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, Kc, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G);
+    k_tc_prep<<<grid, dim3(32, 8), 0, st>>>(p.X32, slots, Kc, K_pad, p.N, p.nb, p.L, bin_lo, nbb, nscale, G,
+                                            neg_planes ? 1 : 0);
   }
   *K_pad_out = K_pad;
   return G;
@@ -766,8 +768,19 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
     cs_set_error("cuTensorMapEncodeTiled unavailable");
     return false;
   }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
+  // CTA pairs (256 x 64 tiles, cta_group::2) when the whole pair space gives every pair of
+  // SMs at least two tiles; small pair spaces keep single-CTA 128 x 64 tiles and bin
+  // splitting.  Decided by N, not by the row range, so every shard of a multi-GPU split
+  // runs the same kernel as the single-GPU run (identical per-pair arithmetic)
+  const char* pair_s = getenv("CSCONN_K2_PAIR");  // A/B and test override: 0 single CTAs, 1 CTA pairs
+  const int pair_env = pair_s ? atoi(pair_s) : -1;
+  const int rows2 = (p.N + 2 * kTcTile - 1) / (2 * kTcTile), nt64 = (p.N + kTcTileJ - 1) / kTcTileJ;
+  const int64_t est_pair_tiles = (int64_t)rows2 * nt64 - 2LL * rows2 * (rows2 - 1);
+  const bool pair = pair_env >= 0 ? pair_env > 0 : est_pair_tiles >= nsm;
   int K_pad = 0;
-  __half* G = tc_prep_ops(p, slots, K, bin_lo, nbb, nscale, st, &K_pad);
+  __half* G = tc_prep_ops(p, slots, K, bin_lo, nbb, nscale, st, &K_pad, pair);
   if (!G) return false;
   const int Kc = K * p.L;
   CUtensorMap mapA, mapB;
@@ -791,17 +804,6 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   a.i_lo = rb * kTile;
   a.i_hi = re * kTile < p.N ? re * kTile : p.N;
   a.nt = (p.N + kTcTileJ - 1) / kTcTileJ;
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
-  // CTA pairs (256 x 64 tiles, cta_group::2) when the whole pair space gives every pair of
-  // SMs at least two tiles; small pair spaces keep single-CTA 128 x 64 tiles and bin
-  // splitting.  Decided by N, not by the row range, so every shard of a multi-GPU split
-  // runs the same kernel as the single-GPU run (identical per-pair arithmetic)
-  const char* pair_s = getenv("CSCONN_K2_PAIR");  // A/B and test override: 0 single CTAs, 1 CTA pairs
-  const int pair_env = pair_s ? atoi(pair_s) : -1;
-  const int rows2 = (p.N + 2 * kTcTile - 1) / (2 * kTcTile);
-  const int64_t est_pair_tiles = (int64_t)rows2 * a.nt - 2LL * rows2 * (rows2 - 1);
-  const bool pair = pair_env >= 0 ? pair_env > 0 : est_pair_tiles >= nsm;
   const int unit_rows = pair ? 2 * kTcTile : kTcTile;
   a.tile_row0 = a.i_lo / unit_rows;
   int64_t n_tiles = 0;

@@ -122,7 +122,8 @@ def test_forced_pairs_row_shards():
 
 def test_default_pairs_match_single_cta_at_scale():
     """N = 2600 (pairs by default): every per-bin and band value of COH / COHY / PLV /
-    IMAGCOHY identical to the single-CTA kernel's, and a node subset against the oracle."""
+    IMAGCOHY identical to the single-CTA kernel's (IMAGCOHY band means up to the order of
+    the fp64 fallback's atomic adds), and a node subset against the oracle."""
     K, N, T, nfft, lo, hi = 24, 2600, 96, 128, 3, 6
     rng = np.random.default_rng(12)
     xh = rng.standard_normal((K, N, T)).astype(np.float32)
@@ -141,8 +142,9 @@ def test_default_pairs_match_single_cta_at_scale():
     for m in metrics:
         d = float((one[m]["bins"] - two[m]["bins"]).abs().max())
         db = float((one[m]["band"] - two[m]["band"]).abs().max())
-        # same products in the same accumulation order per element: bit-identical
-        assert d == 0.0 and db == 0.0, (m, d, db)
+        # same products in the same accumulation order per element: bit-identical per bin;
+        # band means of IMAGCOHY get the fp64 fallback's atomics (order-dependent last bits)
+        assert d == 0.0 and db <= (1e-6 if m == "IMAGCOHY" else 0.0), (m, d, db)
     sub = np.array([0, 1, 11, 255, 256, 257, 511, 1024, 2047, 2500, 2599])
     want, _ = O.compute(list(xh[:, sub].astype(np.float64)), nfft, lo, hi, ("COH", "PLV", "IMAGCOHY"))
     ii, jj = np.triu_indices(len(sub), 1)
