@@ -115,7 +115,6 @@ struct Lag1Args {
   const float4* nf;          // [nbb][N64] node factors {M', rsqrt(psd) / s, rsqrt(psd), M' 2^-10}
                              // (k_lag_prep; M' = 0 on exactly-real bins, s = the fp16 operand scale):
                              // the FULL epilogue's per-node inputs
-  const int2* tiles;         // (I, J) per CTA tile in an explicit order (else the closed-form row order)
 };
 
 
@@ -155,13 +154,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 
   int I, J;
   const int bchunk = blockIdx.x % a.nbc;
-  if (a.tiles) {  // an explicit tile order
-    const int2 tij = a.tiles[blockIdx.x / a.nbc];
-    I = tij.x;
-    J = tij.y;
-  } else {
-    decode_tile(blockIdx.x / a.nbc, a.nt, a.row_begin, I, J);
-  }
+  decode_tile(blockIdx.x / a.nbc, a.nt, a.row_begin, I, J);
   const int bl0 = bchunk * a.bpc;                      // first bin (of the call's nbb) of this CTA
   const int nbl = min(a.bpc, a.nbb - bl0);
   const int iBase = I * kTile, jBase = J * kTile;
