@@ -770,15 +770,23 @@ bool run_pairs_tc(Plan& p, const int* slots, int K, int bin_lo, int nbb, int rb,
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
-  // CTA pairs (256 x 64 tiles, cta_group::2) when the whole pair space gives every pair of
-  // SMs at least two tiles; small pair spaces keep single-CTA 128 x 64 tiles and bin
-  // splitting.  Decided by N, not by the row range, so every shard of a multi-GPU split
-  // runs the same kernel as the single-GPU run (identical per-pair arithmetic)
+  // CTA pairs (256 x 64 tiles, cta_group::2) when the row range gives every pair of SMs at
+  // least two tiles and no more masked rows than single-CTA 128 x 64 tiles would (a shard
+  // whose row range is not 256-aligned computes the rows outside it for nothing: at 8 ranks
+  // of cfg5 the busiest rank would run 1.22x the single-CTA work); small pair spaces keep
+  // single CTAs and bin splitting.  Both kernels issue the same products in the same order
+  // per element, so the choice never changes a result bit (tests/test_gpu_pair.py).
   const char* pair_s = getenv("CSCONN_K2_PAIR");  // A/B and test override: 0 single CTAs, 1 CTA pairs
   const int pair_env = pair_s ? atoi(pair_s) : -1;
-  const int rows2 = (p.N + 2 * kTcTile - 1) / (2 * kTcTile), nt64 = (p.N + kTcTileJ - 1) / kTcTileJ;
-  const int64_t est_pair_tiles = (int64_t)rows2 * nt64 - 2LL * rows2 * (rows2 - 1);
-  const bool pair = pair_env >= 0 ? pair_env > 0 : est_pair_tiles >= nsm;
+  const int nt64 = (p.N + kTcTileJ - 1) / kTcTileJ;
+  const int r_lo = rb * kTile, r_hi = re * kTile < p.N ? re * kTile : p.N;
+  auto unit_tiles = [&](int rows) {  // tiles of `rows` x 64 over [r_lo, r_hi), J >= rows / 64 * I
+    int64_t n = 0;
+    for (int I = r_lo / rows; I < (r_hi + rows - 1) / rows; ++I) n += nt64 - rows / kTcTileJ * I > 0 ? nt64 - rows / kTcTileJ * I : 0;
+    return n;
+  };
+  const int64_t t128 = unit_tiles(kTcTile), t256 = unit_tiles(2 * kTcTile);
+  const bool pair = pair_env >= 0 ? pair_env > 0 : (t256 >= nsm && 2 * t256 <= t128 + t128 / 50);
   int K_pad = 0;
   __half* G = tc_prep_ops(p, slots, K, bin_lo, nbb, nscale, st, &K_pad, pair);
   if (!G) return false;

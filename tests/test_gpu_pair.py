@@ -1,11 +1,12 @@
 """The CTA-pair tensor-core kernel (k_pairs_tc<true>: clusters of two CTAs, one
 M = 256 x N = 128 cta_group::2 MMA per hi/lo product giving D_re and D_im together).
 
-It is the default once the pair space gives every SM pair two 256 x 64 tiles
-(config 3, config 5); CSCONN_K2_PAIR=1 forces it on small shapes so the ragged
-edges (partial tiles, the diagonal, N not a multiple of 64 / 256, odd K, multitaper,
-row-range shards) are checked against the oracle, and CSCONN_K2_PAIR=0 gives the
-single-CTA kernel for a like-for-like comparison at a size where pairs are the default.
+It is chosen per launch when the row range gives every SM pair two 256 x 64 tiles
+and no more masked rows than 128 x 64 single-CTA tiles (config 5 on one GPU);
+CSCONN_K2_PAIR=1 forces it on small shapes so the ragged edges (partial tiles, the
+diagonal, N not a multiple of 64 / 256, odd K, multitaper, row-range shards) are
+checked against the oracle, and CSCONN_K2_PAIR=0 gives the single-CTA kernel for a
+like-for-like comparison.
 Reference: spectral.py:204-241 (CSD and unit-phasor sums), metrics.py:32-56, 115-134.
 """
 import os
@@ -121,7 +122,7 @@ def test_forced_pairs_row_shards():
 
 
 def test_default_pairs_match_single_cta_at_scale():
-    """N = 2600 (pairs by default): every per-bin and band value of COH / COHY / PLV /
+    """N = 2600: every per-bin and band value of COH / COHY / PLV /
     IMAGCOHY identical to the single-CTA kernel's (IMAGCOHY band means up to the order of
     the fp64 fallback's atomic adds), and a node subset against the oracle."""
     K, N, T, nfft, lo, hi = 24, 2600, 96, 128, 3, 6
@@ -136,7 +137,7 @@ def test_default_pairs_match_single_cta_at_scale():
     slots = torch.arange(K, dtype=torch.int32, device="cuda")
     with _pairs("0"):
         one = plan.pair_metrics(slots, metrics)
-    with _pairs("-1"):   # the default choice: pairs at this size
+    with _pairs("1"):
         two = plan.pair_metrics(slots, metrics)
     torch.cuda.synchronize()
     for m in metrics:
