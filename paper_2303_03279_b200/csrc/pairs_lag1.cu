@@ -175,26 +175,46 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
     bin_mask = IMAGIN ? 30u : 31u;
     band_mask = 31u;
   }
-  if (threadIdx.x == 0) {
+  const int n_stage = (a.Kp + KCL - 1) / KCL;
+  int kc = (a.Kp + n_stage - 1) / n_stage;         // balanced stage size (<= KCL trial pairs)
+  if (L == 1 && (kc & 1) && kc < KCL) ++kc;        // even stages: the 2-unrolled loop has no remainder
+  const int total = n_stage * nbl;
+  constexpr bool kDedicated = L == 1;
+  // single taper: the producer thread (warp 16, lane 0) issues stage t
+  const bool producer = kDedicated && warp == k1Warps && lane == 0;
+  auto produce = [&](int t) {
+    const int s = t % k1Stages;
+    mbar_wait_backoff(&empty[s], ((t / k1Stages) & 1) ^ 1);
+    const int bl = bl0 + t / n_stage, st = t % n_stage;
+    const int row = (bl * a.Kp + st * kc) * L;
+    const bool nf_now = kF && st == n_stage - 1;  // the bin's node factors ride on its last stage
+    mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16 + (nf_now ? 2 * kTile * 16 : 0));
+    tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
+    tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
+    if (nf_now) {
+      float4* dst = nf_s + (bl % 3) * 2 * kTile;
+      bulk_load_1d(dst, a.nf + (int64_t)bl * a.N64 + iBase, kTile * 16, &full[s]);
+      bulk_load_1d(dst + kTile, a.nf + (int64_t)bl * a.N64 + jBase, kTile * 16, &full[s]);
+    }
+  };
+  // the barriers are initialised by the thread that issues the TMA loads, which then starts
+  // the first stages at once, so their latency overlaps the band zeroing and the CTA barrier
+  if (threadIdx.x == (kDedicated ? k1Warps * 32 : 0)) {
     for (int s = 0; s < k1Stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], k1Warps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (kDedicated)
+      for (int t = 0; t < min(k1Stages, total); ++t) produce(t);
   }
   if (band_mask)
     for (int e = threadIdx.x; e < NM * kTile * kTile; e += blockDim.x) band_s[e] = 0.f;
   __syncthreads();
 
-  const int n_stage = (a.Kp + KCL - 1) / KCL;
-  int kc = (a.Kp + n_stage - 1) / n_stage;         // balanced stage size (<= KCL trial pairs)
-  if (L == 1 && (kc & 1) && kc < KCL) ++kc;        // even stages: the 2-unrolled loop has no remainder
-  const int total = n_stage * nbl;
-
-  // TMA issue (warp 0, lane 0): stage t into slot t % stages once every warp has
+  // multitaper TMA issue (warp 0, lane 0): stage t into slot t % stages once every warp has
   // released that slot's previous use.  16 warps = 4 per SMSP keep 128 registers
   // per thread available (a 17th producer warp would cap them at 96).
-  constexpr bool kDedicated = L == 1;
   auto issue = [&](int t) {
     if (!kDedicated && warp == 0 && lane == 0 && t < total) {
       const int s = t % k1Stages;
@@ -209,22 +229,8 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   if (kDedicated) {
     if (warp >= k1Warps) {  // producer warpgroup: 24 registers; warp 16 lane 0 issues the stages
       asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
-      if (warp == k1Warps && lane == 0)
-        for (int t = 0; t < total; ++t) {
-          const int s = t % k1Stages;
-          mbar_wait_backoff(&empty[s], ((t / k1Stages) & 1) ^ 1);
-          const int bl = bl0 + t / n_stage, st = t % n_stage;
-          const int row = (bl * a.Kp + st * kc) * L;
-          const bool nf_now = kF && st == n_stage - 1;  // the bin's node factors ride on its last stage
-          mbar_expect_tx(&full[s], 2 * (k1Rows / L) * L * kTile * 16 + (nf_now ? 2 * kTile * 16 : 0));
-          tma_load_2d(XI + s * k1StageF4, &mapI, &full[s], iBase * 4, row);
-          tma_load_2d(XJ + s * k1StageF4, &mapJ, &full[s], jBase * 4, row);
-          if (nf_now) {
-            float4* dst = nf_s + (bl % 3) * 2 * kTile;
-            bulk_load_1d(dst, a.nf + (int64_t)bl * a.N64 + iBase, kTile * 16, &full[s]);
-            bulk_load_1d(dst + kTile, a.nf + (int64_t)bl * a.N64 + jBase, kTile * 16, &full[s]);
-          }
-        }
+      if (producer)
+        for (int t = k1Stages; t < total; ++t) produce(t);
       return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
