@@ -82,7 +82,10 @@ struct TcArgs {
   int flag_cap;
   float imag_tau;
   int dbg;   // ablation bits (builds with -DCS_TC_ABLATION only): 1 per-bin stores, 2 TMEM-phase
-             // math, 4 band phase, 8 MMAs, 16 TMA loads are skipped (timing experiments)
+             // math, 4 band phase, 8 MMAs, 16 TMA loads are skipped (timing experiments).  With
+             // CTA pairs, 16 takes the peer's loads out of the leader's stage barrier, so with
+             // 1 | 8 as well the leader can lap the peer's producer by two phases (a hang the
+             // watchdog traps); with the loads on, the peer's bytes keep the pair in step.
 };
 
 // 16 consecutive fp32 columns of this thread's TMEM lane
@@ -286,6 +289,12 @@ k_pairs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUt
             if (++stage == kTcStages) { stage = 0; phase ^= 1; }
           }
         }
+      }
+      // drain: every stage's last use released, so no MMA commit (PAIR: multicast from the
+      // leader) can still be in flight to this CTA's barriers when it exits
+      for (int i = 0; i < kTcStages; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
