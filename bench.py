@@ -462,6 +462,15 @@ def main():
                                     + ("sum |t| 1 (sum t: IMAGCOHY hand-off from k_pairs_tc)" if handoff
                                        else "sum t 1, sum |t| 1")
                                     + (f", multitaper PLV {2 * L_k3 + 4}" if plv_k3 else ""))}
+        # the same kernel on SURVEY.md 8(d)'s own basis: FP32 instructions per update (t = FMUL +
+        # FFMA per taper, sum of signs, sum |Im|, sum Im unless handed over) at the nominal
+        # 148 x 128 x 1.965 GHz = 3.72e13 instr/s, or the output bytes at HBM, whichever is longer
+        if not plv_k3:
+            n_instr = 2 * L_k3 + 2 + (0 if handoff else 1)
+            t_issue = n_instr * upd / 3.72e13
+            t_out = 16.0 * P_loc * (c.n_bins + 1) / (peaks["hbm_gbs"] * 1e9)
+            roof_k3["survey_8d"] = {"instr_per_update": n_instr, "bound_ms": max(t_issue, t_out) * 1e3,
+                                    "frac": max(t_issue, t_out) / (lag_ms * 1e-3)}
     if per.get(spec_key, 0.0) > 0:
         k1_ms = per[spec_key]
         L_ = 1 if not isinstance(c.taper, tuple) else c.taper[2]
