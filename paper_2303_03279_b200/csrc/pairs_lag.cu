@@ -388,7 +388,11 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   }
   a.plv_bins = plvk ? (float*)out->bins[3] : nullptr;
   a.plv_band = plvk ? (float*)out->band[3] : nullptr;
-  a.g = 1.5f * (4.f + (float)p.L) * 5.9604645e-8f;
+  // exact-sign guard: t = sum_l FFMA(Im_i, Re_j, FMUL(Re_i, -Im_j)) from fp32-rounded
+  // spectra errs by at most (2 + 2L) u sum_l |X_il| |X_jl| <= (2 + 2L) u M_i M_j (two input
+  // roundings per product, then one rounding per multiply and per fused add; Cauchy-Schwarz
+  // over the tapers), u = 2^-24; 1.25x margin for the fp32 magnitudes M
+  a.g = 1.25f * (2.f + 2.f * (float)p.L) * 5.9604645e-8f;
   a.x64_of = p.n_ranks > 1 ? p.peer_x64 : nullptr;
   a.node_block = p.node_block;
   if (const char* gs = getenv("CSCONN_GUARD_G")) a.g *= (float)atof(gs);  // test override (negative control)

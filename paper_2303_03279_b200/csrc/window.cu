@@ -335,7 +335,7 @@ int cs_window_update(cs_window* w, const int* changed_slots, int n_add, int n_su
   a.S_im = w->S_im; a.S_abs = w->S_abs; a.S_sign = w->S_sign; a.risky = w->risky;
   a.S_re = w->S_re; a.U_re = w->U_re; a.U_im = w->U_im; a.psd_state = w->psd;
   a.K = K;
-  a.g = 1.5f * 5.f * 5.9604645e-8f;
+  a.g = 1.25f * 4.f * 5.9604645e-8f;  // per trial: 4 u |X_i| |X_j| (pairs_lag.cu), 1.25x margin
   if (const char* gs = getenv("CSCONN_GUARD_G")) a.g *= (float)atof(gs);
   a.want = w->mask;
   for (int m = 0; m < 8; ++m) {
