@@ -11,7 +11,7 @@ for c in 5 1 2 3 4; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $O/${T}_bench_cfg$c.log 2>&1; echo "bench cfg$c rc=$?"
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/${T}_bench_reference_cfg5.log 2>&1; echo "ref rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${T}_launches_cfg5.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv --log-file $O/${T}_launches_cfg5.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-per-metric > $O/${T}_ncu_launch.log 2>&1; echo "launch rc=$?"
 for k in k_pairs_lag1 k_pairs_tc k_spectra_dmma; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $O/${T}_$k \
