@@ -35,9 +35,16 @@ constexpr int kTcPlanes = 6;
 
 constexpr int kTile = 64;        // node tile edge of the upper-triangular pair tiling
 constexpr int kThreads = 256;    // pair-kernel CTA size (16 x 16 threads, 4 x 4 pairs each)
-// exact-sign guard overflow records (pairs_lag1.cu guard_push): bit (r kGuardTC + c) of
-// mask word, lane l -> pair (row0 + kGuardRowStep r, col0 + l + kGuardColStep c)
-constexpr int kGuardRowStep = 16, kGuardColStep = 32, kGuardTC = 2, kGuardWarps = 16;
+// The phase-lag kernel's register tile (pairs_lag1.cu): every compute thread owns
+// kGuardTR x kGuardTC pairs (i = row0 + ty + kGuardRowStep r, j = col0 + tx + kGuardColStep c).
+// Exact-sign guard overflow records (guard_push; window.cu): kGuardRecI4 int4 each, a header
+// (row of the warp's lane 0, column base, bin, lanes per row) then kGuardNP mask words; bit
+// lane of word (r kGuardTC + c) -> pair (h.x + lane / h.w + kGuardRowStep r,
+// h.y + lane % h.w + kGuardColStep c)
+constexpr int kGuardTR = 4, kGuardTC = 2, kGuardNP = kGuardTR * kGuardTC;
+constexpr int kGuardRowStep = 64 / kGuardTR, kGuardColStep = 64 / kGuardTC;
+constexpr int kGuardWarps = kGuardRowStep * kGuardColStep / 32;
+constexpr int kGuardRecI4 = 1 + kGuardNP / 4;
 
 struct Plan {
   int device = 0;

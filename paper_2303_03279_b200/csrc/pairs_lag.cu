@@ -190,13 +190,18 @@ __global__ void k_lag_fallback(const LagArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, n_warps = (gridDim.x * blockDim.x) >> 5;
   const int g = (threadIdx.x >> 3) & 3;
   for (int rr = warp; rr < n_rec; rr += n_warps) {
-    const int4 h = a.recs[3 * rr], m0 = a.recs[3 * rr + 1], m1 = a.recs[3 * rr + 2];
-    const unsigned m[8] = {(unsigned)m0.x, (unsigned)m0.y, (unsigned)m0.z, (unsigned)m0.w,
-                           (unsigned)m1.x, (unsigned)m1.y, (unsigned)m1.z, (unsigned)m1.w};
-    int q = 0, pos = 0;  // walk the 256 mask bits (word q, bit pos); group g takes every 4th set bit
+    const int4 h = a.recs[kGuardRecI4 * rr];
+    unsigned m[kGuardNP];
+#pragma unroll
+    for (int w4 = 0; w4 < kGuardNP / 4; ++w4) {
+      const int4 v = a.recs[kGuardRecI4 * rr + 1 + w4];
+      m[4 * w4] = (unsigned)v.x; m[4 * w4 + 1] = (unsigned)v.y; m[4 * w4 + 2] = (unsigned)v.z; m[4 * w4 + 3] = (unsigned)v.w;
+    }
+    const int lpr = h.w > 0 ? h.w : 32;  // lanes per tile row of the writer
+    int q = 0, pos = 0;  // walk the mask bits (word q, bit pos); group g takes every 4th set bit
     for (;;) {
       int found[4], nf = 0;
-      while (nf < 4 && q < 8) {
+      while (nf < 4 && q < kGuardNP) {
         const unsigned rest = m[q] >> pos;
         if (!rest || pos >= 32) { ++q; pos = 0; continue; }
         pos += __ffs(rest) - 1;
@@ -206,7 +211,8 @@ __global__ void k_lag_fallback(const LagArgs a) {
       if (nf == 0) break;
       const bool live = g < nf;
       const int bit = live ? found[g] : 0, qq = bit >> 5, ln = bit & 31;
-      const int i = h.x + kGuardRowStep * (qq / kGuardTC), j = h.y + ln + kGuardColStep * (qq % kGuardTC);
+      const int i = h.x + ln / lpr + kGuardRowStep * (qq / kGuardTC),
+                j = h.y + ln % lpr + kGuardColStep * (qq % kGuardTC);
       fallback_entry(a, live ? i : 0, live ? j : 1, h.z, lane, live);
     }
   }
@@ -406,10 +412,10 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   const size_t n_rec = (size_t)n_tiles * nbb * kGuardWarps;
   if (n_rec > p.rec_cap) {
     if (p.recs) cudaFreeAsync(p.recs, st);
-    if (cudaMallocAsync(&p.recs, n_rec * 3 * sizeof(int4), st) != cudaSuccess) {
+    if (cudaMallocAsync(&p.recs, n_rec * kGuardRecI4 * sizeof(int4), st) != cudaSuccess) {
       p.recs = nullptr;
       p.rec_cap = 0;
-      cs_set_error("device allocation failed (guard records %zu bytes)", n_rec * 3 * sizeof(int4));
+      cs_set_error("device allocation failed (guard records %zu bytes)", n_rec * kGuardRecI4 * sizeof(int4));
       return -1;
     }
     p.rec_cap = n_rec;

@@ -29,15 +29,24 @@ namespace cs {
 #endif
 constexpr int k1Rows = CS_K3_ROWS;       // max operand rows (trial pair x taper) per stage
 constexpr int k1Stages = CS_K3_STAGES;   // (build-time overrides for stage sweeps)
-constexpr int k1TR = 4, k1TC = 2;  // pairs per thread (rows x cols)
+constexpr int k1TR = kGuardTR, k1TC = kGuardTC;  // pairs per thread (rows x cols; common.cuh)
 constexpr int k1TY = kTile / k1TR, k1TX = kTile / k1TC;
 constexpr int k1NP = k1TR * k1TC;
 constexpr int k1Warps = k1TY * k1TX / 32;  // compute warps
 constexpr int k1Threads = k1Warps * 32;        // multitaper: lane 0 of warp 0 also issues the TMA loads
-// single taper: plus a producer warpgroup (warp 16 issues the TMA loads, 17-19 idle) whose
-// registers go to the compute warps with setmaxnreg (launch pool 640 x 96 = 128 x 24 +
-// 512 x 112), so the compute warps run with 112 registers instead of 96
+constexpr int k1Quads = k1NP / 4;              // float4 band slots per thread and metric
+constexpr int k1RowsPerQuad = 4 / k1TC;        // tile rows of a band slot's four pairs
+constexpr int k1LanesPerRow = k1TX < 32 ? k1TX : 32;
+// single taper: plus a producer warpgroup (the first producer warp issues the TMA loads, the
+// others idle) whose registers go to the compute warps with setmaxnreg: the launch gives every
+// thread k1RegLaunch registers, the producers drop to 24 and the compute warps rise to
+// k1RegCompute (4 x 4 pairs, 8 compute warps: 384 x 168 = 128 x 24 + 256 x 240)
 constexpr int k1ThreadsP = k1Threads + 128;
+constexpr int k1RegLaunch = ((65536 / k1ThreadsP) & ~7) > 255 ? 248 : ((65536 / k1ThreadsP) & ~7);
+constexpr int k1RegProducer = 24;
+constexpr int k1RegCompute0 = ((k1ThreadsP * k1RegLaunch - 128 * k1RegProducer) / k1Threads) & ~7;
+constexpr int k1RegCompute = k1RegCompute0 > 240 ? 240 : k1RegCompute0;
+static_assert(k1TC == 2 || k1TC == 4, "band slots hold 4 pairs: 2 rows x 2 or 1 row x 4");
 constexpr int k1StageF4 = k1Rows * kTile;  // float4 per side per stage
 constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 
@@ -48,7 +57,7 @@ constexpr float k1Phantom = 9.765625e-4f;  // 2^-10 (see k_lag_prep)
 // ever dropped (k_lag_fallback processes both).  counters: [0] flagged entries,
 // [1] list overflowed, [2] records.
 __device__ __noinline__ void guard_push(int4* flags, int4* recs, int* counters, int cap, unsigned fl,
-                                        int iBase, int jBase, int w, int lane, int bl) {
+                                        int iBase, int jBase, int ty, int tx, int lane, int bl) {
   const int n = __popc(fl);
   int incl = n;
 #pragma unroll
@@ -67,7 +76,7 @@ __device__ __noinline__ void guard_push(int4* flags, int4* recs, int* counters, 
 #pragma unroll
       for (int c = 0; c < k1TC; ++c)
         if ((fl >> (r * k1TC + c)) & 1u)
-          flags[s++] = make_int4(iBase + w + k1TY * r, jBase + lane + k1TX * c, bl, 0);
+          flags[s++] = make_int4(iBase + ty + k1TY * r, jBase + tx + k1TX * c, bl, 0);
     return;
   }
   // slots this warp reserved below the capacity stay unused: mark them empty
@@ -75,15 +84,18 @@ __device__ __noinline__ void guard_push(int4* flags, int4* recs, int* counters, 
   unsigned m[k1NP];
 #pragma unroll
   for (int q = 0; q < k1NP; ++q) m[q] = __ballot_sync(0xffffffffu, (fl >> q) & 1u);
-  if (lane == 0) {
+  if (lane == 0) {  // lane 0 holds tx = 0 and the warp's first row ty
     const int rec = atomicAdd(&counters[2], 1);
-    recs[3 * rec] = make_int4(iBase + w, jBase, bl, 0);
-    recs[3 * rec + 1] = make_int4((int)m[0], (int)m[1], (int)m[2], (int)m[3]);
-    recs[3 * rec + 2] = make_int4((int)m[4], (int)m[5], (int)m[6], (int)m[7]);
+    recs[kGuardRecI4 * rec] = make_int4(iBase + ty, jBase, bl, k1LanesPerRow);
+#pragma unroll
+    for (int w4 = 0; w4 < k1Quads; ++w4)
+      recs[kGuardRecI4 * rec + 1 + w4] =
+          make_int4((int)m[4 * w4], (int)m[4 * w4 + 1], (int)m[4 * w4 + 2], (int)m[4 * w4 + 3]);
     counters[1] = 1;
   }
 }
-static_assert(k1NP == 8 && k1Warps == kGuardWarps && k1TY == kGuardRowStep && k1TX == kGuardColStep && k1TC == kGuardTC,
+static_assert(k1NP == kGuardNP && k1Warps == kGuardWarps && k1TY == kGuardRowStep && k1TX == kGuardColStep &&
+                  k1TC == kGuardTC && k1NP <= 32,
               "guard record layout (common.cuh)");
 
 // first pair index of row i minus one, i (N - 1) - i (i - 1) / 2 - i - 1, mod 2^32: the FULL
@@ -228,12 +240,12 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
   };
   if (kDedicated) {
     if (warp >= k1Warps) {  // producer warpgroup: 24 registers; warp 16 lane 0 issues the stages
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(k1RegProducer));
       if (producer)
         for (int t = k1Stages; t < total; ++t) produce(t);
       return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(k1RegCompute));
   } else {
     for (int t = 0; t < k1Stages - 1; ++t) issue(t);
   }
@@ -406,21 +418,22 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       auto pairs = [&](auto fast_tag) {
         constexpr bool kFast = decltype(fast_tag)::value;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // pairs 4h .. 4h + 3: rows r = 2h, 2h + 1
+        for (int h = 0; h < k1Quads; ++h) {  // pairs 4h .. 4h + 3 (k1RowsPerQuad rows)
           float bsum[5][4];
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
-            const float4 q = band4[(m * 2 + h) * k1Threads + tid];
+            const float4 q = band4[(m * k1Quads + h) * k1Threads + tid];
             bsum[m][0] = q.x; bsum[m][1] = q.y; bsum[m][2] = q.z; bsum[m][3] = q.w;
           }
 #pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const int r = 2 * h + rr;
+          for (int rr = 0; rr < k1RowsPerQuad; ++rr) {
+            const int r = k1RowsPerQuad * h + rr;
             const int i = iBase + ty + k1TY * r;
-            // offset of the c = 1 pair (i, jBase + tx + 32): exact whenever either pair is valid
-            // (the c = 0 offset wraps below 0 for i = 0, tx = 0); c = 0 stores at -32 floats
+            // offset of the last column's pair (i, jBase + tx + k1TX (k1TC - 1)): exact whenever
+            // any pair of the row is valid (the c = 0 offset wraps below 0 for i = 0, tx = 0);
+            // column c stores k1TX (k1TC - 1 - c) floats before it
             const uint32_t ro = row_off32((uint32_t)i, (uint32_t)a.N) - (uint32_t)a.pair_base + bin_off +
-                                (uint32_t)(jBase + tx + k1TX);
+                                (uint32_t)(jBase + tx + k1TX * (k1TC - 1));
             float* pb[5];
 #pragma unroll
             for (int m = IMAGIN ? 1 : 0; m < 5; ++m) pb[m] = a.bins[m] + ro;
@@ -457,9 +470,9 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
 #pragma unroll
               for (int m = 0; m < 5; ++m) {
                 if (m > 0 || !IMAGIN) {
-                  if (ok) __stcs(pb[m] - k1TX * (1 - c), v[m]);  // streaming: keep the operands in L2
+                  if (ok) __stcs(pb[m] - k1TX * (k1TC - 1 - c), v[m]);  // streaming: keep the operands in L2
                 }
-                bsum[m][rr * 2 + c] += ok ? v[m] : 0.f;
+                bsum[m][rr * k1TC + c] += ok ? v[m] : 0.f;
               }
               sim[p] = 0ull;
               sabs[p] = 0.f;
@@ -469,7 +482,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
           }
 #pragma unroll
           for (int m = 0; m < 5; ++m)
-            band4[(m * 2 + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
+            band4[(m * k1Quads + h) * k1Threads + tid] = make_float4(bsum[m][0], bsum[m][1], bsum[m][2], bsum[m][3]);
         }
       };
       bool fast = interior;
@@ -481,7 +494,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         pairs(std::true_type{});
       else
         pairs(std::false_type{});
-      if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
+      if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, tx, lane, bl);
       continue;
     }
 
@@ -594,7 +607,7 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
         if (WIDE) negw[p] = 0u;
       }
     }
-    if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, lane, bl);
+    if (__any_sync(0xffffffffu, fl)) guard_push(a.flags, a.recs, a.counters, a.flag_cap, fl, iBase, jBase, ty, tx, lane, bl);
   }
 
   if (kF) {
@@ -607,11 +620,11 @@ k_pairs_lag1(const __grid_constant__ CUtensorMap mapI, const __grid_constant__ C
       const int64_t rowoff = (int64_t)i * (a.N - 1) - (int64_t)i * (i - 1) / 2 - i - 1 - a.pair_base;
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
-        const float4 q = band4[(m * 2 + r / 2) * k1Threads + tid];
+        const float4 q = band4[(m * k1Quads + r / k1RowsPerQuad) * k1Threads + tid];
 #pragma unroll
         for (int c = 0; c < k1TC; ++c) {
           const int j = jBase + tx + k1TX * c;
-          const int e = (r % 2) * 2 + c;
+          const int e = (r % k1RowsPerQuad) * k1TC + c;
           const float v = (e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w) * inv;
           if (i < j && j < a.N) {
             if (a.nbc > 1)

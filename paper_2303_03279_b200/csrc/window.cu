@@ -217,9 +217,9 @@ __global__ void __launch_bounds__(kWinThreads, 4) k_window_update(const WinArgs 
       if (tx < __popc(m) && base + tx < a.flag_cap) a.flags[base + tx] = make_int4(-1, -1, 0, 0);
       if (tx == 0) {  // record (row, column base, bin, mask) in the fallback's format (pairs_lag.cu)
         const int rec = atomicAdd(&a.counters[2], 1);
-        a.recs[3 * rec] = make_int4(i, j0, bl, 0);
-        a.recs[3 * rec + 1] = make_int4((int)m, 0, 0, 0);
-        a.recs[3 * rec + 2] = make_int4(0, 0, 0, 0);
+        a.recs[kGuardRecI4 * rec] = make_int4(i, j0, bl, 32);  // 32 lanes along the row
+        a.recs[kGuardRecI4 * rec + 1] = make_int4((int)m, 0, 0, 0);
+        for (int w4 = 2; w4 < kGuardRecI4; ++w4) a.recs[kGuardRecI4 * rec + w4] = make_int4(0, 0, 0, 0);
         a.counters[1] = 1;
       }
     }
@@ -236,7 +236,7 @@ struct cs_window {
   int64_t P = 0;
   float *S_im = nullptr, *S_abs = nullptr, *S_re = nullptr, *U_re = nullptr, *U_im = nullptr, *psd = nullptr;
   int *S_sign = nullptr, *risky = nullptr;
-  int4* recs = nullptr;           // guard overflow records (3 int4 each)
+  int4* recs = nullptr;           // guard overflow records (kGuardRecI4 int4 each)
 };
 
 namespace cs {
@@ -277,7 +277,7 @@ int cs_window_create(cs_window** out, cs_plan* plan, unsigned mask, int bin_lo, 
   if (plv) { al((void**)&w->U_re, n * 4); al((void**)&w->U_im, n * 4); }
   {  // at most one record per (32 x 32 tile, bin, row)
     const int64_t nt = (p->N + cs::kWinTile - 1) / cs::kWinTile;
-    al((void**)&w->recs, (size_t)(nt * (nt + 1) / 2) * nbb * cs::kWinTile * 3 * sizeof(int4));
+    al((void**)&w->recs, (size_t)(nt * (nt + 1) / 2) * nbb * cs::kWinTile * cs::kGuardRecI4 * sizeof(int4));
   }
   if (!ok) {
     cudaGetLastError();
