@@ -1,6 +1,6 @@
-// K2: the coherency family (COH, COHY, PLV) as complex-as-real tcgen05 tensor-core
-// contractions over trials, per frequency bin, on 128 x 128 node tiles of the
-// upper-triangular pair space.
+// K2: the coherency family (COH, COHY, PLV; IMAGCOHY from D_im) as complex-as-real
+// tcgen05 tensor-core contractions over trials, per frequency bin, on 128 x 64 node tiles
+// (one CTA) or 256 x 64 tiles (a CTA pair, cta_group::2) of the upper-triangular pair space.
 //
 // Reference: spectral.py:204-241 (CSD = X_i conj X_j and unit phasor sums),
 // metrics.py:32-56 (cohy/coh/plv finalisers), metrics.py:115-134 (band mean).
@@ -11,20 +11,21 @@
 // Operands are fp16 hi/lo splits (x = h + l, |x| <= 1 after a per-node-bin power
 // of two) so each real product is h*h + h*l + l*h: ~22-bit products on the f16
 // tensor path (the plain fp16/bf16/tf32 product misses the 1e-4 COH tolerance;
-// SURVEY.md section 7, hard part 2).  The subtraction in D_im uses the
-// instruction descriptor's A-negate bit, so no negated copies are stored.
+// SURVEY.md section 7, hard part 2).  Single CTA: the subtraction in D_im uses the
+// instruction descriptor's A-negate bit; CTA pair: the peer's B half is the -Im plane.
 //
-// Pipeline (warp specialised, one CTA per tile, all bins and both passes):
+// Pipeline (warp specialised, persistent CTAs / CTA pairs, all bins and both passes of a
+// tile per work unit):
 //   warp 0: TMA producer (cp.async.bulk.tensor, 64B swizzle) into a 3-stage ring
-//   warp 1: single-thread tcgen05.mma issuer, tcgen05.commit to mbarriers
-//   warp 2: TMEM allocator (512 columns: pass 0 -> [0,128), pass 1 -> [128,256),
-//           band-mean accumulators -> [256,512))
+//   warp 1: tcgen05.mma issuer (pair: the leader CTA's), tcgen05.commit to mbarriers
+//   warp 2: TMEM allocator (512 columns: up to three 128-column accumulator regions
+//           round-robin over the (bin, pass) sequence, band-mean accumulators)
 //   warps 4-19: epilogue (tcgen05.ld/st 32x32b.x8; TMEM lane quadrant = warp % 4,
-//           four warps per quadrant split the 64 columns; 96 registers each),
-//           per-bin values leave through a shared-memory transpose buffer as
-//           coalesced row stores; band means accumulate in TMEM across bins.
-// The two passes use disjoint TMEM regions, so the epilogue of one pass overlaps
-// the MMAs of the next.
+//           four warps per quadrant split the 64 columns; 112 registers each after
+//           setmaxnreg), per-bin values leave through a shared-memory transpose buffer
+//           as coalesced row stores; band means accumulate in TMEM across bins.
+// The (bin, pass) units use rotating TMEM regions, so the epilogue of one overlaps the
+// MMAs of the next ones.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
