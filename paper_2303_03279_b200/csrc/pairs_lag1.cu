@@ -1,19 +1,20 @@
-// K3 (single taper): phase-lag family + IMAGCOHY on the FP32/ALU pipes, with a
-// TMA producer warp and an mbarrier ring instead of CTA-wide barriers.
+// K3: the phase-lag family (PLI, USPLI, WPLI, DSWPLI) + IMAGCOHY (+ multitaper PLV) on the
+// FP32/ALU pipes, with a TMA producer and an mbarrier ring instead of CTA-wide barriers.
 //
 // Reference: spectral.py:216-241 (_fold_csd: Im flush, sign(Im), |Im|, Im sums),
 // metrics.py:49-86 (imagcohy / pli / uspli / wpli / dswpli), metrics.py:115-134
 // and core.py:208-215 (band mean).
 //
-// CTA = 64 x 64 node tile x all bins of the band.  16 warps (512 threads,
-// 16 x 32, each thread 4 x 2 pairs: i = ty + 16 r, j = tx + 32 c); lane 0 of warp
-// 0 issues the TMA loads.  The packed trial-pair operands (k_lag_prep: float4 (re_a, re_b, im_a,
-// im_b), J side with Im negated) are streamed by 2D TMA boxes of 64 nodes x KC
-// trial pairs into a 4-stage ring; consumers wait on the stage's full barrier and
-// release it with one arrive per warp, so stages never need a CTA-wide sync.
-// Per trial pair and pair of nodes: FMUL2 + FFMA2 (t = Im X_i conj X_j for two
-// trials), FADD2 (sum t), 2 FADD |.| (sum |t|), 2 LEA.HI (#(t < 0)), FMNMX3
-// (min |t|, the exact-sign guard of pairs_lag.cu).
+// CTA = 64 x 64 node tile x all bins of the band (small pair spaces: a bin chunk).  16
+// compute warps (512 threads, each 4 x 2 pairs: i = ty + 16 r, j = tx + 32 c; common.cuh
+// kGuardTR x kGuardTC); single taper adds a producer warpgroup whose first thread issues the
+// TMA loads (multitaper: warp 0 lane 0).  The packed trial-pair operands (k_lag_prep: float4
+// (re_a, re_b, im_a, im_b), J side with Im negated) are streamed by 2D TMA boxes of 64 nodes
+// x up to 26 rows into a 2-stage ring; consumers wait on the stage's full barrier and release
+// it with one arrive per warp.  Per trial pair and pair of nodes: FMUL2 + FFMA2 (t = Im X_i
+// conj X_j for two trials), 2 FADD |.| (sum |t|), PRMT + 1/2 IADD3 (packed #(t < 0)),
+// FMNMX3 (min |t|, the exact-sign guard of pairs_lag.cu) and, unless the tensor-core kernel
+// hands IMAGCOHY over, FADD2 (sum t).
 #include <type_traits>
 
 #include "common.cuh"
