@@ -461,6 +461,7 @@ int cs_put_taper_spectra(cs_plan* p, const void* src, int n, int bin_lo, int nbi
   }
   if (n <= 0) return CS_OK;
   DeviceGuard g(p->device);
+  p->spectra_put = true;  // arbitrary spectra: no exactly-real DC / Nyquist shortcut from now on
   {
     cs::PhaseMark ph(*p, "put_spectra", (cudaStream_t)stream);
     for (int c0 = 0; c0 < n; c0 += 65535)  // trials ride on grid.y

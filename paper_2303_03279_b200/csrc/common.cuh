@@ -99,6 +99,8 @@ struct Plan {
   bool prep_valid = false;
   bool reuse_prep = false;       // set for the duration of one call
   bool imag_handoff = false;     // the last call handed IMAGCOHY from K2 to K3
+  bool spectra_put = false;      // caller spectra entered the ring (cs_put_spectra): DC / Nyquist may
+                                 // be complex, so the phase-lag kernel must not treat them as real
   // multi-GPU (shard.cu): peers' rings attached by cs_ring_attach[_ptrs]
   int n_ranks = 0, rank = 0, node_block = 0;  // node n's fp64 spectra live on rank n / node_block
   double2** peer_x64 = nullptr;  // device [n_ranks] fp64 ring of every rank (own included)
