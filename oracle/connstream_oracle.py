@@ -134,26 +134,31 @@ def trial_csd_psd(spectra: np.ndarray, n_channels: int):
     return csd, psd
 
 
-def fold_csd(acc: Sums, csd: np.ndarray, psd: np.ndarray) -> None:
-    """spectral.py:216-241 (count=True, all accumulated columns)."""
+def fold_csd(acc: Sums, csd: np.ndarray, psd: np.ndarray, bins=None, count: bool = True) -> None:
+    """spectral.py:216-241: ``bins`` selects the accumulator columns csd / psd cover (None =
+    all); ``count=False`` back-fills columns of trials already counted."""
     im = csd.imag
     im[np.abs(im) <= 1e-13 * np.abs(csd.real)] = 0.0
     mag = np.abs(csd)
     nz = mag > TINY
     unit = np.zeros_like(csd)
     np.divide(csd, mag, out=unit, where=nz)
-    acc.psd_sum += psd
-    acc.csd_sum += csd
-    acc.plv_sum += unit
-    acc.pli_sum += np.sign(im)
-    acc.abs_im_sum += np.abs(im)
-    acc.n_trials_accumulated += 1
+    sl = slice(None) if bins is None else bins
+    acc.psd_sum[:, sl] += psd
+    acc.csd_sum[:, sl] += csd
+    acc.plv_sum[:, sl] += unit
+    acc.pli_sum[:, sl] += np.sign(im)
+    acc.abs_im_sum[:, sl] += np.abs(im)
+    if count:
+        acc.n_trials_accumulated += 1
 
 
-def accumulate(acc: Sums, spectra_cols: np.ndarray) -> None:
-    """spectral.py:244-261 with spectra already restricted to the columns."""
-    csd, psd = trial_csd_psd(spectra_cols, acc.n_channels)
-    fold_csd(acc, csd, psd)
+def accumulate(acc: Sums, spectra_cols: np.ndarray, bins=None, count: bool = True) -> None:
+    """spectral.py:244-261: spectra over all of acc's columns, folded into ``bins`` (None =
+    all) -- or, with bins None, spectra already restricted to acc's columns."""
+    sub = spectra_cols if bins is None else spectra_cols[:, bins]
+    csd, psd = trial_csd_psd(sub, acc.n_channels)
+    fold_csd(acc, csd, psd, bins=bins, count=count)
 
 
 def accumulate_multitaper(acc: Sums, spectra_l: np.ndarray) -> None:

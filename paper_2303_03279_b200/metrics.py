@@ -36,6 +36,39 @@ def _check_k(K: int, metric: str):
         raise DegenerateTrialCountError("USPLI needs at least 2 trials")
 
 
+def _bins_from_sums(acc: SpectrumSet, metric: str, band, want_band=False):
+    """The reference's finalisers (metrics.py:32-98) over the running sums of every fold
+    (cs_pair_sums, fp64 reference arithmetic) -- the path for an accumulator whose columns
+    were folded from different trial sets (accumulate_spectra ``bins`` / ``count=False``,
+    spectral.py:216-261), where no single slot list serves every column.  The sums'
+    normalisation is the reference's: n_trials_accumulated for PLV / PLI / USPLI."""
+    plan = acc.plan
+    lo, nbb = band.lo_bin, band.n_bins
+    slots = torch.tensor([s for s, _ in acc._entries], dtype=torch.int32, device=plan.device)
+    o = plan.pair_sums(slots, lo, nbb)                   # bin-major [nbb, P] / [nbb, C]
+    K = float(acc.n_trials_accumulated)
+    pi, pj = (torch.as_tensor(v, device=plan.device) for v in pair_index(acc.n_channels))
+    tiny = float(np.finfo(np.float64).tiny)
+    if metric in ("COHY", "COH", "IMAGCOHY"):
+        den = torch.sqrt(o["psd"][:, pi] * o["psd"][:, pj])
+        cohy_v = torch.where(den > tiny, o["csd"] / torch.where(den > tiny, den, 1.0), torch.zeros_like(o["csd"]))
+        val = cohy_v if metric == "COHY" else (cohy_v.abs() if metric == "COH" else cohy_v.imag)
+    elif metric == "PLV":
+        val = o["plv"].abs() / K
+    elif metric in ("PLI", "USPLI"):
+        pli = o["pli"].to(torch.float64).abs() / K
+        val = pli if metric == "PLI" else (K * pli * pli - 1.0) / (K - 1.0)
+    else:  # WPLI, DSWPLI
+        num, den = o["csd"].imag.abs(), o["abs_im"]
+        w = torch.where(den > 0.0, num / torch.where(den > 0.0, den, 1.0), torch.zeros_like(num))
+        val = w if metric == "WPLI" else w * w
+    bins = val.to(torch.complex64 if metric == "COHY" else torch.float32)
+    out = {"bins": bins}
+    if want_band:  # core.py:208-215 / metrics.py:124-134: arithmetic mean over the band
+        out["band"] = val.mean(dim=0).to(bins.dtype)
+    return out
+
+
 def _device_bins(acc: SpectrumSet, metric: str, band, want_band=False):
     """Run the pair kernels for ``metric`` over acc's folded trials -> device
     tensors (bins [nb, P], band [P])."""
@@ -45,8 +78,7 @@ def _device_bins(acc: SpectrumSet, metric: str, band, want_band=False):
         raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {acc.n_bins} bins")
     slots = acc.slots_for(band.lo_bin, band.hi_bin)
     if slots is None or len(slots) != acc.n_trials_accumulated:
-        raise ParameterError("accumulator columns were folded from different trial sets; "
-                             "read the running sums (acc.csd_sum, ...) instead")
+        return _bins_from_sums(acc, metric, band, want_band)
     plan = acc.plan
     st = torch.tensor(slots, dtype=torch.int32, device=plan.device)
     out = plan.pair_metrics(st, (metric,), band.lo_bin, band.n_bins, per_bin=True, band=want_band)
@@ -132,8 +164,11 @@ def finalize_spectral(acc: SpectrumSet, metric: MetricId, band: FrequencyBand, p
     band = _full_band(acc, band)
     _check_k(acc.n_trials_accumulated, metric.value)
     slots = acc.slots_for(band.lo_bin, band.hi_bin)
-    if slots is None or len(slots) != acc.n_trials_accumulated:
-        raise ParameterError("accumulator columns were folded from different trial sets")
+    if slots is None or len(slots) != acc.n_trials_accumulated:  # mixed column sets: the sums path
+        if band.hi_bin >= acc.n_bins:
+            raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {acc.n_bins} bins")
+        w = _bins_from_sums(acc, metric.value, band, want_band=True)["band"]
+        return _network_from_band(metric, band, acc.n_trials_accumulated, acc.n_channels, w, positions, node_ids)
     plan = acc.plan
     st = torch.tensor(slots, dtype=torch.int32, device=plan.device)
     out = plan.pair_metrics(st, (metric.value,), band.lo_bin, band.n_bins, per_bin=False, band=True)

@@ -92,3 +92,28 @@ def test_straddling_spectra_negative_control():
     n_bad = int((got != np.rint(O.pli_bins(ref) * K)).sum())
     print(f"guard at 0.02x: {n_bad} K*PLI mismatches")
     assert n_bad >= 1
+
+
+def test_bins_and_count_against_the_reference():
+    """accumulate_spectra with column subsets (slice / index array) and a count=False
+    back-fill, replayed against vectors from the unmodified reference
+    (tests/golden/make_golden_bins.py)."""
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "bins_count.npz")
+    spectra = g["spectra"]
+    K, C, nb = spectra.shape
+    acc = S.SpectrumSet(C, 2 * (nb - 1))
+    for i in range(int(g["n_plan"])):
+        b = g[f"plan_{i}_bins"]
+        bins = None if (b.size == 1 and b[0] == -1) else b
+        S.accumulate_spectra(acc, spectra[int(g[f"plan_{i}_trial"])], bins=bins, count=bool(g[f"plan_{i}_count"]))
+    assert acc.n_trials_accumulated == int(g["n_trials"])
+    fns = {"COHY": M.cohy_bins, **{m: f[0] for m, f in FAM.items()}}
+    tol = {"COHY": 1e-4, **{m: f[2] for m, f in FAM.items()}}
+    for m, fn in fns.items():
+        got, want = fn(acc), g["bins_" + m]
+        assert got.shape == want.shape, m
+        err = np.abs(got - want)
+        assert err.max() <= tol[m], f"{m}: max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
+    kk = int(g["n_trials"])
+    assert np.array_equal(np.rint(M.pli_bins(acc) * kk), np.rint(g["bins_PLI"] * kk))

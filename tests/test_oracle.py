@@ -9,7 +9,7 @@ import pytest
 import oracle as O
 from conftest import GOLDEN, REFERENCE_SRC
 
-CASES = sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "timedomain")
+CASES = sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem not in ("timedomain", "bins_count"))
 
 
 def _load(name):
@@ -83,3 +83,20 @@ def test_oracle_time_domain_matches_reference_golden():
         a, lags = O.xcor(eps, ml)
         assert np.abs(a - g["xcor_w_" + key]).max() <= 1e-12
         assert np.array_equal(lags, g["xcor_lag_" + key])
+
+
+def test_oracle_bins_and_count_match_reference_golden():
+    """accumulate_spectra with column subsets and a count=False back-fill (spectral.py:
+    216-261): the oracle's fold replays tests/golden/bins_count.npz (made by the unmodified
+    reference, make_golden_bins.py)."""
+    g = np.load(GOLDEN / "bins_count.npz")
+    spectra = g["spectra"]
+    K, C, nb = spectra.shape
+    acc = O.Sums(C, nb)
+    for i in range(int(g["n_plan"])):
+        b = g[f"plan_{i}_bins"]
+        bins = None if (b.size == 1 and b[0] == -1) else b
+        O.accumulate(acc, spectra[int(g[f"plan_{i}_trial"])], bins=bins, count=bool(g[f"plan_{i}_count"]))
+    assert acc.n_trials_accumulated == int(g["n_trials"])
+    for m, fn in O.BINS.items():
+        np.testing.assert_allclose(fn(acc), g["bins_" + m], rtol=1e-12, atol=1e-12, err_msg=m)
