@@ -81,7 +81,8 @@ struct Plan {
   TileList tc_tiles[kTileCache];
   int tc_tiles_next = 0;
   int4* flags = nullptr;         // fp64-fallback work list (i, j, local bin, -)
-  int* counters = nullptr;       // [0] flagged entries, [1] list overflowed, [2] overflow records
+  int* counters = nullptr;       // [0] flagged entries, [1] list overflowed, [2] overflow records,
+                                 // [3] caller spectra put a non-real value into an exactly-real bin
   int4* recs = nullptr;          // guard overflow records (3 int4 each), grown on demand
   size_t rec_cap = 0;            // records
   int flag_cap = 0;
@@ -99,8 +100,8 @@ struct Plan {
   bool prep_valid = false;
   bool reuse_prep = false;       // set for the duration of one call
   bool imag_handoff = false;     // the last call handed IMAGCOHY from K2 to K3
-  bool spectra_put = false;      // caller spectra entered the ring (cs_put_spectra): DC / Nyquist may
-                                 // be complex, so the phase-lag kernel must not treat them as real
+  bool spectra_put = false;      // caller spectra entered the ring (cs_put_spectra): counters[3] says
+                                 // whether one was complex at DC / Nyquist (then those bins are not real)
   // multi-GPU (shard.cu): peers' rings attached by cs_ring_attach[_ptrs]
   int n_ranks = 0, rank = 0, node_block = 0;  // node n's fp64 spectra live on rank n / node_block
   double2** peer_x64 = nullptr;  // device [n_ranks] fp64 ring of every rank (own included)

@@ -383,9 +383,15 @@ int run_lag_family(Plan& p, const int* slots, int K, unsigned mask, int bin_lo, 
   a.bin_lo = bin_lo; a.nbb = nbb;
   a.psd = p.psd; a.mag = p.mag;
   // exactly-real bins (DC := 0 and the real Nyquist bin of K1's spectra) are resolved in the
-  // epilogue without the fp64 fallback; caller spectra (cs_put_spectra) may be complex there
-  a.real0 = p.spectra_put ? -1 : p.dc_local;
-  a.real1 = p.spectra_put ? -1 : p.nyq_local;
+  // epilogue without the fp64 fallback; caller spectra (cs_put_spectra) may be complex there,
+  // which k_put_spectra records in counters[3] (read here only when caller spectra were put)
+  int complex_edge = 0;
+  if (p.spectra_put) {
+    cudaMemcpyAsync(&complex_edge, p.counters + 3, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+  }
+  a.real0 = complex_edge ? -1 : p.dc_local;
+  a.real1 = complex_edge ? -1 : p.nyq_local;
   a.nt = (p.N + kTile - 1) / kTile;
   a.row_begin = rb;
   a.pair_base = out->pair_base;

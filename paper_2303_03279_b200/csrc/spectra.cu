@@ -545,7 +545,8 @@ extern "C" int cs_probe_peaks(int device, double* fp32_lane_ops, double* fp64_fm
 namespace cs {
 __global__ void k_put_spectra(const double2* __restrict__ src, int n, int N, int nb, int L, int bin_lo,
                               int nbins, int slot0, int slot_cap, int taper, double w, float scale,
-                              double2* __restrict__ X64, float2* __restrict__ X32) {
+                              double2* __restrict__ X64, float2* __restrict__ X32, int real0, int real1,
+                              int* __restrict__ complex_edge) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
   if (idx >= (int64_t)N * nbins) return;
@@ -557,12 +558,15 @@ __global__ void k_put_spectra(const double2* __restrict__ src, int n, int N, int
   const int64_t o = (((int64_t)slot * L + taper) * nb + bin_lo + bl) * N + node;
   X64[o] = v;
   X32[o] = make_float2((float)(v.x * (double)scale), (float)(v.y * (double)scale));
+  // a caller spectrum that is not exactly real at DC / Nyquist: the phase-lag kernel must fold
+  // those bins like any other (spectral.py:216-241) instead of treating them as real
+  if (v.y != 0.0 && (bin_lo + bl == real0 || bin_lo + bl == real1)) atomicOr(complex_edge, 1);
 }
 void run_put_spectra(const Plan& p, const void* src, int n, int bin_lo, int nbins, int slot0, int taper, double w,
                      cudaStream_t st) {
   dim3 grid((unsigned)(((int64_t)p.N * nbins + 255) / 256), n);
   k_put_spectra<<<grid, 256, 0, st>>>((const double2*)src, n, p.N, p.nb, p.L, bin_lo, nbins, slot0, p.slot_cap,
-                                       taper, w, p.scale, p.X64, p.X32);
+                                       taper, w, p.scale, p.X64, p.X32, p.dc_local, p.nyq_local, p.counters + 3);
 }
 }  // namespace cs
 
