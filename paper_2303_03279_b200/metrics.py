@@ -231,6 +231,15 @@ def compute_metric(epochs, metric: MetricId, nfft: int, band: FrequencyBand | No
         raise ParameterError("need at least one epoch")
     if nfft < 2:
         raise ParameterError(f"nfft must be >= 2, got {nfft}")
+    if len({tuple(e.data.shape) for e in epochs}) > 1:
+        # epochs of different lengths: each is cropped / padded to nfft on its own, as the
+        # reference's per-trial path does (spectral.py:49-97, metrics.py:541-551)
+        acc = SpectrumSet(epochs[0].n_channels, nfft)
+        for e in epochs:
+            spectral.accumulate_epoch(acc, e, taper=taper)
+        if band is None:
+            band = FrequencyBand(0, acc.n_bins - 1, epochs[0].sfreq / nfft)
+        return finalize_spectral(acc, metric, band, positions=positions, node_ids=node_ids)
     x, T = _stack_epochs(epochs)
     K, C = x.shape[0], x.shape[1]
     if band is None:

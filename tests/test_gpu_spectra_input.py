@@ -117,3 +117,19 @@ def test_bins_and_count_against_the_reference():
         assert err.max() <= tol[m], f"{m}: max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
     kk = int(g["n_trials"])
     assert np.array_equal(np.rint(M.pli_bins(acc) * kk), np.rint(g["bins_PLI"] * kk))
+
+
+@pytest.mark.parametrize("metric", ["COH", "IMAGCOHY", "PLV", "PLI", "USPLI", "WPLI", "DSWPLI", "COHY"])
+def test_compute_metric_epochs_of_different_lengths(metric):
+    """compute_metric over epochs of different lengths (some cropped to nfft, some padded):
+    every epoch is conditioned on its own, as in the reference (metrics.py:541-551)."""
+    from paper_2303_03279_b200 import EpochMatrix, MetricId, compute_metric
+    rng = np.random.default_rng(5)
+    C, nfft = 9, 128
+    data = [rng.standard_normal((C, T)) for T in (90, 128, 200, 64, 128, 300, 150)]
+    data[2][3] = 0.5 * data[2][1]
+    net = compute_metric([EpochMatrix(d, 500.0) for d in data], MetricId.parse(metric), nfft)
+    want, _ = O.compute(data, nfft, 0, nfft // 2, (metric,))
+    ref = want[metric]["band"] if metric != "COHY" else np.abs(want[metric]["cband"])
+    tol = 1e-4 if metric in ("COH", "IMAGCOHY", "PLV", "COHY") else 1e-3
+    assert np.abs(np.asarray(net.weights) - ref).max() <= tol
