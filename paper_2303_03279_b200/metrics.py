@@ -349,6 +349,8 @@ class ConnectivityEngine:
         self._next_slot = 0
         self._slot_of: dict = {}
         self._seg0_of: dict = {}     # welch: slot holding only the first segment (the cached spectra)
+        self._mixed = False          # widened ring: every trial through _slot_other_length
+        self._plans_by_length: dict = {}
         self._sum_trials: list = []
         self._fold_slots: list = []  # ring slot of every fold, in order
         self.n_trials = 0
@@ -380,24 +382,110 @@ class ConnectivityEngine:
                     e.validate()
 
     # -- ring ------------------------------------------------------------------
-    def _ensure_plan(self, T: int, scale: float):
-        if self._plan is not None and T != self._T:
-            raise ParameterError("epochs of one engine must share n_samples")
+    def _ensure_plan(self, T: int, scale: float, n_tapers: int = 0):
+        """Room for two more slots (and ``n_tapers`` taper slots per trial).  The ring
+        is grown by doubling; it is widened only for a welch trial with more segments
+        than the ring holds, after which it is a rectangular ring filled through
+        per-length plans (``_mixed``)."""
         need = self._next_slot + 2
-        if self._plan is None or need > self._plan.slot_capacity:
-            cap = self._slot_capacity if self._plan is None else 2 * self._plan.slot_capacity
+        grow = self._plan is None or need > self._plan.slot_capacity
+        widen = self._plan is not None and n_tapers > self._plan.n_tapers
+        if not (grow or widen):
+            return
+        dev = spectral._device()
+        if self._plan is None:
             new = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper,
-                             slot_capacity=cap, device=spectral._device(),
-                             scale=self._plan.scale if self._plan is not None else scale,
+                             slot_capacity=self._slot_capacity, device=dev, scale=scale,
                              welch=self.spectral_mode == "welch")
-            if self._plan is not None:
-                o64, o32 = self._plan.ring()
-                n64, n32 = new.ring()
-                n64[: o64.shape[0]].copy_(o64)
-                n32[: o32.shape[0]].copy_(o32)
-            self._plan = new
             self._T = T
-            self.cache.bytes_per_trial = self.n_channels * self.n_bins * 24 * new.n_tapers
+        else:
+            cap = 2 * self._plan.slot_capacity if grow else self._plan.slot_capacity
+            self._mixed = self._mixed or widen
+            if self._mixed:
+                new = DevicePlan(self.n_channels, self._T, self.nfft, 0, self.n_bins - 1, slot_capacity=cap,
+                                 device=dev, scale=self._plan.scale,
+                                 n_tapers=max(n_tapers, self._plan.n_tapers))
+            else:
+                new = DevicePlan(self.n_channels, self._T, self.nfft, 0, self.n_bins - 1, taper=self.taper,
+                                 slot_capacity=cap, device=dev, scale=self._plan.scale,
+                                 welch=self.spectral_mode == "welch")
+            o64, o32 = self._plan.ring()
+            n64, n32 = new.ring()
+            L = o64.shape[1]
+            n64[: o64.shape[0], :L].copy_(o64)
+            n32[: o32.shape[0], :L].copy_(o32)
+            n64[: o64.shape[0], L:].zero_()    # segments a widened ring adds: nothing folded
+            n32[: o32.shape[0], L:].zero_()
+        self._plan = new
+        self.cache.bytes_per_trial = self.n_channels * self.n_bins * 24 * new.n_tapers
+
+    def _length_plan(self, T: int) -> DevicePlan:
+        """K1 plan for trials of ``T`` samples other than the ring's own length
+        (same taper / welch rule and fp32 scale as the ring)."""
+        p = self._plans_by_length.get(T)
+        if p is None:
+            p = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper, slot_capacity=1,
+                           device=spectral._device(), scale=self._plan.scale, welch=self.spectral_mode == "welch")
+            self._plans_by_length[T] = p
+        return p
+
+    def _slot_other_length(self, x: torch.Tensor, idx) -> int:
+        """A trial whose length differs from the ring's: its own plan computes the
+        spectra (crop / pad to nfft, or welch segments when n_samples >= 2 nfft --
+        spectral.py:264-286 decides per trial), copied into a ring slot; taper slots
+        past its own segments stay zero, which adds nothing to any sum."""
+        aux = self._length_plan(x.shape[1])
+        L = aux.n_tapers
+        self._ensure_plan(self._T, 1.0, n_tapers=L)
+        aux.spectra(x[None].contiguous(), 0)
+        spectral._count_ffts(self.n_channels * L)
+        a64, a32 = aux.ring()
+        r64, r32 = self._plan.ring()
+        slot = self._next_slot
+        self._next_slot += 1
+        r64[slot, L:].zero_()
+        r32[slot, L:].zero_()
+        r64[slot, :L].copy_(a64[0])
+        r32[slot, :L].copy_(a32[0])
+        if aux.welch:
+            s0 = self._next_slot
+            self._next_slot += 1
+            r64[s0].zero_()
+            r32[s0].zero_()
+            r64[s0, 0].copy_(a64[0, 0])
+            r32[s0, 0].copy_(a32[0, 0])
+            w = 1.0 / float(np.sqrt(L))
+            r64[slot].mul_(w)
+            r32[slot].mul_(w)
+            self._seg0_of[idx] = s0
+        return slot
+
+    def _slot_ring_length(self, x: torch.Tensor, idx, data) -> int:
+        # the fp32 scale is fixed by the first trial (host data: no device sync)
+        scale = 1.0 if self._plan is not None else pow2_scale(_abs_max(data), min(x.shape[1], self.nfft))
+        self._ensure_plan(x.shape[1], scale)
+        slot = self._next_slot
+        self._next_slot += 1
+        self._plan.spectra(x[None].contiguous(), slot)
+        spectral._count_ffts(self.n_channels * self._plan.n_tapers)
+        if self._plan.welch:
+            # the reference caches the first segment's spectra (spectral.py:286) and
+            # re-folds cached trials in fixed mode (metrics.py:337-341, 450-460):
+            # keep that segment in a slot of its own, then weight the welch slot's
+            # S segments by 1/sqrt(S) so its summed CSD is the segment mean
+            S = self._plan.n_tapers
+            r64, r32 = self._plan.ring()
+            s0 = self._next_slot
+            self._next_slot += 1
+            r64[s0].zero_()
+            r32[s0].zero_()
+            r64[s0, 0].copy_(r64[slot, 0])
+            r32[s0, 0].copy_(r32[slot, 0])
+            w = 1.0 / float(np.sqrt(S))
+            r64[slot].mul_(w)
+            r32[slot].mul_(w)
+            self._seg0_of[idx] = s0
+        return slot
 
     # -- accumulation -------------------------------------------------------------
     def add_trial(self, epoch: EpochMatrix) -> None:
@@ -406,30 +494,10 @@ class ConnectivityEngine:
         idx = epoch.trial_index
         if not (self.cache.enabled and idx in self._slot_of):
             x = spectral._as_device_samples(epoch.data)
-            # the fp32 scale is fixed by the first trial (host data: no device sync)
-            scale = 1.0 if self._plan is not None else pow2_scale(_abs_max(epoch.data), min(x.shape[1], self.nfft))
-            self._ensure_plan(x.shape[1], scale)
-            slot = self._next_slot
-            self._next_slot += 1
-            self._plan.spectra(x[None].contiguous(), slot)
-            spectral._count_ffts(self.n_channels * self._plan.n_tapers)
-            if self._plan.welch:
-                # the reference caches the first segment's spectra (spectral.py:286) and
-                # re-folds cached trials in fixed mode (metrics.py:337-341, 450-460):
-                # keep that segment in a slot of its own, then weight the welch slot's
-                # S segments by 1/sqrt(S) so its summed CSD is the segment mean
-                S = self._plan.n_tapers
-                r64, r32 = self._plan.ring()
-                s0 = self._next_slot
-                self._next_slot += 1
-                r64[s0].zero_()
-                r32[s0].zero_()
-                r64[s0, 0].copy_(r64[slot, 0])
-                r32[s0, 0].copy_(r32[slot, 0])
-                w = 1.0 / float(np.sqrt(S))
-                r64[slot].mul_(w)
-                r32[slot].mul_(w)
-                self._seg0_of[idx] = s0
+            if self._plan is not None and (self._mixed or x.shape[1] != self._T):
+                slot = self._slot_other_length(x, idx)
+            else:
+                slot = self._slot_ring_length(x, idx, epoch.data)
             self._slot_of[idx] = slot
             if self.cache.enabled:
                 self.cache.spectra[idx] = slot
@@ -449,13 +517,17 @@ class ConnectivityEngine:
         self.n_trials += 1
 
     def _xcor_add(self, epochs) -> None:
-        max_lag = self.max_lag if self.max_lag is not None else epochs[0].n_samples - 1
-        pk, lg = timedomain.xcor_sums([e.data for e in epochs], self.n_channels, max_lag)
-        if self._xcor_peak_sum is None:
-            self._xcor_peak_sum, self._xcor_lag_sum = pk, lg
-        else:
-            self._xcor_peak_sum += pk
-            self._xcor_lag_sum += lg
+        # without a max_lag each trial uses its own n_samples - 1 (metrics.py:385)
+        groups: dict = {}
+        for e in epochs:
+            groups.setdefault(self.max_lag if self.max_lag is not None else e.n_samples - 1, []).append(e)
+        for max_lag, grp in groups.items():
+            pk, lg = timedomain.xcor_sums([e.data for e in grp], self.n_channels, max_lag)
+            if self._xcor_peak_sum is None:
+                self._xcor_peak_sum, self._xcor_lag_sum = pk, lg
+            else:
+                self._xcor_peak_sum += pk
+                self._xcor_lag_sum += lg
         self._xcor_trials += len(epochs)
 
     def _finalize_time_domain(self, metric: MetricId, band: FrequencyBand) -> ConnectivityNetwork:
