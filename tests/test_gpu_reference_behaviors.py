@@ -1,0 +1,169 @@
+"""Behaviours the reference's own metric tests pin (reference pkg/tests/test_metrics.py,
+TestCor / TestXcor / TestEngine / TestConvergence), restated on this package's
+public API with independent data and checked against the oracle where a number is
+involved: COR and XCOR (metrics.py:141-260), the engine's time-domain switch and
+back-fill rules, reset, band hints and the FFT-count contract (metrics.py:285-460),
+and convergence_curve (metrics.py:501-528)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2303_03279_b200 import ConnectivityEngine, EpochMatrix, FrequencyBand, MetricId, compute_metric
+from paper_2303_03279_b200 import metrics as M
+from paper_2303_03279_b200 import spectral as S
+from paper_2303_03279_b200.core import ParameterError
+
+pytestmark = pytest.mark.gpu
+
+
+def _epochs(K, C, T, seed, sfreq=600.0):
+    rng = np.random.default_rng(seed)
+    return [EpochMatrix(rng.standard_normal((C, T)), sfreq, trial_index=k) for k in range(K)]
+
+
+# -- COR (metrics.py:141-177) ---------------------------------------------------
+def test_cor_hand_computed_value():
+    # x = (0, 1, 2, 3), y = (0, 2, 1, 3): cov = 4, var = 5 each -> r = 0.8
+    d = np.array([[0.0, 1.0, 2.0, 3.0], [0.0, 2.0, 1.0, 3.0]])
+    assert M.cor([EpochMatrix(d, 20.0)]).weights[0] == pytest.approx(0.8, abs=1e-14)
+
+
+def test_cor_mean_over_trials_against_oracle():
+    eps = _epochs(6, 5, 33, seed=101)
+    got = M.cor(eps).weights
+    want, dead = O.cor([e.data for e in eps])
+    assert not dead
+    assert np.abs(got - want).max() <= 1e-12
+
+
+def test_cor_zero_variance_channel_warns():
+    d = np.vstack([np.arange(20.0), np.full(20, 2.5), np.sin(np.arange(20.0))])
+    net = M.cor([EpochMatrix(d, 20.0)])
+    assert net.weights[0] == 0.0 and net.weights[2] == 0.0        # pairs (0,1) and (1,2)
+    assert any("zero-variance" in w and "1" in w for w in net.warnings)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_cor_bounded_and_duplicate_is_one(seed):
+    d = np.random.default_rng(seed).standard_normal((4, 19))
+    assert np.all(np.abs(M.cor([EpochMatrix(d, 20.0)]).weights) <= 1.0)
+    dup = np.vstack([d[2], d[2]])
+    assert M.cor([EpochMatrix(dup, 20.0)]).weights[0] == pytest.approx(1.0, abs=1e-12)
+
+
+# -- XCOR (metrics.py:180-260) --------------------------------------------------
+def test_xcor_pair_recovers_a_known_delay():
+    base = np.random.default_rng(8).standard_normal(300)
+    d = 9
+    x, y = base[30:-30], np.roll(base, d)[30:-30]    # y lags x by d samples
+    v, lag = M.xcor_pair(x, y, 20)
+    assert lag == -d and v > 0.9                      # negative lag: x leads
+
+
+def test_xcor_pair_identical_constant_and_bound():
+    x = np.random.default_rng(9).standard_normal(70)
+    v, lag = M.xcor_pair(x, x.copy(), 15)
+    assert v == pytest.approx(1.0, abs=1e-10) and lag == 0
+    assert M.xcor_pair(np.full(24, 4.0), np.arange(24.0), 6) == (0.0, 0)
+    with pytest.raises(ParameterError):
+        M.xcor_pair(np.ones(10), np.ones(10), 10)
+
+
+def test_xcor_pair_methods_agree_with_oracle():
+    rng = np.random.default_rng(12)
+    for _ in range(6):
+        x, y = rng.standard_normal(45), rng.standard_normal(45)
+        ml = int(rng.integers(1, 44))
+        ov, ol = O.xcor_pair(x, y, ml)
+        for method in ("fft", "direct"):
+            v, l = M.xcor_pair(x, y, ml, method=method)
+            assert v == pytest.approx(ov, abs=1e-10) and l == ol
+
+
+def test_xcor_network_mean_peak_and_lag():
+    eps = _epochs(4, 4, 50, seed=13)
+    net = M.xcor(eps, max_lag=12)
+    w, lags = O.xcor([e.data for e in eps], max_lag=12)
+    assert np.abs(net.weights - w).max() <= 1e-10
+    assert np.array_equal(np.asarray(net.lags), lags)
+
+
+# -- engine rules (metrics.py:285-460) ------------------------------------------
+def test_late_switch_to_xcor_backfills_from_the_cache():
+    eps = _epochs(5, 4, 45, seed=14)
+    band = FrequencyBand(0, 5, 1.0)
+    eng = ConnectivityEngine(4, 48, 600.0, storage_mode=True, max_lag=11)
+    for e in eps:
+        eng.update_and_finalize(e, MetricId.PLV, band)
+    net = eng.finalize(MetricId.XCOR, band)
+    w, lags = O.xcor([e.data for e in eps], max_lag=11)
+    assert np.abs(net.weights - w).max() <= 1e-10
+    assert np.array_equal(np.asarray(net.lags), lags)
+
+
+def test_late_switch_to_xcor_without_storage_raises():
+    eng = ConnectivityEngine(4, 32, 600.0, storage_mode=False)
+    eng.add_trial(_epochs(1, 4, 32, seed=15)[0])
+    with pytest.raises(ParameterError):
+        eng.finalize(MetricId.XCOR, FrequencyBand(0, 3, 1.0))
+
+
+def test_reset_clears_trials_sums_and_cache():
+    eng = ConnectivityEngine(4, 32, 600.0)
+    for e in _epochs(2, 4, 32, seed=16):
+        eng.add_trial(e)
+    eng.reset()
+    assert eng.n_trials == 0
+    assert eng.acc.n_trials_accumulated == 0
+    assert not eng.cache.spectra and eng.cache.memory_bytes() == 0
+    e = _epochs(1, 4, 32, seed=17)[0]
+    eng.add_trial(e)
+    assert eng.n_trials == 1 and eng.cache.memory_bytes() > 0
+
+
+def test_band_backfill_needs_no_new_ffts_and_matches_batch():
+    eps = _epochs(5, 4, 40, seed=18)
+    eng = ConnectivityEngine(4, 48, 600.0, storage_mode=True, accumulate_band=(8, 14))
+    for e in eps:
+        eng.add_trial(e)
+    S.reset_fft_call_count()
+    wide = FrequencyBand(0, 24, 12.5)
+    got = eng.finalize(MetricId.COH, wide)
+    assert S.fft_call_count() == 0
+    want, _ = O.compute([e.data for e in eps], 48, 0, 24, ("COH",))
+    assert np.abs(got.weights - want["COH"]["band"]).max() <= 1e-4
+
+
+def test_band_hint_is_ignored_without_storage():
+    eps = _epochs(3, 4, 40, seed=19)
+    eng = ConnectivityEngine(4, 48, 600.0, storage_mode=False, accumulate_band=(8, 14))
+    for e in eps:
+        eng.add_trial(e)
+    got = eng.finalize(MetricId.COH, FrequencyBand(0, 24, 12.5))
+    want = compute_metric(eps, MetricId.COH, 48, FrequencyBand(0, 24, 12.5))
+    assert np.abs(got.weights - want.weights).max() <= 1e-6
+
+
+def test_band_hint_outside_the_spectrum_is_rejected():
+    with pytest.raises(ParameterError):
+        ConnectivityEngine(4, 48, 600.0, accumulate_band=(20, 25))
+    with pytest.raises(ParameterError):
+        ConnectivityEngine(4, 48, 600.0, accumulate_band=(-1, 3))
+
+
+# -- convergence_curve (metrics.py:501-528) -------------------------------------
+def test_convergence_curve_counts_and_last_point():
+    eps = _epochs(8, 5, 40, seed=20)
+    band = FrequencyBand(2, 9, 600.0 / 48)
+    counts, curve = M.convergence_curve(eps, MetricId.PLV, 48, band, n_top=4)
+    assert counts.tolist() == list(range(1, 9)) and curve.shape == (8,)
+    want, _ = O.compute([e.data for e in eps], 48, 2, 9, ("PLV",))
+    w = want["PLV"]["band"] / want["PLV"]["band"].max()
+    assert curve[-1] == pytest.approx(np.sort(w)[-4:].mean(), abs=1e-5)
+
+
+@pytest.mark.parametrize("metric", [MetricId.COR, MetricId.XCOR])
+def test_convergence_curve_time_domain(metric):
+    eps = _epochs(5, 4, 40, seed=21)
+    counts, curve = M.convergence_curve(eps, metric, 32, FrequencyBand(0, 3, 1.0), max_lag=7)
+    assert len(curve) == 5 and np.all(np.isfinite(curve))
