@@ -165,12 +165,23 @@ class ConnectivityNetwork:
     first access.
     """
 
-    def __init__(self, metric, band, n_trials, node_ids, positions, weights, edge_i=None, edge_j=None,
+    def __init__(self, metric, band, n_trials, node_ids, positions, edge_i=None, edge_j=None, weights=None,
                  complex_weights=None, lags=None, normalized=False, warnings=(), pairs=None):
-        """pairs: optional device int64 pair indices (triu order) of the edges when
-        they are a subset (thresholded on the device); None = all i < j pairs."""
+        """Fields in the reference dataclass's order (core.py:130-141), so positional
+        construction by reference callers keeps working.  edge_i / edge_j may be
+        omitted: then the edges are all i < j pairs, or ``pairs`` -- optional device
+        int64 pair indices (triu order) when they are a subset thresholded on the device."""
+        if weights is None:
+            raise ParameterError("weights are required")
         if n_trials < 1:
             raise ParameterError("n_trials must be >= 1")
+        if edge_i is not None or edge_j is not None:
+            if edge_i is None or edge_j is None:
+                raise ParameterError("edge_i and edge_j go together")
+            edge_i = np.asarray(edge_i, dtype=np.int64)
+            edge_j = np.asarray(edge_j, dtype=np.int64)
+            if np.any(edge_i >= edge_j):
+                raise ParameterError("edges must satisfy i < j")
         self._pairs = pairs
         self.metric = metric
         self.band = band
@@ -253,7 +264,10 @@ class ConnectivityNetwork:
                  complex_weights=self._cw, lags=self.lags, normalized=self.normalized, warnings=self.warnings,
                  pairs=self._pairs)
         d.update(kw)
-        return ConnectivityNetwork(**d)
+        ei, ej = d.pop("edge_i"), d.pop("edge_j")
+        net = ConnectivityNetwork(**d)
+        net._ei, net._ej = ei, ej        # subsets of validated edges: no second i < j pass
+        return net
 
     @property
     def n_nodes(self) -> int:
@@ -394,5 +408,5 @@ def deserialize_network(raw: bytes) -> ConnectivityNetwork:
         cw = np.sqrt(np.maximum(w * w - im * im, 0.0)) + 1j * im
     if any(e["lag"] is not None for e in edges):
         lags = np.array([e["lag"] or 0 for e in edges], dtype=np.int64)
-    return ConnectivityNetwork(MetricId.parse(obj["metric"]), band, obj["n_trials"], node_ids, positions, w,
-                               edge_i=ei, edge_j=ej, complex_weights=cw, lags=lags, normalized=obj["normalized"])
+    return ConnectivityNetwork(MetricId.parse(obj["metric"]), band, obj["n_trials"], node_ids, positions, ei, ej, w,
+                               complex_weights=cw, lags=lags, normalized=obj["normalized"])

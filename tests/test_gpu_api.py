@@ -524,7 +524,7 @@ def test_device_threshold_matches_host_semantics(P, ties):
     while n * (n - 1) // 2 < P:
         n += 1
     wd = torch.tensor(w, device="cuda")
-    net = ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 2, tuple(range(n)), np.zeros((n, 3)), wd)
+    net = ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 2, tuple(range(n)), np.zeros((n, 3)), weights=wd)
     for f in (1e-6, 0.01, 0.37, 1.0):
         k = int(np.ceil(f * P))
         got = threshold_network(net, f)

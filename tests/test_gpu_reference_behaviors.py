@@ -167,3 +167,44 @@ def test_convergence_curve_time_domain(metric):
     eps = _epochs(5, 4, 40, seed=21)
     counts, curve = M.convergence_curve(eps, metric, 32, FrequencyBand(0, 3, 1.0), max_lag=7)
     assert len(curve) == 5 and np.all(np.isfinite(curve))
+
+
+# -- SpectrumSet / fft_real (spectral.py:65-201) --------------------------------
+def test_csd_entry_is_hermitian_and_matches_oracle():
+    eps = _epochs(4, 6, 45, seed=22)
+    acc = S.SpectrumSet(6, 32)
+    ref = O.Sums(6, 17)
+    for e in eps:
+        S.accumulate_epoch(acc, e)
+        O.accumulate(ref, O.trial_spectra(e.data, 32))
+    pi, pj = O.pair_index(6)
+    for i in range(6):
+        assert np.abs(acc.csd_entry(i, i).imag).max() == 0.0          # diagonal: the PSD sum
+        assert np.abs(acc.csd_entry(i, i).real - ref.psd_sum[i]).max() <= 1e-9
+        for j in range(6):
+            if i != j:
+                assert np.array_equal(acc.csd_entry(i, j), np.conj(acc.csd_entry(j, i)))
+    k = 7
+    assert np.abs(acc.csd_entry(pi[k], pj[k]) - ref.csd_sum[k]).max() <= 1e-9
+
+
+def test_merge_of_mismatched_sets_is_rejected():
+    with pytest.raises(ParameterError):
+        S.SpectrumSet(3, 24).merge(S.SpectrumSet(4, 24))
+    with pytest.raises(ParameterError):
+        S.SpectrumSet(3, 24).merge(S.SpectrumSet(3, 32))
+
+
+def test_fft_real_parseval_and_crop_pad():
+    rng = np.random.default_rng(23)
+    x = rng.standard_normal(64)
+    X = S.fft_real(x, 64)
+    xd = x - x.mean()
+    # one-sided spectrum: interior bins count twice, DC (zero) and Nyquist once
+    energy = (np.abs(X[0]) ** 2 + 2 * np.sum(np.abs(X[1:-1]) ** 2) + np.abs(X[-1]) ** 2) / 64
+    assert energy == pytest.approx(np.sum(xd ** 2), rel=1e-12)
+    y = rng.standard_normal(100)                                    # cropped to nfft
+    assert np.abs(S.fft_real(y, 64) - O.trial_spectra(y[None, :64], 64)[0]).max() <= 1e-9
+    z = np.array([2.0, -1.0, 0.5, 3.0, -0.25])                      # zero-padded to nfft
+    got = S.fft_real(z, 16)
+    assert got.shape == (9,) and np.abs(got - O.trial_spectra(z[None], 16)[0]).max() <= 1e-12

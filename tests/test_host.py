@@ -108,7 +108,7 @@ def test_synthetic_generation_is_node_subset_stable():
 def _net(w, n_nodes, cw=None, lags=None):
     from paper_2303_03279_b200.core import ConnectivityNetwork
     return ConnectivityNetwork(MetricId.COH, FrequencyBand(2, 5, 1.0), 3, tuple(range(n_nodes)),
-                               np.zeros((n_nodes, 3)), np.asarray(w, dtype=np.float64), complex_weights=cw, lags=lags)
+                               np.zeros((n_nodes, 3)), weights=np.asarray(w, dtype=np.float64), complex_weights=cw, lags=lags)
 
 
 def test_pair_to_ij_inverts_triu_order():
@@ -157,3 +157,66 @@ def test_post_processing_matches_reference_functions():
         assert np.array_equal(a.weights, b.weights) and np.array_equal(a.complex_weights, b.complex_weights)
         assert np.array_equal(a.lags, b.lags)
         assert RC.serialize_network(a) == serialize_network(b)
+
+
+def test_network_fields_in_reference_order_and_wire_format():
+    """Positional construction in the reference dataclass's field order (core.py:130-141),
+    its i < j validation, and the JSON wire format: key order, byte-level round trip
+    (core.py:218-273)."""
+    import json
+    from paper_2303_03279_b200.core import ConnectivityNetwork, deserialize_network, serialize_network
+    band = FrequencyBand(1, 4, 2.0)
+    net = ConnectivityNetwork(MetricId.IMAGCOHY, band, 5, (0, 1, 2), np.zeros((3, 3)), np.array([0, 0, 1]),
+                              np.array([1, 2, 2]), np.array([0.5, -0.25, 0.125]), None, np.array([2, 0, -3]))
+    assert net.n_edges == 3 and net.edge_j.tolist() == [1, 2, 2] and net.lags.tolist() == [2, 0, -3]
+    raw = serialize_network(net)
+    obj = json.loads(raw)
+    assert list(obj) == ["metric", "band", "n_trials", "normalized", "nodes", "edges"]
+    assert list(obj["edges"][0]) == ["i", "j", "w", "w_im", "lag"] and obj["edges"][2]["lag"] == -3
+    back = deserialize_network(raw)
+    assert serialize_network(back) == raw
+    assert back.metric is MetricId.IMAGCOHY and back.band == band
+    assert np.array_equal(back.edge_i, net.edge_i) and np.array_equal(back.weights, net.weights)
+    cw = np.array([0.3 + 0.4j, 0.25 + 0j, -0.125j])
+    c = ConnectivityNetwork(MetricId.COHY, band, 2, (0, 1, 2), np.zeros((3, 3)), [0, 0, 1], [1, 2, 2],
+                            np.abs(cw), complex_weights=cw)
+    assert json.loads(serialize_network(c))["edges"][0]["w_im"] == 0.4
+    with pytest.raises(ParameterError):
+        ConnectivityNetwork(MetricId.COH, band, 1, (0, 1), np.zeros((2, 3)), np.array([1]), np.array([0]),
+                            np.array([0.5]))
+    with pytest.raises(ParameterError):
+        ConnectivityNetwork(MetricId.COH, band, 1, (0, 1), np.zeros((2, 3)), [0], [1], [np.inf])
+
+
+def test_threshold_count_and_dominance_property():
+    """threshold_network keeps ceil(f n) edges and every kept |w| >= every dropped |w|
+    (core.py:184-205), ties toward ascending (i, j)."""
+    from hypothesis import given, settings, strategies as st
+    from paper_2303_03279_b200.core import normalize_network, threshold_network
+
+    @given(st.lists(st.floats(-1, 1, allow_nan=False), min_size=1, max_size=36), st.floats(0.01, 1.0))
+    @settings(max_examples=60, deadline=None)
+    def check(ws, frac):
+        n = 2
+        while n * (n - 1) // 2 < len(ws):
+            n += 1
+        i, j = np.triu_indices(n, 1)
+        from paper_2303_03279_b200.core import ConnectivityNetwork
+        net = ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 1, tuple(range(n)), np.zeros((n, 3)),
+                                  i[:len(ws)], j[:len(ws)], np.array(ws))
+        kept = threshold_network(net, frac)
+        assert kept.n_edges == int(np.ceil(frac * len(ws)))
+        ke = set(zip(kept.edge_i.tolist(), kept.edge_j.tolist()))
+        dropped = [abs(w) for a, b, w in zip(net.edge_i.tolist(), net.edge_j.tolist(), ws) if (a, b) not in ke]
+        if dropped and kept.n_edges:
+            assert min(abs(v) for v in kept.weights) >= max(dropped)
+
+    check()
+    from paper_2303_03279_b200.core import ConnectivityNetwork
+    tie = ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 1, tuple(range(4)), np.zeros((4, 3)),
+                              *np.triu_indices(4, 1), np.full(6, 0.5))
+    t = threshold_network(tie, 0.5)
+    assert list(zip(t.edge_i.tolist(), t.edge_j.tolist())) == [(0, 1), (0, 2), (0, 3)]
+    with pytest.raises(ParameterError):
+        normalize_network(ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 1, (0, 1), np.zeros((2, 3)),
+                                              np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)))
