@@ -208,3 +208,27 @@ def test_fft_real_parseval_and_crop_pad():
     z = np.array([2.0, -1.0, 0.5, 3.0, -0.25])                      # zero-padded to nfft
     got = S.fft_real(z, 16)
     assert got.shape == (9,) and np.abs(got - O.trial_spectra(z[None], 16)[0]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("nfft,T", [(63, 50), (63, 80), (9, 9), (255, 300)])
+def test_odd_nfft_has_no_nyquist_bin(nfft, T):
+    """Odd nfft (np.fft.rfft: nfft // 2 + 1 bins, the last one complex, not a Nyquist bin):
+    every spectral metric over all bins against the oracle, including the last bin's
+    phase-lag terms."""
+    rng = np.random.default_rng(nfft + T)
+    data = [rng.standard_normal((7, T)) for _ in range(9)]
+    data[0][3] = 0.5 * data[0][2]
+    hi = nfft // 2
+    want, _ = O.compute(data, nfft, 0, hi, ("COH", "IMAGCOHY", "PLV", "PLI", "WPLI", "DSWPLI", "USPLI"))
+    assert np.abs(want["PLI"]["bins"][:, -1]).max() > 0          # the last bin carries phase
+    band = FrequencyBand(0, hi, 500.0 / nfft)
+    for m, tol in (("COH", 1e-4), ("IMAGCOHY", 1e-4), ("PLV", 1e-4), ("PLI", 1e-3), ("WPLI", 1e-3),
+                   ("DSWPLI", 1e-3), ("USPLI", 1e-3)):
+        net = compute_metric([EpochMatrix(d, 500.0) for d in data], MetricId.parse(m), nfft, band)
+        assert np.abs(net.weights - want[m]["band"]).max() <= tol, m
+    acc = S.SpectrumSet(7, nfft)
+    for d in data:
+        S.accumulate_epoch(acc, EpochMatrix(d, 500.0))
+    assert acc.n_bins == hi + 1
+    assert np.abs(M.pli_bins(acc) - want["PLI"]["bins"]).max() <= 1e-3
+    assert np.abs(M.imagcohy_bins(acc) - want["IMAGCOHY"]["bins"]).max() <= 1e-4
