@@ -395,11 +395,11 @@ class ConnectivityEngine:
         dev = spectral._device()
         if self._plan is None:
             new = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper,
-                             slot_capacity=self._slot_capacity, device=dev, scale=scale,
+                             slot_capacity=max(self._slot_capacity, need), device=dev, scale=scale,
                              welch=self.spectral_mode == "welch")
             self._T = T
         else:
-            cap = 2 * self._plan.slot_capacity if grow else self._plan.slot_capacity
+            cap = max(2 * self._plan.slot_capacity, need) if grow else self._plan.slot_capacity
             self._mixed = self._mixed or widen
             if self._mixed:
                 new = DevicePlan(self.n_channels, self._T, self.nfft, 0, self.n_bins - 1, slot_capacity=cap,
@@ -424,6 +424,8 @@ class ConnectivityEngine:
         (same taper / welch rule and fp32 scale as the ring)."""
         p = self._plans_by_length.get(T)
         if p is None:
+            if len(self._plans_by_length) >= 8:      # bounded: one plan per recent length
+                self._plans_by_length.pop(next(iter(self._plans_by_length)))
             p = DevicePlan(self.n_channels, T, self.nfft, 0, self.n_bins - 1, taper=self.taper, slot_capacity=1,
                            device=spectral._device(), scale=self._plan.scale, welch=self.spectral_mode == "welch")
             self._plans_by_length[T] = p

@@ -63,12 +63,12 @@ def _fold(acc, ep, nfft, mode, taper=None):
         O.accumulate(acc, O.trial_spectra(ep, nfft))
 
 
-@pytest.mark.parametrize("storage", [True, False])
-def test_fixed_mode_trials_of_different_lengths(storage):
+@pytest.mark.parametrize("storage,cap", [(True, 64), (False, 64), (True, 1)])
+def test_fixed_mode_trials_of_different_lengths(storage, cap):
     C, nfft, sfreq = 10, 128, 250.0
     lengths = (100, 128, 256, 60, 128, 300, 131)
     data = _data(lengths, C)
-    eng = ConnectivityEngine(C, nfft, sfreq, storage_mode=storage)
+    eng = ConnectivityEngine(C, nfft, sfreq, storage_mode=storage, slot_capacity=cap)
     acc = O.Sums(C, nfft // 2 + 1)
     lo, hi = 4, 30
     band = FrequencyBand(lo, hi, sfreq / nfft)
@@ -86,13 +86,15 @@ def test_fixed_mode_trials_of_different_lengths(storage):
     assert np.abs(np.asarray(net.weights) - O.cor(data)[0]).max() <= 1e-9
 
 
-def test_welch_mode_segment_counts_grow_past_the_ring():
+@pytest.mark.parametrize("cap", [64, 1])
+def test_welch_mode_segment_counts_grow_past_the_ring(cap):
     """First trial shorter than 2 nfft (a one-segment ring), then 2, 4 and 3 segments
-    and a short trial again; rebuild_last re-folds the cached first segments."""
+    and a short trial again; rebuild_last re-folds the cached first segments.  cap = 1:
+    the ring also doubles its slots while it is widened."""
     C, nfft, sfreq = 10, 64, 250.0
     lengths = (100, 130, 256, 64, 200, 90)
     data = _data(lengths, C, seed=3)
-    eng = ConnectivityEngine(C, nfft, sfreq, storage_mode=True, spectral_mode="welch")
+    eng = ConnectivityEngine(C, nfft, sfreq, storage_mode=True, spectral_mode="welch", slot_capacity=cap)
     acc = O.Sums(C, nfft // 2 + 1)
     lo, hi = 2, 20
     band = FrequencyBand(lo, hi, sfreq / nfft)
