@@ -605,7 +605,7 @@ class ConnectivityEngine:
         a new slot list over the cached spectra, no FFTs and no re-fold."""
         if not self.cache.enabled:
             raise ParameterError("trial-window rebuild requires storage mode")
-        keep = sorted(self.cache.epochs)[-n_last:] if n_last > 0 else []
+        keep = sorted(self.cache.epochs)[-n_last:]   # as the reference slices: n_last = 0 keeps all
         # the reference resets (time-domain sums included) and re-adds the kept trials
         self._xcor_peak_sum = self._xcor_lag_sum = None
         self._xcor_trials = 0

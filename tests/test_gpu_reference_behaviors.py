@@ -232,3 +232,21 @@ def test_odd_nfft_has_no_nyquist_bin(nfft, T):
     assert acc.n_bins == hi + 1
     assert np.abs(M.pli_bins(acc) - want["PLI"]["bins"]).max() <= 1e-3
     assert np.abs(M.imagcohy_bins(acc) - want["IMAGCOHY"]["bins"]).max() <= 1e-4
+
+
+@pytest.mark.parametrize("n_last,kept", [(2, [3, 4]), (0, [0, 1, 2, 3, 4]), (-2, [2, 3, 4]), (9, [0, 1, 2, 3, 4])])
+def test_rebuild_last_slices_like_the_reference(n_last, kept):
+    """rebuild_last keeps sorted(cache)[-n_last:] (metrics.py:450-460): n_last = 0 keeps
+    every cached trial, a negative count drops the oldest |n_last|."""
+    eps = _epochs(5, 5, 48, seed=30)
+    eng = ConnectivityEngine(5, 48, 600.0, storage_mode=True)
+    for e in reversed(eps):                       # cache order is by trial index, not arrival
+        eng.add_trial(e)
+    eng.rebuild_last(n_last)
+    assert eng.n_trials == len(kept) and eng.acc.n_trials_accumulated == len(kept)
+    band = FrequencyBand(2, 10, 12.5)
+    want, _ = O.compute([eps[k].data for k in kept], 48, 2, 10, ("PLV", "WPLI"))
+    for m in ("PLV", "WPLI"):
+        assert np.abs(eng.finalize(MetricId.parse(m), band).weights - want[m]["band"]).max() <= 1e-3, m
+    w, _ = O.cor([eps[k].data for k in kept])
+    assert np.abs(eng.finalize(MetricId.COR, band).weights - w).max() <= 1e-12
