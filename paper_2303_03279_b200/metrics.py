@@ -681,6 +681,8 @@ def convergence_curve(epochs, metric: MetricId, nfft: int, band: FrequencyBand, 
     snapshots, counts = [], []
     for k, ep in enumerate(epochs, start=1):
         engine.add_trial(ep)
+        if metric is MetricId.XCOR:
+            engine._xcor_add([ep])     # the trial itself, as the reference does (not the cache by index)
         try:
             net = engine.finalize(metric, band)
         except DegenerateTrialCountError:

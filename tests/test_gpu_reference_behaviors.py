@@ -250,3 +250,19 @@ def test_rebuild_last_slices_like_the_reference(n_last, kept):
         assert np.abs(eng.finalize(MetricId.parse(m), band).weights - want[m]["band"]).max() <= 1e-3, m
     w, _ = O.cor([eps[k].data for k in kept])
     assert np.abs(eng.finalize(MetricId.COR, band).weights - w).max() <= 1e-12
+
+
+def test_convergence_curve_xcor_uses_each_trial_even_with_repeated_indices():
+    """convergence_curve folds XCOR peaks from every epoch it is given (metrics.py:517-518),
+    so epochs that share the default trial_index still count one by one."""
+    rng = np.random.default_rng(31)
+    data = [rng.standard_normal((4, 40)) for _ in range(5)]
+    eps = [EpochMatrix(d, 600.0) for d in data]            # all trial_index 0
+    counts, curve = M.convergence_curve(eps, MetricId.XCOR, 32, FrequencyBand(0, 3, 1.0), n_top=3, max_lag=6)
+    assert counts.tolist() == [1, 2, 3, 4, 5]
+    snaps = []
+    for k in range(1, 6):
+        w, _ = O.xcor(data[:k], max_lag=6)
+        snaps.append(w / w.max())
+    top = np.argsort(-snaps[-1])[:3]
+    assert np.abs(curve - np.array([s[top].mean() for s in snaps])).max() <= 1e-9
