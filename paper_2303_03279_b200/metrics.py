@@ -352,6 +352,7 @@ class ConnectivityEngine:
         self._mixed = False          # widened ring: every trial through _slot_other_length
         self._plans_by_length: dict = {}
         self._sum_trials: list = []
+        self._fold_epochs: list = []  # the epoch given at each fold (COR sums, metrics.py:355-357)
         self._fold_slots: list = []  # ring slot of every fold, in order
         self.n_trials = 0
         # time-domain state (metrics.py:320-326): COR sums are kept eagerly only
@@ -515,6 +516,7 @@ class ConnectivityEngine:
             self._cor_sum = w if self._cor_sum is None else self._cor_sum + w
             self._dead_channels.update(dead)
         self._sum_trials.append(idx)
+        self._fold_epochs.append(epoch)
         self._fold_slots.append(fold_slot)
         self.n_trials += 1
 
@@ -537,7 +539,7 @@ class ConnectivityEngine:
             raise DegenerateTrialCountError("no trials accumulated")
         if metric is MetricId.COR:
             if self.cache.enabled:
-                total, dead = timedomain.cor_sums([self.cache.epochs[i].data for i in self._sum_trials],
+                total, dead = timedomain.cor_sums([e.data for e in self._fold_epochs],
                                                   self.n_channels)
             else:
                 total, dead = self._cor_sum, sorted(self._dead_channels)
@@ -610,6 +612,7 @@ class ConnectivityEngine:
         self._xcor_peak_sum = self._xcor_lag_sum = None
         self._xcor_trials = 0
         self._sum_trials = list(keep)
+        self._fold_epochs = [self.cache.epochs[i] for i in keep]
         self._init_cols()   # the reference's reset() restores the accumulate-band mask
         # re-added from the cache: fixed-mode folds of the cached spectra
         self._fold_slots = [self._seg0_of.get(i, self._slot_of[i]) for i in keep]

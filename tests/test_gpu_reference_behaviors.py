@@ -266,3 +266,22 @@ def test_convergence_curve_xcor_uses_each_trial_even_with_repeated_indices():
         snaps.append(w / w.max())
     top = np.argsort(-snaps[-1])[:3]
     assert np.abs(curve - np.array([s[top].mean() for s in snaps])).max() <= 1e-9
+
+
+def test_repeated_trial_index_folds_cached_spectra_but_cor_sees_each_epoch():
+    """With storage on, an epoch whose trial_index is already cached re-folds the cached
+    spectra (metrics.py:341-343) -- here every epoch has the default index 0, so the
+    spectral sums hold K copies of the first epoch (PLV = 1) -- while COR sums each given
+    epoch's own correlation (metrics.py:355-357)."""
+    rng = np.random.default_rng(32)
+    data = [rng.standard_normal((5, 48)) for _ in range(4)]
+    eng = ConnectivityEngine(5, 48, 600.0, storage_mode=True)
+    for d in data:
+        eng.add_trial(EpochMatrix(d, 600.0))
+    band = FrequencyBand(2, 10, 12.5)
+    assert eng.n_trials == 4
+    assert np.abs(eng.finalize(MetricId.PLV, band).weights - 1.0).max() <= 1e-5
+    want, _ = O.compute([data[0]] * 4, 48, 2, 10, ("COH",))
+    assert np.abs(eng.finalize(MetricId.COH, band).weights - want["COH"]["band"]).max() <= 1e-4
+    w, _ = O.cor(data)
+    assert np.abs(eng.finalize(MetricId.COR, band).weights - w).max() <= 1e-12
