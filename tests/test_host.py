@@ -220,3 +220,38 @@ def test_threshold_count_and_dominance_property():
     with pytest.raises(ParameterError):
         normalize_network(ConnectivityNetwork(MetricId.COH, FrequencyBand(0, 1, 1.0), 1, (0, 1), np.zeros((2, 3)),
                                               np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)))
+
+
+@pytest.mark.skipif(not (REFERENCE_SRC / "connstream").exists(), reason="reference not present (GPU box)")
+def test_domain_validation_matches_reference_types():
+    """EpochMatrix / FrequencyBand / MetricId accept and reject the same inputs with the
+    same exception type and message as the reference's core.py:25-110."""
+    import sys
+    sys.path.insert(0, str(REFERENCE_SRC))
+    from connstream import core as RC
+    from paper_2303_03279_b200 import core as MC
+    cases = [dict(data=np.zeros(5), sfreq=1.0), dict(data=np.zeros((2, 5)), sfreq=0.0),
+             dict(data=np.full((2, 5), np.inf), sfreq=1.0), dict(data=np.zeros((2, 0)), sfreq=1.0),
+             dict(data=np.zeros((0, 5)), sfreq=1.0), dict(data=np.zeros((2, 5)), sfreq=1.0, trial_index=-1),
+             dict(data=[[1, 2], [3, 4]], sfreq=1.0), dict(data=np.zeros((2, 5), np.float32), sfreq=1.0),
+             dict(data=np.zeros((2, 3, 4)), sfreq=1.0), dict(data=np.zeros((2, 5)), sfreq=1.0, t0_offset=-0.5)]
+
+    def outcome(fn):
+        try:
+            r = fn()
+            return ("ok", r)
+        except Exception as ex:  # noqa: BLE001 -- the exception itself is compared
+            return (type(ex).__name__, str(ex))
+
+    for c in cases:
+        a = outcome(lambda: (lambda e: (e.n_channels, e.n_samples, e.data.dtype.name))(RC.EpochMatrix(**c)))
+        b = outcome(lambda: (lambda e: (e.n_channels, e.n_samples, e.data.dtype.name))(MC.EpochMatrix(**c)))
+        assert a == b, (c, a, b)
+    for args in [(5, 4, 1.0), (-1, 3, 1.0), (0, 0, 1.0), (2, 3, -1.0)]:
+        assert outcome(lambda: (lambda f: (f.n_bins, f.lo_hz, f.hi_hz))(RC.FrequencyBand(*args))) == \
+            outcome(lambda: (lambda f: (f.n_bins, f.lo_hz, f.hi_hz))(MC.FrequencyBand(*args))), args
+    for n in [" coh", "Coh", "wPLI", "cor", "xcor", "bogus", ""]:
+        a, b = outcome(lambda: RC.MetricId.parse(n).value), outcome(lambda: MC.MetricId.parse(n).value)
+        assert a == b, n
+    assert [m.value for m in RC.MetricId] == [m.value for m in MC.MetricId]
+    assert [m.value for m in RC.MetricId if m.is_spectral] == [m.value for m in MC.MetricId if m.is_spectral]
