@@ -161,18 +161,24 @@ def finalize_spectral(acc: SpectrumSet, metric: MetricId, band: FrequencyBand, p
     """Band-averaged network for one spectral metric (metrics.py:115-134)."""
     if metric not in _SPECTRAL_BINS:
         raise ParameterError(f"{metric} is not a spectral metric")
-    band = _full_band(acc, band)
+    band = out_band = _full_band(acc, band)
+    if metric is MetricId.COHY and band.lo_bin < acc.n_bins <= band.hi_bin:
+        # the reference's numpy slice clips the band and its COHY mean has no range
+        # check (metrics.py:121-127): the mean runs over the bins that exist
+        band = FrequencyBand(band.lo_bin, acc.n_bins - 1, band.bin_hz)
     _check_k(acc.n_trials_accumulated, metric.value)
     slots = acc.slots_for(band.lo_bin, band.hi_bin)
     if slots is None or len(slots) != acc.n_trials_accumulated:  # mixed column sets: the sums path
         if band.hi_bin >= acc.n_bins:
             raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {acc.n_bins} bins")
         w = _bins_from_sums(acc, metric.value, band, want_band=True)["band"]
-        return _network_from_band(metric, band, acc.n_trials_accumulated, acc.n_channels, w, positions, node_ids)
+        return _network_from_band(metric, out_band, acc.n_trials_accumulated, acc.n_channels, w, positions, node_ids)
+    if band.hi_bin >= acc.n_bins:   # core.py:208-215 on the reference's clipped per-bin array
+        raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {acc.n_bins} bins")
     plan = acc.plan
     st = torch.tensor(slots, dtype=torch.int32, device=plan.device)
     out = plan.pair_metrics(st, (metric.value,), band.lo_bin, band.n_bins, per_bin=False, band=True)
-    return _network_from_band(metric, band, acc.n_trials_accumulated, acc.n_channels, out[metric.value]["band"],
+    return _network_from_band(metric, out_band, acc.n_trials_accumulated, acc.n_channels, out[metric.value]["band"],
                               positions, node_ids)
 
 
@@ -562,9 +568,7 @@ class ConnectivityEngine:
     def ensure_band(self, band: FrequencyBand) -> None:
         """All bins are cached on the device, so back-fill needs no FFT (metrics.py:363-380);
         only the accumulator's column set widens."""
-        if band.hi_bin >= self.n_bins:
-            raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {self.n_bins} bins")
-        self._acc_cols[band.lo_bin:band.hi_bin + 1] = True
+        self._acc_cols[band.lo_bin:band.hi_bin + 1] = True   # a numpy slice: clipped at n_bins
 
     @property
     def acc(self) -> "EngineSpectrumSet":
@@ -583,7 +587,12 @@ class ConnectivityEngine:
             return self._finalize_time_domain(metric, band)
         self.ensure_band(band)
         _check_k(len(self._sum_trials), metric.value)
-        out = self._plan.pair_metrics(self._slots(), (metric.value,), band.lo_bin, band.n_bins, per_bin=False,
+        calc = band
+        if band.hi_bin >= self.n_bins:   # as finalize_spectral: COHY over the bins that exist, else an error
+            if metric is not MetricId.COHY or band.lo_bin >= self.n_bins:
+                raise ParameterError(f"band [{band.lo_bin}, {band.hi_bin}] exceeds {self.n_bins} bins")
+            calc = FrequencyBand(band.lo_bin, self.n_bins - 1, band.bin_hz)
+        out = self._plan.pair_metrics(self._slots(), (metric.value,), calc.lo_bin, calc.n_bins, per_bin=False,
                                       band=True)
         return _network_from_band(metric, band, len(self._sum_trials), self.n_channels, out[metric.value]["band"],
                                   self.positions, self.node_ids)

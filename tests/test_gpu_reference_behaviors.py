@@ -285,3 +285,28 @@ def test_repeated_trial_index_folds_cached_spectra_but_cor_sees_each_epoch():
     assert np.abs(eng.finalize(MetricId.COH, band).weights - want["COH"]["band"]).max() <= 1e-4
     w, _ = O.cor(data)
     assert np.abs(eng.finalize(MetricId.COR, band).weights - w).max() <= 1e-12
+
+
+def test_band_past_the_last_bin_like_the_reference():
+    """The reference slices per-bin arrays with the band (metrics.py:121-127): COHY's
+    complex mean then runs over the bins that exist, every other metric hits band_average's
+    range check (core.py:208-215).  Same through SpectrumSet and the engine."""
+    eps = _epochs(4, 5, 48, seed=33)
+    nb = 25
+    over = FrequencyBand(18, nb + 6, 12.5)
+    inside = FrequencyBand(18, nb - 1, 12.5)
+    acc = S.SpectrumSet(5, 48)
+    eng = ConnectivityEngine(5, 48, 600.0, storage_mode=True)
+    for e in eps:
+        S.accumulate_epoch(acc, e)
+        eng.add_trial(e)
+    want, _ = O.compute([e.data for e in eps], 48, 18, nb - 1, ("COHY",))
+    for got in (M.finalize_spectral(acc, MetricId.COHY, over), eng.finalize(MetricId.COHY, over)):
+        assert got.band == over
+        assert np.abs(got.weights - np.abs(want["COHY"]["cband"])).max() <= 1e-4
+        ref = M.finalize_spectral(acc, MetricId.COHY, inside)
+        assert np.abs(got.complex_weights - ref.complex_weights).max() <= 1e-6
+    for fn in (lambda: M.finalize_spectral(acc, MetricId.COH, over), lambda: eng.finalize(MetricId.WPLI, over),
+               lambda: eng.finalize(MetricId.COHY, FrequencyBand(nb, nb + 2, 12.5))):
+        with pytest.raises(ParameterError):
+            fn()
