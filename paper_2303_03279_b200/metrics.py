@@ -13,6 +13,7 @@ Reference anchors: metrics.py:32-98 (*_bins, _SPECTRAL_BINS), :101-134
 """
 from __future__ import annotations
 
+from collections.abc import MutableMapping
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -302,7 +303,8 @@ xcor_pair = timedomain.xcor_pair
 
 @dataclass
 class TrialCache:
-    """Storage mode (metrics.py:267-282): trial_index -> ring slot of its spectra."""
+    """Storage mode (metrics.py:267-282).  In an engine ``spectra`` maps trial_index to
+    the cached spectra (complex128 [C, n_bins], read from the ring slot on access)."""
 
     enabled: bool = True
     spectra: dict = field(default_factory=dict)
@@ -311,6 +313,34 @@ class TrialCache:
 
     def memory_bytes(self) -> int:
         return len(self.spectra) * self.bytes_per_trial
+
+
+class _RingSpectra(MutableMapping):
+    """trial_index -> the spectra the reference caches for it (metrics.py:341-347: the trial
+    spectra, or a welch trial's first segment), kept in the engine's HBM ring and copied
+    to the host only when an entry is read."""
+
+    def __init__(self, engine: "ConnectivityEngine"):
+        self._e = engine
+        self._slots: dict = {}
+
+    def __setitem__(self, idx, slot: int) -> None:
+        self._slots[idx] = slot
+
+    def __getitem__(self, idx):
+        e = self._e
+        slot = e._seg0_of.get(idx, self._slots[idx])
+        sp = e._plan.get_spectra(torch.tensor([slot], dtype=torch.int32, device=e._plan.device))
+        return sp[0].cpu().numpy()
+
+    def __delitem__(self, idx) -> None:
+        del self._slots[idx]
+
+    def __iter__(self):
+        return iter(self._slots)
+
+    def __len__(self) -> int:
+        return len(self._slots)
 
 
 class ConnectivityEngine:
@@ -349,6 +379,7 @@ class ConnectivityEngine:
         self._storage_mode = storage_mode
         self._init_cols()
         self.cache = TrialCache(enabled=storage_mode)
+        self.cache.spectra = _RingSpectra(self)
         self._slot_capacity = max(int(slot_capacity), 1)
         self._plan: DevicePlan | None = None
         self._T = None

@@ -310,3 +310,20 @@ def test_band_past_the_last_bin_like_the_reference():
                lambda: eng.finalize(MetricId.COHY, FrequencyBand(nb, nb + 2, 12.5))):
         with pytest.raises(ParameterError):
             fn()
+
+
+def test_engine_cache_holds_the_reference_cached_spectra():
+    """engine.cache.spectra[idx] is what the reference caches (metrics.py:341-347): the
+    trial's spectra, or a welch trial's first segment; read from the HBM ring on access."""
+    rng = np.random.default_rng(34)
+    fixed = ConnectivityEngine(4, 32, 250.0, storage_mode=True)
+    welch = ConnectivityEngine(4, 32, 250.0, storage_mode=True, spectral_mode="welch")
+    data = [rng.standard_normal((4, T)) for T in (40, 100, 20)]
+    for k, d in enumerate(data):
+        fixed.add_trial(EpochMatrix(d, 250.0, trial_index=k))
+        welch.add_trial(EpochMatrix(d, 250.0, trial_index=k))
+    assert sorted(fixed.cache.spectra) == [0, 1, 2] and len(welch.cache.spectra) == 3
+    for k, d in enumerate(data):
+        assert np.abs(fixed.cache.spectra[k] - O.trial_spectra(d, 32)).max() <= 1e-9
+        first = O.segments(d, 32)[0] if d.shape[1] >= 64 else d
+        assert np.abs(welch.cache.spectra[k] - O.trial_spectra(first, 32)).max() <= 1e-9
