@@ -312,7 +312,9 @@ class TrialCache:
     bytes_per_trial: int = 0
 
     def memory_bytes(self) -> int:
-        return len(self.spectra) * self.bytes_per_trial
+        """Cached spectra (their ring slots) plus the cached epochs' samples, as the
+        reference counts them (metrics.py:279-282)."""
+        return len(self.spectra) * self.bytes_per_trial + sum(int(e.data.nbytes) for e in self.epochs.values())
 
 
 class _RingSpectra(MutableMapping):
